@@ -1,0 +1,337 @@
+#!/usr/bin/env python3
+"""Benchmark: GOTHIC-style octree gravity step on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], the paper's headline case): M31-like model
+N = 2^23 (reference sample_model("m31", N, seed 1), reproduced bit-identically
+by the library's sampler), dacc = 2^-9, eps = 2^-5, leaf 8, group 32.  One
+"step" is one ALL-ACTIVE full block step through the library's Simulation:
+predict -> makeTree (bbox, keys, radix sort, split) -> calcNode -> walkTree
+(all N sinks) -> correct, with the tree rebuilt every step.
+
+  value   seconds per step, state resident in HBM, device time (CUDA events on
+          the library's stream), max over ranks.  Lower is better.
+  e2e     the same step through the public C-ABI with host buffers: pinned
+          positions/velocities uploaded, accelerations read back every step.
+  roofline  walkTree (the dominant kernel) in TFLOP/s by the reference's own
+          convention (27 Flop / interaction, 5 / MAC evaluation) against the
+          FP32 CUDA-core peak (148 SM x 128 lanes x 2 x f_max).
+
+`--impl reference` times the reference's CPU implementation (oracle/_ref) of
+the same step on this host's cores, on a bounded sample (all of makeTree and
+calcNode, a 1/S sample of the sink groups for the walk, scaled by S).
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+EPS = 2.0 ** -5
+DACC = 2.0 ** -9
+PAPER_V100_S_PER_STEP = 3.3e-2  # PAPER.md:18,191 (block-step average, not all-active)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="g2", choices=["g2", "reference"])
+    ap.add_argument("--n", type=int, default=1 << 23)
+    ap.add_argument("--model", default="m31")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="walk 1 of every S groups on the CPU (0: auto)")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, device):
+        self.device, self.rows, self.proc = device, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if len(r) > 3 + k and r[3 + k] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def walk_traffic_per_launch():
+    """dram bytes per walk launch from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "walk_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except OSError:
+        return None
+
+
+# ------------------------------------------------------------------------- CPU reference
+def cpu_reference_step(mass, pos, vel, amag, sample, threads=0):
+    """One all-active step of the reference (oracle/_ref) on a bounded sample:
+    predict (all), build_structure + refresh (all), evaluate on every S-th sink
+    group (exact reference groups: whole 32-particle chunks of the Morton order),
+    correct (all).  Returns (estimated s/step, phase dict)."""
+    from oracle.refpy import Ref
+    ref = Ref()
+    n = len(mass)
+    t0 = time.perf_counter()
+    p2, v2 = ref.predict(pos, vel, np.zeros_like(pos), 0.0)
+    t_pred = time.perf_counter() - t0
+    eng = ref.engine(eps=EPS, dacc=DACC, threads=threads)
+    t0 = time.perf_counter()
+    eng.build(mass, pos, with_nodes=False)
+    t_make = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    eng.refresh(mass, pos)
+    t_calc = time.perf_counter() - t0
+    tree = eng.tree()
+    groups = np.arange(0, (n + 31) // 32, sample)
+    idx = (groups[:, None] * 32 + np.arange(32)[None, :]).ravel()
+    idx = idx[idx < n]
+    targets = tree.perm[idx].astype(np.uint32)
+    t0 = time.perf_counter()
+    _, _, ev = eng.evaluate(mass, pos, amag, targets=targets)
+    t_walk = (time.perf_counter() - t0) * sample
+    t0 = time.perf_counter()
+    ref.correct(vel, np.zeros_like(pos), amag, np.zeros_like(pos), 0.0)
+    t_corr = time.perf_counter() - t0
+    total = t_pred + t_make + t_calc + t_walk + t_corr
+    return total, {"predict": t_pred, "make_tree": t_make, "calc_node": t_calc, "walk_tree_scaled": t_walk,
+                   "correct": t_corr, "walk_sample_events": ev, "groups_walked": int(len(groups))}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle.refpy import Ref
+    ref = Ref()
+    threads = ref.lib.gtref_resolve_threads(0)
+    t0 = time.perf_counter()
+    mass, pos, vel = ref.sample_model(args.model, args.n, 1)
+    t_ic = time.perf_counter() - t0
+    eng = ref.engine(eps=EPS, dacc=DACC, threads=0)
+    t0 = time.perf_counter()
+    _, amag, _ = eng.bootstrap(mass, pos)
+    t_boot = time.perf_counter() - t0
+    del eng
+    sample = args.cpu_sample or max(1, args.n // (1 << 18))
+    for _ in range(args.warmup):
+        cpu_reference_step(mass, pos, vel, amag, sample)
+    times, phases = [], None
+    for _ in range(args.steps):
+        t, phases = cpu_reference_step(mass, pos, vel, amag, sample)
+        times.append(t)
+    v = float(np.mean(times))
+    desc = (f"reference (oracle/_ref) all-active step on {args.model} N={args.n}: predict, makeTree, calcNode "
+            f"and correct on all N; walkTree on 1 of every {sample} sink groups x{sample}; {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": "sec/step (all-active full step)", "value": v, "unit": "s/step",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(args),
+        "cpu_baseline": {"value": v, "unit": "s/step", "cores": int(threads), "kind": "reference", "sample": desc},
+        "e2e": {"value": v, "unit": "s/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "setup_seconds": {"ic": t_ic, "bootstrap": t_boot}, "phases_last_step": phases}))
+
+
+def workload_config(args):
+    return {"workload": f"{args.model} N={args.n} all-active full step (predict+makeTree+calcNode+walkTree+correct, "
+                        f"rebuild every step)", "model": args.model, "n": args.n, "dacc": DACC, "eps": EPS,
+            "leaf_cap": 8, "group_size": 32, "parallelism": f"groups sharded over {dist_env()[1]} GPU(s)",
+            "l2": "no flush: the resident state (~1 GB at 2^23) exceeds the 126 MB L2"}
+
+
+# ------------------------------------------------------------------------- g2 arm
+def run_g2(args):
+    rank, world, local = dist_env()
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1811_02761_b200 as g2
+    from paper_1811_02761_b200.gravitree import lib, sample_model
+
+    mass, pos, vel = sample_model(args.model, args.n, 1)
+    params = g2.GravParams(1.0, EPS, DACC)
+    scheme = g2.StepScheme(eta=0.5, dt_max=1.0 / 16, adaptive=False, fixed_level=0)  # every particle active
+    sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), params, scheme, g2.EngineConfig(), device=local)
+    sim.set_rebuild_every_step(True)
+    if world > 1:
+        import torch.distributed as dist
+        uid = [g2.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sim.set_mesh(rank, world, uid[0])
+    t0 = time.perf_counter()
+    sim.init()
+    t_init = time.perf_counter() - t0
+    import ctypes
+    hs = ctypes.c_void_p()
+    lib().g2_sim_stream(sim._h, ctypes.byref(hs))
+    stream = torch.cuda.ExternalStream(hs.value, device=torch.device("cuda", local))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        sim.step()
+    barrier()
+    lib().g2_launch_count.restype = ctypes.c_ulonglong
+    l0 = lib().g2_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    results = []
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            results.append(sim.step())
+        ev1.record(stream)
+        ev1.synchronize()
+    launches = (lib().g2_launch_count() - l0) / args.steps
+    total_s = ev0.elapsed_time(ev1) / 1e3
+    walk_s = float(np.mean([r.timings.walk_tree for r in results]))
+    per_step = total_s / args.steps
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([per_step, walk_s], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        per_step, walk_s = float(t[0]), float(t[1])
+    r0 = results[-1]
+    flops = g2.walk_flops(r0.events)
+    peaks = measured_peaks()
+    f_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fp32_peak = 148 * 128 * 2 * f_max * 1e6 / 1e12  # TFLOP/s
+    achieved = flops / walk_s / 1e12 if walk_s > 0 else 0.0
+    clocks = clk.summary()
+
+    # e2e: through the public API with host buffers (pinned), copies in the timed region
+    e2e = None
+    if not args.no_e2e:
+        hpos = torch.empty((args.n, 3), dtype=torch.float64, pin_memory=True).numpy()
+        hvel = torch.empty((args.n, 3), dtype=torch.float64, pin_memory=True).numpy()
+        hacc = torch.empty((args.n, 3), dtype=torch.float64, pin_memory=True).numpy()
+        st = sim.system()
+        hpos[:], hvel[:] = st.pos, st.vel
+        hp = hacc.ctypes.data_as(ctypes.c_void_p)
+        barrier()
+        k = max(2, args.steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(k):
+            sim.set_state(hpos, hvel)
+            sim.step()
+            lib().g2_sim_get_state(sim._h, None, None, hp, None, None, None)
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / k
+        if world > 1:
+            import torch.distributed as dist
+            t = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t[0])
+        e2e = {"value": e2e_s, "unit": "s/step", "h2d_bytes_per_step": int(hpos.nbytes + hvel.nbytes),
+               "d2h_bytes_per_step": int(hacc.nbytes),
+               "how": "host wall clock around set_state(pinned pos, vel) + step + get acc, per step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle.refpy import Ref
+            amag = sim.system().acc_old_mag
+            sample = args.cpu_sample or max(1, args.n // (1 << 16))
+            t, ph = cpu_reference_step(mass, pos, vel, amag, sample)
+            cpu = {"value": t, "unit": "s/step", "cores": int(Ref().lib.gtref_resolve_threads(0)), "kind": "reference",
+                   "sample": f"oracle/_ref (unmodified reference library) on the same M31 N={args.n} input: "
+                             f"predict/makeTree/calcNode/correct on all N, walkTree on every {sample}-th sink group "
+                             f"scaled x{sample}", "phases": ph}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "s/step", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        out = {
+            "metric": "sec/step (M31 N=2^23 all-active full step), walkTree TFlop/s", "value": per_step,
+            "unit": "s/step", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": per_step * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32 walk / f64 tree+integrator", "data": "synthetic (reference sample_model m31, seed 1)",
+            "config": workload_config(args),
+            "roofline": {"bound": "fp32", "kernel": "walk_kernel", "achieved": achieved, "peak": fp32_peak,
+                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": walk_traffic_per_launch(),
+                         "peak_note": f"148 SM x 128 FP32 lanes x 2 x {f_max:.0f} MHz (sm_max_mhz of "
+                                      "MEASURED_PEAKS.json); no FP32 peak is measured there",
+                         "flop_per_launch": flops, "walk_seconds": walk_s},
+            "phases_last_step": vars(r0.timings), "events_last_step": vars(r0.events), "active": r0.active,
+            "init_seconds": t_init, "e2e": e2e, "gpu_launches": launches * args.steps,
+            "gpu_launches_per_step": launches, "clocks": clocks, "cpu_baseline": cpu,
+            "paper_v100_s_per_step": PAPER_V100_S_PER_STEP,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_g2(args)
+
+
+if __name__ == "__main__":
+    main()

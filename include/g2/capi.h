@@ -1,0 +1,157 @@
+/* g2 — B200-native GOTHIC-style octree gravity: the drop-in C ABI.
+ *
+ * Plain pointers and sizes only.  Every entry point replaces one member of
+ * the reference C++ operator API (gravitree, /root/reference/proj/core); the
+ * citation next to each declaration names the interface it stands in for.
+ * Array conventions follow gravitree's ParticleSystem (particle_system.hpp:
+ * 14-49): positions/velocities/accelerations are `double[3*n]` xyz
+ * interleaved (a std::vector<Vec3> reinterpreted), masses `double[n]`,
+ * indices in the caller's (original) particle order.  Host buffers in, host
+ * buffers out; all device state stays resident between calls.
+ *
+ * Status codes (errors.hpp:8-23, CLI exit codes main.cpp:30-33):
+ *   G2_OK 0, G2_INTERNAL 1, G2_DATA_ERROR 3, G2_RESOURCE_ERROR 4,
+ *   G2_SINGULARITY 5 (a data_error subclass in the reference).
+ * g2_last_error() returns the thread-local message of the last failure.
+ */
+#ifndef G2_CAPI_H
+#define G2_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { G2_OK = 0, G2_INTERNAL = 1, G2_DATA_ERROR = 3, G2_RESOURCE_ERROR = 4, G2_SINGULARITY = 5 };
+
+/* GravParams (particle_system.hpp:53-57) */
+typedef struct {
+    double G, eps, dacc;
+} g2_grav_params;
+
+/* EngineConfig (engine.hpp:14-23).  group_size must be 1..32 (one warp per
+ * group; larger is rejected with G2_DATA_ERROR); list_capacity only has to be
+ * >= 1 (results do not depend on it, test_gravity.cpp:213-229); frontier_cap
+ * (0 = 8n) is honoured as the error contract of traversal.cpp:145-146;
+ * threads is ignored on the device. */
+typedef struct {
+    size_t leaf_cap, group_size, list_capacity, frontier_cap;
+    int count_ops;
+    double bootstrap_theta;
+    size_t bootstrap_direct_limit;
+    unsigned threads;
+} g2_engine_config;
+
+/* TraversalEvents (op_counters.hpp:33-46) */
+typedef struct {
+    uint64_t interactions, mac_evals, list_pushes;
+} g2_events;
+
+/* StepScheme (integrator.hpp:18-23) and TunerConfig (rebuild_tuner.hpp:9-13) */
+typedef struct {
+    double eta, dt_max;
+    int adaptive, fixed_level;
+} g2_step_scheme;
+typedef struct {
+    size_t min_interval, max_interval, initial_interval;
+} g2_tuner_config;
+
+/* StepResult (integrator.hpp:43-50) with PhaseTimings (phase_timings.hpp:6-23);
+ * phase times are device (CUDA-event) seconds, wall_seconds is host wall time. */
+typedef struct {
+    double walk_tree, calc_node, make_tree, predict, correct;
+    g2_events events;
+    size_t active, rebuild_interval;
+    int rebuilt;
+    double wall_seconds;
+} g2_step_result;
+
+typedef struct g2_engine g2_engine;
+typedef struct g2_sim g2_sim;
+
+const char* g2_last_error(void);
+void g2_default_params(g2_grav_params* p);          /* GravParams{} */
+void g2_default_engine_config(g2_engine_config* c); /* EngineConfig{} */
+void g2_default_step_scheme(g2_step_scheme* s);     /* StepScheme{} */
+void g2_default_tuner_config(g2_tuner_config* t);   /* TunerConfig{} */
+
+/* ---- GravityEngine (engine.hpp:29-66, engine.cpp:13-103) ---------------- */
+/* GravityEngine(GravParams, EngineConfig)  engine.cpp:13-18 */
+int g2_engine_create(const g2_grav_params* p, const g2_engine_config* c, int device, g2_engine** out);
+void g2_engine_destroy(g2_engine* e);
+/* build / build_structure / refresh   engine.cpp:20-29 */
+int g2_engine_build(g2_engine* e, size_t n, const double* mass, const double* pos);
+int g2_engine_build_structure(g2_engine* e, size_t n, const double* mass, const double* pos);
+int g2_engine_refresh(g2_engine* e, size_t n, const double* mass, const double* pos);
+int g2_engine_has_tree(const g2_engine* e);
+/* evaluate(system, targets, pot_out)  engine.cpp:31-81.  targets == NULL:
+ * all particles (engine.cpp:83-87).  acc_inout[3n] / pot_out[n] (nullable)
+ * are written for the targets only, like system.acc / pot_out. */
+int g2_engine_evaluate(g2_engine* e, size_t n, const double* mass, const double* pos, const double* acc_old_mag,
+                       size_t n_targets, const uint32_t* targets, double* acc_inout, double* pot_out,
+                       g2_events* events);
+/* bootstrap(system)  engine.cpp:89-103: fills acc[3n] and acc_old_mag[n]
+ * (acc_old_mag is read first: all-zero selects the geometric MAC). */
+int g2_engine_bootstrap(g2_engine* e, size_t n, const double* mass, const double* pos, double* acc_out,
+                        double* acc_old_mag_inout, g2_events* events);
+/* tree() accessors (octree.hpp:32-42): sizes, then flat copies.
+ * cells4 = {first_child, child_count, first, count} per cell, nodes5 =
+ * {mass, com.x, com.y, com.z, extent}; any pointer may be NULL. */
+int g2_engine_tree_size(const g2_engine* e, size_t* n, size_t* ncells);
+int g2_engine_get_tree(g2_engine* e, double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* rank,
+                       uint32_t* cells4, uint8_t* depth, double* nodes5);
+/* params().dacc setter (engine.hpp:40 exposes a mutable params()) */
+int g2_engine_set_params(g2_engine* e, const g2_grav_params* p);
+
+/* ---- free functions -------------------------------------------------------- */
+/* direct_sum (gravity.cpp:18-43), on the device, FP64, bit-identical order */
+int g2_direct_sum(size_t n, const double* mass, const double* pos, double G, double eps, int device, double* acc_out);
+/* block_level (integrator.cpp:21-33) evaluated by the device kernel */
+int g2_block_level(size_t n, const double* acc_mag, const g2_step_scheme* s, double eps, int device, int* levels);
+/* predict (integrator.cpp:40-45) on the device; pos/vel updated in place */
+int g2_predict(size_t n, double* pos, double* vel, const double* acc, double dt, int device);
+
+/* ---- Simulation (integrator.hpp:54-91, integrator.cpp:56-164) ------------- */
+int g2_sim_create(size_t n, const double* mass, const double* pos, const double* vel, const g2_grav_params* p,
+                  const g2_step_scheme* s, const g2_engine_config* c, const g2_tuner_config* t, int device,
+                  g2_sim** out);
+void g2_sim_destroy(g2_sim* s);
+int g2_sim_init(g2_sim* s);
+int g2_sim_step(g2_sim* s, g2_step_result* r);
+int g2_sim_set_fixed_rebuild_interval(g2_sim* s, size_t interval);
+/* state in original particle order; any pointer may be NULL */
+int g2_sim_get_state(g2_sim* s, double* pos, double* vel, double* acc, double* acc_old_mag, uint8_t* level,
+                     double* time);
+/* overwrite positions / velocities (original order) of the device-resident state */
+int g2_sim_set_state(g2_sim* s, const double* pos, const double* vel);
+/* extension: rebuild the tree every step (the all-active "full step" benchmark) */
+int g2_sim_set_rebuild_every_step(g2_sim* s, int on);
+int g2_sim_tuner_interval(g2_sim* s, size_t* interval);
+
+/* the CUDA stream (cudaStream_t) all of the simulation's work is issued on,
+ * so callers can time it with their own events */
+int g2_sim_stream(g2_sim* s, void** stream);
+/* kernels launched by this library since load (benchmark evidence) */
+unsigned long long g2_launch_count(void);
+/* autotune_rebuild (rebuild_tuner.cpp:28-61) on a walk-time history: host logic */
+size_t g2_autotune(double build_time, size_t n_hist, const double* hist, size_t min_interval, size_t max_interval,
+                   size_t current_interval);
+/* sample_model (models.cpp:442-460), bit-identical to the reference, multithreaded
+ * (threads 0 = all cores); returns 0 or G2_DATA_ERROR (message: g2_ics_last_error) */
+int g2_sample_model(const char* name, size_t n, uint64_t seed, unsigned threads, double* mass, double* pos,
+                    double* vel);
+const char* g2_ics_last_error(void);
+
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) --------------------- */
+/* NCCL unique id (128 bytes) for rank 0 to broadcast out of band */
+int g2_nccl_unique_id(unsigned char id[128]);
+/* join a communicator; the simulation then walks only its shard of sink
+ * groups and all-gathers the new accelerations each step */
+int g2_sim_set_mesh(g2_sim* s, int rank, int world, const unsigned char id[128]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* G2_CAPI_H */

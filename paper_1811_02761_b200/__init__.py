@@ -1,0 +1,15 @@
+"""g2: a B200-native (sm_100a) GOTHIC-style octree gravity step.
+
+Drop-in for the gravitree hot path (Morton keys + radix sort, makeTree,
+calcNode, walkTree, block-step predict/correct) behind the C-ABI in
+include/g2/capi.h; ``gravitree`` is the Python mirror of the reference API.
+"""
+from .gravitree import (DataError, EngineConfig, GravityEngine, GravParams, InternalError, ParticleSystem,
+                        ResourceError, Simulation, SingularityError, StepResult, StepScheme, TraversalEvents,
+                        TunerConfig, block_level, count_walk_ops, direct_sum, flops_estimate, force_error,
+                        nccl_unique_id, predict, walk_flops)
+
+__all__ = ["DataError", "EngineConfig", "GravityEngine", "GravParams", "InternalError", "ParticleSystem",
+           "ResourceError", "Simulation", "SingularityError", "StepResult", "StepScheme", "TraversalEvents",
+           "TunerConfig", "block_level", "count_walk_ops", "direct_sum", "flops_estimate", "force_error",
+           "nccl_unique_id", "predict", "walk_flops"]

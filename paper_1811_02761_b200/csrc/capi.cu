@@ -1,0 +1,344 @@
+// extern "C" boundary (include/g2/capi.h): exceptions -> status codes, plus the
+// NCCL all-gather exchange for sharded multi-GPU steps.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/g2/capi.h"
+#include "engine.cuh"
+
+struct g2_engine {
+    std::unique_ptr<g2::Engine> e;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return G2_OK;
+    } catch (const g2::Error& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return G2_INTERNAL;
+    }
+}
+
+g2::GravParamsH to_h(const g2_grav_params* p) {
+    g2::GravParamsH h;
+    if (p) h.G = p->G, h.eps = p->eps, h.dacc = p->dacc;
+    return h;
+}
+g2::EngineConfigH to_h(const g2_engine_config* c) {
+    g2::EngineConfigH h;
+    if (c) {
+        h.leaf_cap = c->leaf_cap, h.group_size = c->group_size, h.list_capacity = c->list_capacity;
+        h.frontier_cap = c->frontier_cap, h.count_ops = c->count_ops != 0, h.bootstrap_theta = c->bootstrap_theta;
+        h.bootstrap_direct_limit = c->bootstrap_direct_limit, h.threads = c->threads;
+    }
+    return h;
+}
+g2::StepSchemeH to_h(const g2_step_scheme* s) {
+    g2::StepSchemeH h;
+    if (s) h.eta = s->eta, h.dt_max = s->dt_max, h.adaptive = s->adaptive != 0, h.fixed_level = s->fixed_level;
+    return h;
+}
+g2::TunerConfigH to_h(const g2_tuner_config* t) {
+    g2::TunerConfigH h;
+    if (t) h.min_interval = t->min_interval, h.max_interval = t->max_interval, h.initial_interval = t->initial_interval;
+    return h;
+}
+void put(const g2::EventsH& e, g2_events* o) {
+    if (o) o->interactions = e.interactions, o->mac_evals = e.mac_evals, o->list_pushes = e.list_pushes;
+}
+
+// ---- NCCL, loaded lazily so the library has no hard dependency on it --------------
+struct Nccl {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+    bool ok = false;
+    Nccl() {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        get_unique_id = reinterpret_cast<decltype(get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        all_gather = reinterpret_cast<decltype(all_gather)>(dlsym(h, "ncclAllGather"));
+        comm_destroy = reinterpret_cast<decltype(comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        error_string = reinterpret_cast<decltype(error_string)>(dlsym(h, "ncclGetErrorString"));
+        ok = get_unique_id && comm_init_rank && all_gather && comm_destroy && error_string;
+    }
+};
+Nccl& nccl() {
+    static Nccl n;
+    if (!n.ok) throw g2::Error(G2_INTERNAL, "NCCL (libnccl.so.2) not loadable");
+    return n;
+}
+#define G2_NCCL(expr)                                                                                \
+    do {                                                                                             \
+        ncclResult_t _r = (expr);                                                                    \
+        if (_r != ncclSuccess) throw g2::Error(G2_INTERNAL, std::string("NCCL: ") + nccl().error_string(_r)); \
+    } while (0)
+
+__global__ void unpack_kernel(const float4* __restrict__ gathered, float4* __restrict__ accum,
+                              const uint32_t* n_active, uint32_t gs, uint32_t world, uint32_t per_rank) {
+    const uint32_t na = *n_active;
+    const uint32_t ng = (na + gs - 1) / gs;
+    for (uint32_t r = 0; r < world; ++r) {
+        const uint32_t lo = uint32_t(uint64_t(ng) * r / world) * gs;
+        const uint32_t hi = min(uint32_t(uint64_t(ng) * (r + 1) / world) * gs, na);
+        for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; lo + j < hi; j += gridDim.x * blockDim.x)
+            accum[lo + j] = gathered[size_t(r) * per_rank + j];
+    }
+}
+
+// One ncclAllGather of the walk's FP32 accumulator slots per step:
+// rank r owns slots [lo_r*gs, hi_r*gs); each sends a fixed-size window so the
+// collective has equal counts, then every rank scatters the windows back.
+struct NcclExchange final : g2::Exchange {
+    ncclComm_t comm = nullptr;
+    int world = 1;
+    g2::DBuf<float4> gathered;
+    ~NcclExchange() override {
+        if (comm) nccl().comm_destroy(comm);
+    }
+    void allgather_acc(g2::Simulation& sim) override {
+        auto& eng = sim.engine();
+        cudaStream_t s = eng.stream();
+        const uint32_t gs = uint32_t(sim.group_size());
+        const size_t n = sim.n();
+        const size_t ng_max = (n + gs - 1) / gs;
+        const size_t per_rank = ((ng_max + world - 1) / world) * gs;  // slots per rank window
+        eng.reserve_accum(size_t(sim.shard_lo()) * gs + per_rank + n);
+        gathered.reserve(per_rank * world);
+        float4* send = eng.accum() + size_t(sim.shard_lo()) * gs;
+        G2_NCCL(nccl().all_gather(send, gathered.p, per_rank * 4, ncclFloat32, comm, s));
+        G2_COUNT(1), unpack_kernel<<<256, 256, 0, s>>>(gathered.p, eng.accum(), sim.n_active_dev(), gs, uint32_t(world),
+                                          uint32_t(per_rank));
+    }
+};
+
+}  // namespace
+
+struct g2_sim {
+    std::unique_ptr<g2::Simulation> s;
+    std::unique_ptr<NcclExchange> ex;
+};
+
+
+extern "C" {
+
+const char* g2_last_error(void) { return g_err.c_str(); }
+
+void g2_default_params(g2_grav_params* p) {
+    g2::GravParamsH h;
+    p->G = h.G, p->eps = h.eps, p->dacc = h.dacc;
+}
+void g2_default_engine_config(g2_engine_config* c) {
+    g2::EngineConfigH h;
+    c->leaf_cap = h.leaf_cap, c->group_size = h.group_size, c->list_capacity = h.list_capacity;
+    c->frontier_cap = h.frontier_cap, c->count_ops = h.count_ops, c->bootstrap_theta = h.bootstrap_theta;
+    c->bootstrap_direct_limit = h.bootstrap_direct_limit, c->threads = h.threads;
+}
+void g2_default_step_scheme(g2_step_scheme* s) {
+    g2::StepSchemeH h;
+    s->eta = h.eta, s->dt_max = h.dt_max, s->adaptive = h.adaptive, s->fixed_level = h.fixed_level;
+}
+void g2_default_tuner_config(g2_tuner_config* t) {
+    g2::TunerConfigH h;
+    t->min_interval = h.min_interval, t->max_interval = h.max_interval, t->initial_interval = h.initial_interval;
+}
+
+int g2_engine_create(const g2_grav_params* p, const g2_engine_config* c, int device, g2_engine** out) {
+    return guarded([&] {
+        auto* h = new g2_engine;
+        try {
+            h->e = std::make_unique<g2::Engine>(to_h(p), to_h(c), device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+void g2_engine_destroy(g2_engine* e) { delete e; }
+int g2_engine_build(g2_engine* e, size_t n, const double* mass, const double* pos) {
+    return guarded([&] { e->e->build(n, mass, pos, true); });
+}
+int g2_engine_build_structure(g2_engine* e, size_t n, const double* mass, const double* pos) {
+    return guarded([&] { e->e->build(n, mass, pos, false); });
+}
+int g2_engine_refresh(g2_engine* e, size_t n, const double* mass, const double* pos) {
+    return guarded([&] { e->e->refresh(n, mass, pos); });
+}
+int g2_engine_has_tree(const g2_engine* e) { return e->e->has_tree() ? 1 : 0; }
+int g2_engine_evaluate(g2_engine* e, size_t n, const double* mass, const double* pos, const double* acc_old_mag,
+                       size_t n_targets, const uint32_t* targets, double* acc_inout, double* pot_out,
+                       g2_events* events) {
+    return guarded([&] {
+        put(e->e->evaluate(n, mass, pos, acc_old_mag, n_targets, targets, acc_inout, pot_out), events);
+    });
+}
+int g2_engine_bootstrap(g2_engine* e, size_t n, const double* mass, const double* pos, double* acc_out,
+                        double* acc_old_mag_inout, g2_events* events) {
+    return guarded([&] { put(e->e->bootstrap(n, mass, pos, acc_out, acc_old_mag_inout), events); });
+}
+int g2_engine_tree_size(const g2_engine* e, size_t* n, size_t* ncells) {
+    return guarded([&] {
+        if (n) *n = e->e->n();
+        if (ncells) *ncells = e->e->ncells();
+    });
+}
+int g2_engine_get_tree(g2_engine* e, double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* rank,
+                       uint32_t* cells4, uint8_t* depth, double* nodes5) {
+    return guarded([&] { e->e->get_tree(bbox4, keys, perm, rank, cells4, depth, nodes5); });
+}
+int g2_engine_set_params(g2_engine* e, const g2_grav_params* p) {
+    return guarded([&] {
+        if (!(p->dacc > 0.0)) throw g2::Error(G2_DATA_ERROR, "GravityEngine: dacc must be positive");
+        if (p->eps < 0.0) throw g2::Error(G2_DATA_ERROR, "GravityEngine: eps must be non-negative");
+        e->e->params() = to_h(p);
+    });
+}
+
+int g2_direct_sum(size_t n, const double* mass, const double* pos, double G, double eps, int device,
+                  double* acc_out) {
+    return guarded([&] {
+        g2::GravParamsH p;
+        p.G = G, p.eps = eps;
+        g2::EngineConfigH c;
+        c.bootstrap_direct_limit = ~size_t(0);
+        g2::Engine eng(p, c, device);
+        std::unique_ptr<double[]> amag(new double[n ? n : 1]());
+        eng.bootstrap(n, mass, pos, acc_out, amag.get());
+    });
+}
+
+int g2_block_level(size_t n, const double* acc_mag, const g2_step_scheme* s, double eps, int device, int* levels) {
+    return guarded([&] {
+        G2_CUDA(cudaSetDevice(device));
+        g2::DBuf<double> a;
+        g2::DBuf<int> l;
+        a.reserve(n ? n : 1), l.reserve(n ? n : 1);
+        G2_CUDA(cudaMemcpy(a.p, acc_mag, n * 8, cudaMemcpyHostToDevice));
+        const g2::StepSchemeH h = to_h(s);
+        g2::launch_block_levels(a.p, n, g2::SchemeDev{h.eta, h.dt_max, eps, h.adaptive ? 1 : 0, h.fixed_level}, l.p,
+                                nullptr);
+        G2_CUDA(cudaMemcpy(levels, l.p, n * sizeof(int), cudaMemcpyDeviceToHost));
+    });
+}
+
+int g2_predict(size_t n, double* pos, double* vel, const double* acc, double dt, int device) {
+    return guarded([&] {
+        G2_CUDA(cudaSetDevice(device));
+        g2::DBuf<double> p, v, a;
+        p.reserve(3 * n + 3), v.reserve(3 * n + 3), a.reserve(3 * n + 3);
+        G2_CUDA(cudaMemcpy(p.p, pos, 3 * n * 8, cudaMemcpyHostToDevice));
+        G2_CUDA(cudaMemcpy(v.p, vel, 3 * n * 8, cudaMemcpyHostToDevice));
+        G2_CUDA(cudaMemcpy(a.p, acc, 3 * n * 8, cudaMemcpyHostToDevice));
+        g2::launch_predict_aos(p.p, v.p, a.p, n, dt, nullptr);
+        G2_CUDA(cudaMemcpy(pos, p.p, 3 * n * 8, cudaMemcpyDeviceToHost));
+        G2_CUDA(cudaMemcpy(vel, v.p, 3 * n * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+int g2_sim_create(size_t n, const double* mass, const double* pos, const double* vel, const g2_grav_params* p,
+                  const g2_step_scheme* s, const g2_engine_config* c, const g2_tuner_config* t, int device,
+                  g2_sim** out) {
+    return guarded([&] {
+        auto* h = new g2_sim;
+        try {
+            h->s = std::make_unique<g2::Simulation>(n, mass, pos, vel, to_h(p), to_h(s), to_h(c), to_h(t), device);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+void g2_sim_destroy(g2_sim* s) { delete s; }
+int g2_sim_init(g2_sim* s) {
+    return guarded([&] { s->s->init(); });
+}
+int g2_sim_step(g2_sim* s, g2_step_result* r) {
+    return guarded([&] {
+        const g2::StepResultH x = s->s->step();
+        if (!r) return;
+        r->walk_tree = x.timings.walk_tree, r->calc_node = x.timings.calc_node, r->make_tree = x.timings.make_tree;
+        r->predict = x.timings.predict, r->correct = x.timings.correct;
+        put(x.events, &r->events);
+        r->active = x.active, r->rebuild_interval = x.rebuild_interval, r->rebuilt = x.rebuilt ? 1 : 0;
+        r->wall_seconds = x.wall_seconds;
+    });
+}
+int g2_sim_set_fixed_rebuild_interval(g2_sim* s, size_t interval) {
+    return guarded([&] { s->s->set_fixed_rebuild_interval(interval); });
+}
+int g2_sim_get_state(g2_sim* s, double* pos, double* vel, double* acc, double* acc_old_mag, uint8_t* level,
+                     double* time) {
+    return guarded([&] { s->s->get_state(pos, vel, acc, acc_old_mag, level, time); });
+}
+int g2_sim_set_state(g2_sim* s, const double* pos, const double* vel) {
+    return guarded([&] { s->s->set_state(pos, vel); });
+}
+int g2_sim_set_rebuild_every_step(g2_sim* s, int on) {
+    return guarded([&] { s->s->set_rebuild_every_step(on != 0); });
+}
+int g2_sim_tuner_interval(g2_sim* s, size_t* interval) {
+    return guarded([&] { *interval = s->s->tuner().interval(); });
+}
+
+int g2_sim_stream(g2_sim* s, void** stream) {
+    return guarded([&] { *stream = reinterpret_cast<void*>(s->s->engine().stream()); });
+}
+unsigned long long g2_launch_count(void) { return g2::launch_counter().load(); }
+size_t g2_autotune(double build_time, size_t n_hist, const double* hist, size_t min_interval, size_t max_interval,
+                   size_t current_interval) {
+    try {
+        g2::RebuildTuner t(g2::TunerConfigH{min_interval, max_interval, current_interval});
+        t.record_build(build_time);
+        for (size_t k = 0; k < n_hist; ++k) t.record_walk(hist[k]);
+        return t.autotune();
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 0;
+    }
+}
+
+int g2_nccl_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        ncclUniqueId u;
+        G2_NCCL(nccl().get_unique_id(&u));
+        static_assert(sizeof(u) == 128, "ncclUniqueId size");
+        std::memcpy(id, &u, 128);
+    });
+}
+int g2_sim_set_mesh(g2_sim* s, int rank, int world, const unsigned char id[128]) {
+    return guarded([&] {
+        if (world < 1 || rank < 0 || rank >= world) throw g2::Error(G2_DATA_ERROR, "set_mesh: bad rank/world");
+        if (world == 1) {
+            s->s->set_shard(0, 1, nullptr);
+            return;
+        }
+        auto ex = std::make_unique<NcclExchange>();
+        ncclUniqueId u;
+        std::memcpy(&u, id, 128);
+        G2_NCCL(nccl().comm_init_rank(&ex->comm, world, u, rank));
+        ex->world = world;
+        s->s->set_shard(rank, world, ex.get());
+        s->ex = std::move(ex);
+    });
+}
+
+}  // extern "C"

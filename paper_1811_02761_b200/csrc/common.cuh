@@ -1,0 +1,156 @@
+// Shared device/host definitions for the g2 octree-gravity engine (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+
+namespace g2 {
+
+// ---- status codes (mirror gravitree/errors.hpp:8-23 + main.cpp:30-33) ---------
+enum Status : int { kOk = 0, kInternal = 1, kDataError = 3, kResourceError = 4, kSingularity = 5 };
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define G2_CUDA(expr)                                                                                  \
+    do {                                                                                               \
+        cudaError_t _e = (expr);                                                                       \
+        if (_e != cudaSuccess)                                                                         \
+            throw ::g2::Error(::g2::kInternal, std::string("CUDA: ") + cudaGetErrorString(_e) + " at " \
+                                                   + __FILE__ + ":" + std::to_string(__LINE__));       \
+    } while (0)
+
+// Device-side error flags, read back at API boundaries.
+struct DevFlags {
+    int data_error;       // non-finite position / position outside root cube (morton.hpp:39, octree.cpp:31)
+    int resource_error;   // frontier cap exceeded (traversal.cpp:145-146)
+    int singularity;      // eps == 0 coincident pair in direct_sum (gravity.cpp:32-33)
+    int cell_overflow;    // cell buffer too small: host grows it and rebuilds
+    int stack_overflow;   // walk stack spill area exhausted (internal, sized to never trigger)
+    int queue_overflow;   // walk task queue exhausted (internal)
+    int pad[2];
+};
+
+constexpr int kMaxDepth = 21;        // octree.hpp:47
+constexpr int kMortonBits = 21;      // morton.hpp:9
+constexpr int kMaxBlockLevel = 24;   // integrator.hpp:14
+constexpr int kNumSMs = 148;
+
+// Walk-ready node record: FP64 monopole (calc_node output, octree.hpp:26-30)
+// plus the topology link the traversal needs, 48 B, 16-B aligned.
+//   internal: link = first_child, info = child_count
+//   leaf:     link = first particle (sorted index), info = count | kLeafBit
+struct alignas(16) WNode {
+    double cx, cy, cz, mass, extent;
+    uint32_t link, info;
+};
+constexpr uint32_t kLeafBit = 0x80000000u;
+
+// ---- exact FP64 helpers: explicit _rn intrinsics are never contracted into FMA,
+// so device results match the reference's x86-64 SSE2 arithmetic bit for bit.
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ double dsqrt(double a) { return __dsqrt_rn(a); }
+// std::min / std::max argument conventions (matter only for signed zeros).
+__device__ __forceinline__ double smin(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double smax(double a, double b) { return a < b ? b : a; }
+__device__ __forceinline__ double norm2(double x, double y, double z) {
+    return dadd(dadd(dmul(x, x), dmul(y, y)), dmul(z, z));
+}
+
+// Host-side count of kernel launches issued by the library (bench evidence).
+inline std::atomic<unsigned long long>& launch_counter() {
+    static std::atomic<unsigned long long> c{0};
+    return c;
+}
+#define G2_COUNT(k) (::g2::launch_counter() += (k))
+
+inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
+
+// Grow-only device buffer.
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        if (n == 0) return;
+        G2_CUDA(cudaMalloc(&p, n * sizeof(T)));
+        cap = n;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    operator T*() const { return p; }
+};
+
+// ---- single-pass decoupled look-back scan (shared by split, compaction, sort) ----
+// Status word per tile: bits 62-63 flag (1 = aggregate, 2 = inclusive prefix),
+// bits 0-61 value.  One 64-bit word carries flag and value together, so a
+// relaxed store/load pair is enough for correctness.
+constexpr uint64_t kLbAgg = 1ull << 62;
+constexpr uint64_t kLbInc = 2ull << 62;
+constexpr uint64_t kLbMask = (1ull << 62) - 1;
+
+__device__ __forceinline__ void lb_store(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t lb_load(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Called by ONE full warp of the tile.  Publishes `aggregate` for tile `tile`
+// and returns the exclusive prefix of all earlier tiles (same on all lanes).
+__device__ __forceinline__ uint64_t lookback_warp(uint64_t* status, uint32_t tile, uint64_t aggregate) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) lb_store(&status[0], kLbInc | aggregate);
+        return 0;
+    }
+    if (lane == 0) lb_store(&status[tile], kLbAgg | aggregate);
+    uint64_t excl = 0;
+    int64_t base = static_cast<int64_t>(tile) - 1;  // lane l inspects tile base - l
+    while (true) {
+        const int64_t t = base - lane;
+        uint64_t s = t >= 0 ? lb_load(&status[t]) : kLbInc;  // virtual inclusive 0 before tile 0
+        // wait until every inspected predecessor has published something
+        while (__any_sync(0xffffffffu, (s >> 62) == 0)) {
+            if ((s >> 62) == 0) s = lb_load(&status[t]);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, (s >> 62) == 2);
+        // lanes up to and including the first inclusive one contribute
+        const int stop = inc ? __ffs(inc) - 1 : 31;
+        uint64_t v = lane <= stop ? (s & kLbMask) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        excl += v;
+        if (inc) break;
+        base -= 32;
+    }
+    if (lane == 0) lb_store(&status[tile], kLbInc | (excl + aggregate));
+    return excl;
+}
+
+}  // namespace g2

@@ -1,0 +1,657 @@
+// Host implementation of Engine / Simulation / RebuildTuner (see engine.cuh).
+#include "engine.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+namespace g2 {
+namespace {
+
+constexpr int kB = 256;
+inline unsigned gridn(size_t n) { return std::max(1u, std::min<unsigned>(ceil_div(n, kB), kNumSMs * 16)); }
+
+// AoS xyz (3n) [+ gather by src] -> SoA
+__global__ void deinterleave_kernel(const double* __restrict__ v3, const uint32_t* __restrict__ src, double* x,
+                                    double* y, double* z, size_t n) {
+    for (size_t i = blockIdx.x * size_t(kB) + threadIdx.x; i < n; i += size_t(gridDim.x) * kB) {
+        const size_t j = src ? src[i] : i;
+        x[i] = v3[3 * j], y[i] = v3[3 * j + 1], z[i] = v3[3 * j + 2];
+    }
+}
+// out3[3*j] = x[idx[j]]...  (idx nullable => identity)
+__global__ void interleave_kernel(const double* __restrict__ x, const double* __restrict__ y,
+                                  const double* __restrict__ z, const uint32_t* __restrict__ idx, double* out3,
+                                  size_t n) {
+    for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < n; j += size_t(gridDim.x) * kB) {
+        const size_t k = idx ? idx[j] : j;
+        out3[3 * j] = x[k], out3[3 * j + 1] = y[k], out3[3 * j + 2] = z[k];
+    }
+}
+__global__ void gather_scalar_kernel(const double* __restrict__ in, const uint32_t* __restrict__ idx, double* out,
+                                     size_t n) {
+    for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < n; j += size_t(gridDim.x) * kB)
+        out[j] = in[idx ? idx[j] : j];
+}
+__global__ void xyzm_to_pos3_kernel(const double4* __restrict__ xyzm, double* pos3, size_t n) {
+    for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < n; j += size_t(gridDim.x) * kB) {
+        const double4 q = xyzm[j];
+        pos3[3 * j] = q.x, pos3[3 * j + 1] = q.y, pos3[3 * j + 2] = q.z;
+    }
+}
+// positions (orig order, 3n) written into sorted state through rank
+__global__ void set_pos_kernel(double4* xyzm, const double* __restrict__ pos3, const uint32_t* __restrict__ ids,
+                               size_t n) {
+    for (size_t k = blockIdx.x * size_t(kB) + threadIdx.x; k < n; k += size_t(gridDim.x) * kB) {
+        const size_t id = ids[k];
+        double4 q = xyzm[k];
+        q.x = pos3[3 * id], q.y = pos3[3 * id + 1], q.z = pos3[3 * id + 2];
+        xyzm[k] = q;
+    }
+}
+__global__ void fill_u8_kernel(uint8_t* p, uint8_t v, size_t n) {
+    for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < n; j += size_t(gridDim.x) * kB) p[j] = v;
+}
+__global__ void frontier_check_kernel(const uint32_t* __restrict__ cnt, size_t m, uint32_t cap, DevFlags* flags) {
+    for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < m; j += size_t(gridDim.x) * kB)
+        if (cnt[j] > cap) flags->resource_error = 1;
+}
+
+double seconds(std::chrono::steady_clock::time_point t0) {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+// =============================================================================================
+Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), device_(device) {
+    if (c_.group_size < 1) throw Error(kDataError, "GravityEngine: group_size must be >= 1");
+    if (!(p_.dacc > 0.0)) throw Error(kDataError, "GravityEngine: dacc must be positive");
+    if (p_.eps < 0.0) throw Error(kDataError, "GravityEngine: eps must be non-negative");
+    if (c_.group_size > 32)
+        throw Error(kDataError, "GravityEngine: group_size > 32 is not supported by the warp-per-group walk");
+    G2_CUDA(cudaSetDevice(device_));
+    G2_CUDA(cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking));
+    flags_.reserve(1);
+    G2_CUDA(cudaMemsetAsync(flags_.p, 0, sizeof(DevFlags), s_));
+    level_start_.reserve(kMaxDepth + 3);
+    tile_counters_.reserve(kMaxDepth + 1);
+    cube_.reserve(1);
+    bbox_part_.reserve(6 * kNumSMs * 4);
+    n_sinks_.reserve(1);
+    n_groups_.reserve(1);
+    events_.reserve(3);
+    qstate_.reserve(4);
+    queue_cap_ = 1u << 22;
+    queue_.reserve(queue_cap_);
+    G2_CUDA(cudaMemsetAsync(queue_.p, 0xff, size_t(queue_cap_) * sizeof(uint64_t), s_));
+    spill_.reserve(walk_resident_warps() * walk_spill_words());
+}
+
+Engine::~Engine() {
+    if (s_) {
+        cudaStreamSynchronize(s_);
+        cudaStreamDestroy(s_);
+    }
+}
+
+void Engine::reserve(size_t n) {
+    if (n <= cap_) return;
+    pos3_.reserve(3 * n), mass_.reserve(n), amag_o_.reserve(n);
+    xyzm_o_.reserve(n), xyzm_s_.reserve(n), xyzm_alt_.reserve(n);
+    keys_a_.reserve(n), keys_b_.reserve(n);
+    vals_a_.reserve(n), vals_b_.reserve(n), perm_.reserve(n), rank_.reserve(n), src_.reserve(n),
+        tgt_rank_.reserve(n);
+    amag_s_.reserve(n), ax_s_.reserve(n), ay_s_.reserve(n), az_s_.reserve(n), pot_s_.reserve(n), out_.reserve(3 * n);
+    sinks_.reserve(n), sinks_alt_.reserve(n);
+    groups_.reserve(n), accum_.reserve(n), group_inter_.reserve(n);
+    ensure_cells(std::max<size_t>(n + 64, 1024));
+    cap_ = n;
+}
+
+void Engine::ensure_cells(size_t cap) {
+    if (cap <= cell_cap_) return;
+    first_child_.reserve(cap), child_count_.reserve(cap), first_.reserve(cap), count_.reserve(cap);
+    depth_.reserve(cap), nodes_.reserve(cap);
+    split_status_.reserve(cap / 32 + 64);
+    cell_cap_ = cap;
+}
+
+void Engine::check_flags() {
+    G2_CUDA(cudaStreamSynchronize(s_));
+    DevFlags f;
+    G2_CUDA(cudaMemcpy(&f, flags_.p, sizeof f, cudaMemcpyDeviceToHost));
+    if (f.data_error || f.resource_error || f.singularity || f.stack_overflow || f.queue_overflow) {
+        G2_CUDA(cudaMemset(flags_.p, 0, sizeof(DevFlags)));
+        if (f.singularity) throw Error(kSingularity, "direct_sum: coincident particles with zero softening");
+        if (f.data_error == 1) throw Error(kDataError, "bounding_cube: non-finite position");
+        if (f.data_error) throw Error(kDataError, "morton_key: position outside root cube");
+        if (f.resource_error) throw Error(kResourceError, "walk_tree_group: frontier queue exhausted");
+        throw Error(kInternal, "walk: internal stack/queue overflow");
+    }
+}
+
+void Engine::upload_orig(size_t n, const double* mass, const double* pos) {
+    G2_CUDA(cudaMemcpyAsync(pos3_.p, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s_));
+    G2_CUDA(cudaMemcpyAsync(mass_.p, mass, n * sizeof(double), cudaMemcpyHostToDevice, s_));
+}
+
+void Engine::sort_keys_identity_payload(size_t n) {
+    // keys_a_ holds the key of original particle i at index i
+    const bool alt = radix_sort_pairs<uint64_t>(keys_a_.p, vals_a_.p, keys_b_.p, vals_b_.p, n, 63, true, sort_, s_);
+    uint64_t* ks = alt ? keys_b_.p : keys_a_.p;
+    uint32_t* vs = alt ? vals_b_.p : vals_a_.p;
+    if (ks != keys_a_.p) G2_CUDA(cudaMemcpyAsync(keys_a_.p, ks, n * 8, cudaMemcpyDeviceToDevice, s_));
+    G2_CUDA(cudaMemcpyAsync(perm_.p, vs, n * 4, cudaMemcpyDeviceToDevice, s_));
+    launch_invert_perm(perm_.p, rank_.p, n, s_);
+}
+
+void Engine::build(size_t n, const double* mass, const double* pos, bool with_nodes) {
+    if (n < 1) throw Error(kDataError, "build_tree: empty system");
+    if (c_.leaf_cap < 1) throw Error(kDataError, "build_tree: leaf_cap must be >= 1");
+    if (n >= (size_t(1) << 31)) throw Error(kDataError, "build_tree: n must be < 2^31");
+    reserve(n);
+    n_ = n;
+    upload_orig(n, mass, pos);
+    launch_pack_identity(pos3_.p, mass_.p, xyzm_o_.p, n, s_);
+    launch_bbox(xyzm_o_.p, n, bbox_part_.p, cube_.p, flags_.p, s_);
+    launch_keys(xyzm_o_.p, nullptr, n, cube_.p, keys_a_.p, flags_.p, s_);
+    sort_keys_identity_payload(n);
+    launch_pack_sorted(pos3_.p, mass_.p, perm_.p, xyzm_s_.p, n, s_);
+    has_tree_ = false;
+    check_flags();
+    split_and_nodes(with_nodes);
+    has_tree_ = true;
+}
+
+const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur) {
+    const size_t n = n_;
+    launch_bbox(xyzm_s_.p, n, bbox_part_.p, cube_.p, flags_.p, s_);
+    launch_keys(xyzm_s_.p, ids, n, cube_.p, keys_a_.p, flags_.p, s_);  // keys by original id
+    sort_keys_identity_payload(n);                                      // perm = original ids in Morton order
+    launch_gather_u32(rank_cur, perm_.p, src_.p, n, s_);               // new k <- old position of perm[k]
+    launch_gather_d4(xyzm_s_.p, src_.p, xyzm_alt_.p, n, s_);
+    swap_xyzm();
+    return src_.p;
+}
+
+void Engine::split_and_nodes(bool with_nodes) {
+    const size_t n = n_;
+    while (true) {
+        G2_CUDA(cudaMemsetAsync(level_start_.p, 0, (kMaxDepth + 3) * sizeof(uint32_t), s_));
+        G2_CUDA(cudaMemsetAsync(tile_counters_.p, 0, (kMaxDepth + 1) * sizeof(uint32_t), s_));
+        G2_CUDA(cudaMemsetAsync(split_status_.p, 0, (cell_cap_ / 32 + 64) * sizeof(uint64_t), s_));
+        SplitArgs a{keys_a_.p,  first_child_.p, child_count_.p, first_.p,
+                    count_.p,   depth_.p,       level_start_.p, split_status_.p,
+                    tile_counters_.p, uint32_t(cell_cap_), uint32_t(std::min<size_t>(c_.leaf_cap, 0xffffffffu)),
+                    flags_.p};
+        launch_split(a, uint32_t(n), s_);
+        uint32_t ls[kMaxDepth + 3];
+        G2_CUDA(cudaMemcpyAsync(ls, level_start_.p, sizeof ls, cudaMemcpyDeviceToHost, s_));
+        G2_CUDA(cudaStreamSynchronize(s_));
+        const size_t total = ls[kMaxDepth + 1];
+        if (total <= cell_cap_) {
+            ncells_ = total;
+            max_level_width_ = 0;
+            for (int d = 0; d <= kMaxDepth; ++d) max_level_width_ = std::max(max_level_width_, ls[d + 1] - ls[d]);
+            break;
+        }
+        ensure_cells(total + total / 4 + 1024);
+    }
+    if (with_nodes) calc_nodes();
+}
+
+void Engine::calc_nodes() {
+    launch_calc_node(xyzm_s_.p, first_child_.p, child_count_.p, first_.p, count_.p, depth_.p, level_start_.p,
+                     nodes_.p, s_);
+}
+
+void Engine::refresh(size_t n, const double* mass, const double* pos) {
+    if (!has_tree_) throw Error(kDataError, "GravityEngine::refresh: no tree built");
+    if (n != n_) throw Error(kDataError, "GravityEngine::refresh: particle count differs from the tree");
+    upload_orig(n, mass, pos);
+    launch_pack_sorted(pos3_.p, mass_.p, perm_.p, xyzm_s_.p, n, s_);
+    calc_nodes();
+    check_flags();
+}
+
+void Engine::read_events(EventsH& ev) {
+    unsigned long long e[3];
+    G2_CUDA(cudaMemcpyAsync(e, events_.p, sizeof e, cudaMemcpyDeviceToHost, s_));
+    G2_CUDA(cudaStreamSynchronize(s_));
+    ev.interactions = e[0], ev.mac_evals = e[1], ev.list_pushes = e[2];
+}
+
+void Engine::finalize_walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, bool with_pot) {
+    WalkBuffers b{};
+    b.sinks = sinks;
+    b.n_sinks = n_sinks_dev;
+    b.accum = accum_.p;
+    launch_walk_finalize(b, n_sinks_cap, ax_s_.p, ay_s_.p, az_s_.p, with_pot ? pot_s_.p : nullptr, s_);
+}
+
+EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, const double* amag_s,
+                     bool with_pot, bool sync_events, uint32_t group_lo, uint32_t group_hi, bool finalize) {
+    EventsH ev;
+    if (c_.list_capacity < 1) throw Error(kDataError, "InteractionList: capacity must be >= 1");
+    G2_CUDA(cudaMemsetAsync(events_.p, 0, 3 * sizeof(unsigned long long), s_));
+    const uint32_t gs = uint32_t(c_.group_size);
+    const uint32_t ng_cap = (n_sinks_cap + gs - 1) / gs;
+    const size_t cap = c_.frontier_cap ? c_.frontier_cap : 8 * n_;
+    const bool check = cap < max_level_width_;
+    TreeView tv{xyzm_s_.p, nodes_.p, uint32_t(n_)};
+    WalkBuffers b{};
+    b.sinks = sinks;
+    b.n_sinks = n_sinks_dev;
+    b.groups = groups_.p;
+    b.n_groups = n_groups_.p;
+    b.accum = accum_.p;
+    b.events = events_.p;
+    b.queue = queue_.p;
+    b.queue_cap = queue_cap_;
+    b.qstate = qstate_.p;
+    b.spill = spill_.p;
+    b.group_lo = group_lo;
+    b.group_hi = group_hi;
+    if (check) {
+        level_count_.reserve(size_t(ng_cap) * (kMaxDepth + 1));
+        G2_CUDA(cudaMemsetAsync(level_count_.p, 0, size_t(ng_cap) * (kMaxDepth + 1) * 4, s_));
+        b.level_count = level_count_.p;
+    }
+    b.group_inter = group_inter_.p;
+    G2_CUDA(cudaMemsetAsync(group_inter_.p, 0, size_t(ng_cap) * 8, s_));
+    launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
+    WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
+                  c_.count_ops ? 1 : 0, 0};
+    launch_walk(tv, wp, b, with_pot, n_sinks_cap, flags_.p, s_);
+    if (check)
+        G2_COUNT(1), frontier_check_kernel<<<gridn(size_t(ng_cap) * (kMaxDepth + 1)), kB, 0, s_>>>(
+            level_count_.p, size_t(ng_cap) * (kMaxDepth + 1), uint32_t(std::min<size_t>(cap, 0xffffffffu)),
+            flags_.p);
+    if (finalize) launch_walk_finalize(b, n_sinks_cap, ax_s_.p, ay_s_.p, az_s_.p, with_pot ? pot_s_.p : nullptr, s_);
+    if (sync_events) read_events(ev);
+    return ev;
+}
+
+EventsH Engine::evaluate(size_t n, const double* mass, const double* pos, const double* acc_old_mag,
+                         size_t n_targets, const uint32_t* targets, double* acc_out, double* pot_out) {
+    if (!has_tree_) throw Error(kDataError, "GravityEngine::evaluate: no tree built");
+    if (n != n_) throw Error(kDataError, "GravityEngine::evaluate: particle count differs from the tree");
+    if (targets && n_targets == 0) return {};
+    const size_t nt = targets ? n_targets : n;
+    if (targets)
+        for (size_t j = 0; j < nt; ++j)
+            if (targets[j] >= n) throw Error(kDataError, "GravityEngine::evaluate: target index out of range");
+    upload_orig(n, mass, pos);
+    launch_pack_sorted(pos3_.p, mass_.p, perm_.p, xyzm_s_.p, n, s_);
+    G2_CUDA(cudaMemcpyAsync(amag_o_.p, acc_old_mag, n * sizeof(double), cudaMemcpyHostToDevice, s_));
+    launch_gather_f64(amag_o_.p, perm_.p, amag_s_.p, n, s_);
+    const uint32_t* out_idx;
+    if (targets) {
+        // sinks = ranks of the targets, sorted (engine.cpp:39-41); duplicates kept
+        G2_CUDA(cudaMemcpyAsync(vals_b_.p, targets, nt * 4, cudaMemcpyHostToDevice, s_));
+        launch_gather_u32(rank_.p, vals_b_.p, tgt_rank_.p, nt, s_);
+        G2_CUDA(cudaMemcpyAsync(sinks_.p, tgt_rank_.p, nt * 4, cudaMemcpyDeviceToDevice, s_));
+        int bits = 1;
+        while ((size_t(1) << bits) < n) ++bits;
+        const bool alt = radix_sort_pairs<uint32_t>(sinks_.p, vals_a_.p, sinks_alt_.p, vals_b_.p, nt, bits, true,
+                                                    sort_, s_);
+        if (alt) G2_CUDA(cudaMemcpyAsync(sinks_.p, sinks_alt_.p, nt * 4, cudaMemcpyDeviceToDevice, s_));
+        out_idx = tgt_rank_.p;
+    } else {
+        launch_iota(sinks_.p, n, s_);
+        out_idx = rank_.p;
+    }
+    const uint32_t nt32 = uint32_t(nt);
+    G2_CUDA(cudaMemcpyAsync(n_sinks_.p, &nt32, 4, cudaMemcpyHostToDevice, s_));
+    EventsH ev = walk(sinks_.p, n_sinks_.p, nt32, amag_s_.p, pot_out != nullptr, false);
+    // results for the targets in target order
+    G2_COUNT(1), interleave_kernel<<<gridn(nt), kB, 0, s_>>>(ax_s_.p, ay_s_.p, az_s_.p, out_idx, out_.p, nt);
+    std::vector<double> acc(3 * nt), pot(pot_out ? nt : 0);
+    G2_CUDA(cudaMemcpyAsync(acc.data(), out_.p, 3 * nt * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    if (pot_out) {
+        G2_COUNT(1), gather_scalar_kernel<<<gridn(nt), kB, 0, s_>>>(pot_s_.p, out_idx, amag_o_.p, nt);
+        G2_CUDA(cudaMemcpyAsync(pot.data(), amag_o_.p, nt * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    }
+    read_events(ev);
+    check_flags();
+    for (size_t j = 0; j < nt; ++j) {
+        const size_t id = targets ? targets[j] : j;
+        acc_out[3 * id] = acc[3 * j], acc_out[3 * id + 1] = acc[3 * j + 1], acc_out[3 * id + 2] = acc[3 * j + 2];
+        if (pot_out) pot_out[id] = pot[j];
+    }
+    return ev;
+}
+
+void Engine::direct_sum_orig(const double4* xyzm_orig, size_t n, double* ax, double* ay, double* az) {
+    launch_direct_sum(xyzm_orig, n, p_.G, p_.eps, ax, ay, az, flags_.p, s_);
+}
+
+EventsH Engine::bootstrap(size_t n, const double* mass, const double* pos, double* acc_out, double* acc_old_mag_io) {
+    EventsH ev;
+    if (n <= c_.bootstrap_direct_limit) {  // engine.cpp:91-94
+        if (n < 1) throw Error(kDataError, "direct_sum: empty system");
+        reserve(n);
+        upload_orig(n, mass, pos);
+        launch_pack_identity(pos3_.p, mass_.p, xyzm_o_.p, n, s_);
+        direct_sum_orig(xyzm_o_.p, n, ax_s_.p, ay_s_.p, az_s_.p);
+        ev.interactions = uint64_t(n) * (n - 1);
+        G2_COUNT(1), interleave_kernel<<<gridn(n), kB, 0, s_>>>(ax_s_.p, ay_s_.p, az_s_.p, nullptr, out_.p, n);
+        launch_norm3(ax_s_.p, ay_s_.p, az_s_.p, amag_o_.p, n, s_);
+        G2_CUDA(cudaMemcpyAsync(acc_out, out_.p, 3 * n * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        G2_CUDA(cudaMemcpyAsync(acc_old_mag_io, amag_o_.p, n * sizeof(double), cudaMemcpyDeviceToHost, s_));
+        check_flags();
+        return ev;
+    }
+    if (!has_tree_) build(n, mass, pos, true);
+    ev = evaluate(n, mass, pos, acc_old_mag_io, 0, nullptr, acc_out, nullptr);
+    for (size_t i = 0; i < n; ++i) {
+        const double x = acc_out[3 * i], y = acc_out[3 * i + 1], z = acc_out[3 * i + 2];
+        acc_old_mag_io[i] = std::sqrt(x * x + y * y + z * z);
+    }
+    return ev;
+}
+
+void Engine::get_tree(double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* rank, uint32_t* cells4,
+                      uint8_t* depth, double* nodes5) {
+    if (!has_tree_) throw Error(kDataError, "get_tree: no tree built");
+    const size_t n = n_, nc = ncells_;
+    if (bbox4) G2_CUDA(cudaMemcpyAsync(bbox4, cube_.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s_));
+    if (keys) G2_CUDA(cudaMemcpyAsync(keys, keys_a_.p, n * 8, cudaMemcpyDeviceToHost, s_));
+    if (perm) G2_CUDA(cudaMemcpyAsync(perm, perm_.p, n * 4, cudaMemcpyDeviceToHost, s_));
+    if (rank) G2_CUDA(cudaMemcpyAsync(rank, rank_.p, n * 4, cudaMemcpyDeviceToHost, s_));
+    std::vector<uint32_t> fc(nc), cc(nc), f(nc), c(nc);
+    std::vector<WNode> nd(nodes5 ? nc : 0);
+    G2_CUDA(cudaMemcpyAsync(fc.data(), first_child_.p, nc * 4, cudaMemcpyDeviceToHost, s_));
+    G2_CUDA(cudaMemcpyAsync(cc.data(), child_count_.p, nc * 4, cudaMemcpyDeviceToHost, s_));
+    G2_CUDA(cudaMemcpyAsync(f.data(), first_.p, nc * 4, cudaMemcpyDeviceToHost, s_));
+    G2_CUDA(cudaMemcpyAsync(c.data(), count_.p, nc * 4, cudaMemcpyDeviceToHost, s_));
+    if (depth) G2_CUDA(cudaMemcpyAsync(depth, depth_.p, nc, cudaMemcpyDeviceToHost, s_));
+    if (nodes5) G2_CUDA(cudaMemcpyAsync(nd.data(), nodes_.p, nc * sizeof(WNode), cudaMemcpyDeviceToHost, s_));
+    G2_CUDA(cudaStreamSynchronize(s_));
+    for (size_t i = 0; i < nc; ++i) {
+        if (cells4) cells4[4 * i] = fc[i], cells4[4 * i + 1] = cc[i], cells4[4 * i + 2] = f[i], cells4[4 * i + 3] = c[i];
+        if (nodes5) {
+            nodes5[5 * i] = nd[i].mass;
+            nodes5[5 * i + 1] = nd[i].cx, nodes5[5 * i + 2] = nd[i].cy, nodes5[5 * i + 3] = nd[i].cz;
+            nodes5[5 * i + 4] = nd[i].extent;
+        }
+    }
+}
+
+// =============================================================================================
+RebuildTuner::RebuildTuner(TunerConfigH c) : c_(c), interval_(c.initial_interval) {
+    if (c_.min_interval < 1 || c_.max_interval < c_.min_interval)
+        throw Error(kDataError, "RebuildTuner: bad interval bounds");
+    interval_ = std::clamp(interval_, c_.min_interval, c_.max_interval);
+}
+void RebuildTuner::set_interval(size_t i) { interval_ = std::clamp(i, c_.min_interval, c_.max_interval); }
+void RebuildTuner::on_rebuild() {
+    const size_t fit = autotune();
+    interval_ = std::clamp((interval_ + fit + 1) / 2, c_.min_interval, c_.max_interval);
+    hist_.clear();
+    steps_ = 0;
+}
+size_t RebuildTuner::autotune() const {
+    if (hist_.size() < 2) return interval_;
+    std::vector<double> slopes;
+    for (size_t j = 1; j < hist_.size(); ++j)
+        for (size_t i = 0; i < j; ++i) slopes.push_back((hist_[j] - hist_[i]) / double(j - i));
+    std::nth_element(slopes.begin(), slopes.begin() + slopes.size() / 2, slopes.end());
+    double slope = std::max(0.0, slopes[slopes.size() / 2]);
+    std::vector<double> res(hist_.size());
+    for (size_t k = 0; k < hist_.size(); ++k) res[k] = hist_[k] - slope * double(k);
+    std::nth_element(res.begin(), res.begin() + res.size() / 2, res.end());
+    const double intercept = res[res.size() / 2];
+    size_t best_m = c_.min_interval;
+    double best = 0.0;
+    for (size_t m = c_.min_interval; m <= c_.max_interval; ++m) {
+        const double md = double(m);
+        const double cost = build_time_ / md + intercept + slope * (md - 1.0) / 2.0;
+        if (m == c_.min_interval || cost <= best) best = cost, best_m = m;
+    }
+    return best_m;
+}
+
+// =============================================================================================
+Simulation::Simulation(size_t n, const double* mass, const double* pos, const double* vel, GravParamsH p,
+                       StepSchemeH sc, EngineConfigH ec, TunerConfigH tc, int device)
+    : eng_(p, ec, device), p_(p), sc_(sc), tuner_(tc), n_(n) {
+    if (!(sc_.dt_max > 0.0)) throw Error(kDataError, "Simulation: dt_max must be positive");
+    if (!(sc_.eta > 0.0)) throw Error(kDataError, "Simulation: eta must be positive");
+    if (n < 1) throw Error(kDataError, "Simulation: empty system");
+    for (size_t i = 0; i < n; ++i) {  // ParticleSystem::validate (octree.cpp:14-22)
+        if (!(mass[i] > 0.0) || !std::isfinite(mass[i]))
+            throw Error(kDataError, "particle system: non-positive or non-finite mass");
+        for (int a = 0; a < 3; ++a)
+            if (!std::isfinite(pos[3 * i + a]) || !std::isfinite(vel[3 * i + a]))
+                throw Error(kDataError, "particle system: non-finite state");
+    }
+    tick_ = sc_.dt_max / double(uint64_t(1) << kMaxBlockLevel);
+    eng_.reserve(n);
+    eng_.set_n(n);
+    cudaStream_t s = eng_.stream();
+    for (auto* b : {&vx_, &vy_, &vz_, &ax_, &ay_, &az_, &amag_, &vx2_, &vy2_, &vz2_, &ax2_, &ay2_, &az2_, &amag2_})
+        b->reserve(n);
+    level_.reserve(n), level2_.reserve(n), active_.reserve(n);
+    last_.reserve(n), last2_.reserve(n);
+    ids_.reserve(n), ids2_.reserve(n), rank_cur_.reserve(n), sinks_.reserve(n), n_active_.reserve(1);
+    compact_ctr_.reserve(1);
+    compact_status_.reserve(n / 4096 + 8);
+    t_next_.reserve(1);
+    // state in original order until the first build
+    DBuf<double> tmp3, tmpm;
+    tmp3.reserve(3 * n), tmpm.reserve(n);
+    G2_CUDA(cudaMemcpyAsync(tmp3.p, pos, 3 * n * 8, cudaMemcpyHostToDevice, s));
+    G2_CUDA(cudaMemcpyAsync(tmpm.p, mass, n * 8, cudaMemcpyHostToDevice, s));
+    launch_pack_identity(tmp3.p, tmpm.p, eng_.xyzm_s(), n, s);
+    G2_CUDA(cudaMemcpyAsync(tmp3.p, vel, 3 * n * 8, cudaMemcpyHostToDevice, s));
+    G2_COUNT(1), deinterleave_kernel<<<gridn(n), kB, 0, s>>>(tmp3.p, nullptr, vx_.p, vy_.p, vz_.p, n);
+    for (auto* b : {&ax_, &ay_, &az_, &amag_}) G2_CUDA(cudaMemsetAsync(b->p, 0, n * 8, s));
+    G2_CUDA(cudaMemsetAsync(level_.p, 0, n, s));
+    G2_CUDA(cudaMemsetAsync(last_.p, 0, n * 8, s));
+    launch_iota(ids_.p, n, s);
+    launch_iota(rank_cur_.p, n, s);
+    G2_CUDA(cudaStreamSynchronize(s));
+    for (auto& e : ev_) G2_CUDA(cudaEventCreate(&e));
+}
+
+StepState Simulation::state() {
+    return StepState{eng_.xyzm_s(), vx_.p, vy_.p, vz_.p, ax_.p, ay_.p, az_.p, amag_.p, level_.p, last_.p};
+}
+
+void Simulation::reorder(const uint32_t* src) {
+    cudaStream_t s = eng_.stream();
+    const size_t n = n_;
+    DBuf<double>* pairs[][2] = {{&vx_, &vx2_}, {&vy_, &vy2_}, {&vz_, &vz2_}, {&ax_, &ax2_},
+                                {&ay_, &ay2_}, {&az_, &az2_}, {&amag_, &amag2_}};
+    for (auto& pr : pairs) {
+        launch_gather_f64(pr[0]->p, src, pr[1]->p, n, s);
+        std::swap(pr[0]->p, pr[1]->p);
+    }
+    launch_gather_u8(level_.p, src, level2_.p, n, s);
+    std::swap(level_.p, level2_.p);
+    launch_gather_u64(last_.p, src, last2_.p, n, s);
+    std::swap(last_.p, last2_.p);
+    launch_gather_u8(active_.p, src, level2_.p, n, s);  // active flags ride along (level2_ as scratch)
+    std::swap(active_.p, level2_.p);
+    G2_CUDA(cudaMemcpyAsync(ids_.p, eng_.perm(), n * 4, cudaMemcpyDeviceToDevice, s));
+    G2_CUDA(cudaMemcpyAsync(rank_cur_.p, eng_.rank(), n * 4, cudaMemcpyDeviceToDevice, s));
+}
+
+double Simulation::elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    G2_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms * 1e-3;
+}
+
+void Simulation::init() {
+    cudaStream_t s = eng_.stream();
+    const size_t n = n_;
+    const EngineConfigH& c = eng_.config();
+    if (n <= c.bootstrap_direct_limit) {  // engine.cpp:91-94: state is still in original order
+        eng_.direct_sum_orig(eng_.xyzm_s(), n, ax_.p, ay_.p, az_.p);
+    } else {
+        const uint32_t* src = eng_.rebuild_sorted(ids_.p, rank_cur_.p);
+        reorder(src);
+        eng_.split_and_nodes(true);
+        eng_.mark_tree(true);
+        launch_iota(sinks_.p, n, s);
+        const uint32_t n32 = uint32_t(n);
+        G2_CUDA(cudaMemcpyAsync(n_active_.p, &n32, 4, cudaMemcpyHostToDevice, s));
+        eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false);  // amag == 0: geometric MAC
+        G2_CUDA(cudaMemcpyAsync(ax_.p, eng_.ax_s(), n * 8, cudaMemcpyDeviceToDevice, s));
+        G2_CUDA(cudaMemcpyAsync(ay_.p, eng_.ay_s(), n * 8, cudaMemcpyDeviceToDevice, s));
+        G2_CUDA(cudaMemcpyAsync(az_.p, eng_.az_s(), n * 8, cudaMemcpyDeviceToDevice, s));
+    }
+    launch_norm3(ax_.p, ay_.p, az_.p, amag_.p, n, s);
+    SchemeDev sd{sc_.eta, sc_.dt_max, p_.eps, sc_.adaptive ? 1 : 0, sc_.fixed_level};
+    if (sc_.adaptive)
+        launch_assign_levels(state(), n, sd, s);
+    else
+        G2_COUNT(1), fill_u8_kernel<<<gridn(n), kB, 0, s>>>(level_.p, uint8_t(std::clamp(sc_.fixed_level, 0, kMaxBlockLevel)), n);
+    eng_.check_flags();
+    initialized_ = true;
+}
+
+StepResultH Simulation::step() {
+    if (!initialized_) throw Error(kDataError, "Simulation::step: init() not called");
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t s = eng_.stream();
+    const size_t n = n_;
+    StepResultH r;
+    StepState st = state();
+    SchemeDev sd{sc_.eta, sc_.dt_max, p_.eps, sc_.adaptive ? 1 : 0, sc_.fixed_level};
+
+    G2_CUDA(cudaEventRecord(ev_[0], s));
+    launch_tnext(st, n, t_next_.p, s);
+    launch_predict(st, n, t_next_.p, now_, tick_, active_.p, s);
+    G2_CUDA(cudaEventRecord(ev_[1], s));
+
+    const bool rebuild = !eng_.has_tree() || rebuild_every_step_ || tuner_.should_rebuild();
+    if (rebuild) {
+        if (autotune_)
+            tuner_.on_rebuild();
+        else
+            tuner_.reset_cycle();
+        const uint32_t* src = eng_.rebuild_sorted(ids_.p, rank_cur_.p);
+        reorder(src);
+        eng_.split_and_nodes(false);  // syncs once to size the levels
+        eng_.mark_tree(true);
+        G2_CUDA(cudaEventRecord(ev_[2], s));
+        eng_.calc_nodes();
+        G2_CUDA(cudaEventRecord(ev_[3], s));
+    } else {
+        G2_CUDA(cudaEventRecord(ev_[2], s));
+        eng_.calc_nodes();
+        G2_CUDA(cudaEventRecord(ev_[3], s));
+    }
+    st = state();
+    // active set in (new) Morton order == reference's rank-sorted targets (engine.cpp:39-41)
+    launch_compact(active_.p, n, sinks_.p, n_active_.p, compact_status_.p, compact_ctr_.p, s);
+    uint32_t lo = 0, hi = ~0u;
+    if (world_ > 1) {
+        // contiguous equal shard of the groups (cost-balanced sharding: see DESIGN.md)
+        uint32_t na = 0;
+        G2_CUDA(cudaMemcpyAsync(&na, n_active_.p, 4, cudaMemcpyDeviceToHost, s));
+        G2_CUDA(cudaStreamSynchronize(s));
+        const uint32_t gs = uint32_t(eng_.config().group_size);
+        const uint32_t ng = (na + gs - 1) / gs;
+        lo = uint32_t(uint64_t(ng) * rank_ / world_);
+        hi = uint32_t(uint64_t(ng) * (rank_ + 1) / world_);
+    }
+    shard_lo_ = lo, shard_hi_ = hi;
+    const bool sharded = world_ > 1 && exchange_;
+    eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false, lo, hi, !sharded);
+    G2_CUDA(cudaEventRecord(ev_[4], s));
+    if (sharded) {
+        exchange_->allgather_acc(*this);  // every rank receives every group's accelerations
+        eng_.finalize_walk(sinks_.p, n_active_.p, uint32_t(n), false);
+    }
+    G2_CUDA(cudaEventRecord(ev_[5], s));
+    launch_correct(st, sinks_.p, n_active_.p, uint32_t(n), eng_.ax_s(), eng_.ay_s(), eng_.az_s(), t_next_.p, now_,
+                   tick_, sd, s);
+    G2_CUDA(cudaEventRecord(ev_[6], s));
+
+    unsigned long long tn = 0;
+    uint32_t na = 0;
+    G2_CUDA(cudaMemcpyAsync(&tn, t_next_.p, 8, cudaMemcpyDeviceToHost, s));
+    G2_CUDA(cudaMemcpyAsync(&na, n_active_.p, 4, cudaMemcpyDeviceToHost, s));
+    eng_.read_events(r.events);
+    eng_.check_flags();
+    r.timings.predict = elapsed(ev_[0], ev_[1]);
+    if (rebuild) {
+        r.timings.make_tree = elapsed(ev_[1], ev_[2]);
+        r.rebuilt = true;
+    }
+    r.timings.calc_node = elapsed(ev_[2], ev_[3]);
+    r.timings.walk_tree = elapsed(ev_[3], ev_[4]);
+    r.timings.correct = elapsed(ev_[5], ev_[6]);
+    tuner_.record_walk(r.timings.walk_tree);
+    if (rebuild) tuner_.record_build(r.timings.make_tree + r.timings.calc_node);
+    last_active_ = na;
+    r.active = na;
+    now_ = tn;
+    time_ = double(now_) * tick_;
+    r.rebuild_interval = tuner_.interval();
+    r.wall_seconds = seconds(t0);
+    return r;
+}
+
+void Simulation::get_state(double* pos, double* vel, double* acc, double* acc_old_mag, uint8_t* level,
+                           double* time) {
+    cudaStream_t s = eng_.stream();
+    const size_t n = n_;
+    std::vector<uint32_t> ids(n);
+    G2_CUDA(cudaMemcpyAsync(ids.data(), ids_.p, n * 4, cudaMemcpyDeviceToHost, s));
+    DBuf<double> tmp;
+    tmp.reserve(3 * n);
+    std::vector<double> h(3 * n);
+    auto fetch3 = [&](const double* x, const double* y, const double* z, double* out) {
+        G2_COUNT(1), interleave_kernel<<<gridn(n), kB, 0, s>>>(x, y, z, nullptr, tmp.p, n);
+        G2_CUDA(cudaMemcpyAsync(h.data(), tmp.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));
+        G2_CUDA(cudaStreamSynchronize(s));
+        for (size_t k = 0; k < n; ++k)
+            for (int a = 0; a < 3; ++a) out[3 * size_t(ids[k]) + a] = h[3 * k + a];
+    };
+    if (pos) {
+        G2_COUNT(1), xyzm_to_pos3_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), tmp.p, n);
+        G2_CUDA(cudaMemcpyAsync(h.data(), tmp.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));
+        G2_CUDA(cudaStreamSynchronize(s));
+        for (size_t k = 0; k < n; ++k)
+            for (int a = 0; a < 3; ++a) pos[3 * size_t(ids[k]) + a] = h[3 * k + a];
+    }
+    if (vel) fetch3(vx_.p, vy_.p, vz_.p, vel);
+    if (acc) fetch3(ax_.p, ay_.p, az_.p, acc);
+    if (acc_old_mag) {
+        G2_CUDA(cudaMemcpyAsync(h.data(), amag_.p, n * 8, cudaMemcpyDeviceToHost, s));
+        G2_CUDA(cudaStreamSynchronize(s));
+        for (size_t k = 0; k < n; ++k) acc_old_mag[ids[k]] = h[k];
+    }
+    if (level) {
+        std::vector<uint8_t> lv(n);
+        G2_CUDA(cudaMemcpyAsync(lv.data(), level_.p, n, cudaMemcpyDeviceToHost, s));
+        G2_CUDA(cudaStreamSynchronize(s));
+        for (size_t k = 0; k < n; ++k) level[ids[k]] = lv[k];
+    }
+    if (time) *time = time_;
+}
+
+void Simulation::set_state(const double* pos, const double* vel) {
+    cudaStream_t s = eng_.stream();
+    const size_t n = n_;
+    DBuf<double> tmp;
+    tmp.reserve(3 * n);
+    if (pos) {
+        G2_CUDA(cudaMemcpyAsync(tmp.p, pos, 3 * n * 8, cudaMemcpyHostToDevice, s));
+        G2_COUNT(1), set_pos_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), tmp.p, ids_.p, n);
+    }
+    if (vel) {
+        G2_CUDA(cudaMemcpyAsync(tmp.p, vel, 3 * n * 8, cudaMemcpyHostToDevice, s));
+        G2_COUNT(1), deinterleave_kernel<<<gridn(n), kB, 0, s>>>(tmp.p, ids_.p, vx_.p, vy_.p, vz_.p, n);
+    }
+    G2_CUDA(cudaStreamSynchronize(s));
+}
+
+}  // namespace g2

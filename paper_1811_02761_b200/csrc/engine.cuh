@@ -1,0 +1,239 @@
+// Host-side engine and simulation driver (C++), the implementation behind the
+// C-ABI in include/g2/capi.h.  Mirrors gravitree's GravityEngine
+// (engine.hpp:29-66) and Simulation (integrator.hpp:54-91); all particle state
+// lives on the device in Morton order of the last build.
+#pragma once
+
+#include <chrono>
+#include <vector>
+
+#include "kernels.cuh"
+#include "radix_sort.cuh"
+
+namespace g2 {
+
+struct GravParamsH {
+    double G = 1.0, eps = 0.0, dacc = 0.001953125;  // particle_system.hpp:53-57
+};
+struct EngineConfigH {  // engine.hpp:14-23
+    size_t leaf_cap = 8, group_size = 32, list_capacity = 1024, frontier_cap = 0;
+    bool count_ops = true;
+    double bootstrap_theta = 0.5;
+    size_t bootstrap_direct_limit = 65536;
+    unsigned threads = 0;
+};
+struct EventsH {
+    uint64_t interactions = 0, mac_evals = 0, list_pushes = 0;
+};
+
+class Engine {
+public:
+    Engine(GravParamsH p, EngineConfigH c, int device);
+    ~Engine();
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    // ---- host-order API (GravityEngine) -------------------------------------
+    void build(size_t n, const double* mass, const double* pos, bool with_nodes);
+    void refresh(size_t n, const double* mass, const double* pos);
+    // targets == nullptr: all particles.  acc_out (3n) written for targets only;
+    // pot_out (n, nullable) likewise.  acc_old_mag (n) in original order.
+    EventsH evaluate(size_t n, const double* mass, const double* pos, const double* acc_old_mag, size_t n_targets,
+                     const uint32_t* targets, double* acc_out, double* pot_out);
+    EventsH bootstrap(size_t n, const double* mass, const double* pos, double* acc_out, double* acc_old_mag_out);
+    bool has_tree() const { return has_tree_; }
+    size_t n() const { return n_; }
+    size_t ncells() const { return ncells_; }
+    void get_tree(double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* rank, uint32_t* cells4, uint8_t* depth,
+                  double* nodes5);
+    const GravParamsH& params() const { return p_; }
+    GravParamsH& params() { return p_; }
+    const EngineConfigH& config() const { return c_; }
+
+    // ---- device-level operations (used by Simulation) -------------------------
+    void reserve(size_t n);
+    // Morton-sort the particles currently in xyzm_s() (position k holds original
+    // id ids[k]); reorders xyzm_s and returns src (new position k <- old src[k]).
+    const uint32_t* rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur);
+    void split_and_nodes(bool with_nodes);
+    void calc_nodes();
+    // walk sinks (sorted positions) with acc_old_mag (sorted); results into
+    // ax_s/ay_s/az_s/pot_s at the sinks' sorted positions.
+    EventsH walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, const double* amag_s,
+                 bool with_pot, bool sync_events, uint32_t group_lo = 0, uint32_t group_hi = ~0u,
+                 bool finalize = true);
+    // accum slots -> FP64 accelerations at the sinks' sorted positions
+    void finalize_walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, bool with_pot);
+    float4* accum() { return accum_.p; }
+    size_t accum_cap() const { return accum_.cap; }
+    void reserve_accum(size_t slots) { accum_.reserve(slots); }
+    void direct_sum_orig(const double4* xyzm_orig, size_t n, double* ax, double* ay, double* az);
+    void check_flags();  // syncs and throws on device-side errors
+    void read_events(EventsH& ev);
+
+    cudaStream_t stream() const { return s_; }
+    double4* xyzm_s() { return xyzm_s_.p; }
+    double4* xyzm_alt() { return xyzm_alt_.p; }
+    void swap_xyzm() { std::swap(xyzm_s_.p, xyzm_alt_.p); }
+    uint32_t* perm() { return perm_.p; }
+    uint32_t* rank() { return rank_.p; }
+    double* ax_s() { return ax_s_.p; }
+    double* ay_s() { return ay_s_.p; }
+    double* az_s() { return az_s_.p; }
+    double* pot_s() { return pot_s_.p; }
+    uint64_t* group_inter() { return group_inter_.p; }
+    void set_n(size_t n) { n_ = n; }
+    void mark_tree(bool v) { has_tree_ = v; }
+    uint32_t* n_groups_dev() { return n_groups_.p; }
+
+private:
+    void ensure_cells(size_t cap);
+    void sort_keys_identity_payload(size_t n);  // keys in keys_a_ by original id -> perm_, keys sorted
+    void upload_orig(size_t n, const double* mass, const double* pos);
+
+    GravParamsH p_;
+    EngineConfigH c_;
+    int device_;
+    cudaStream_t s_ = nullptr;
+    size_t n_ = 0, cap_ = 0, ncells_ = 0, cell_cap_ = 0;
+    bool has_tree_ = false;
+    uint32_t max_level_width_ = 0;
+
+    DBuf<double> pos3_, mass_, amag_o_;   // host-order staging
+    DBuf<double4> xyzm_o_, xyzm_s_, xyzm_alt_;
+    DBuf<uint64_t> keys_a_, keys_b_;
+    DBuf<uint32_t> vals_a_, vals_b_, perm_, rank_, src_, tgt_rank_;
+    DBuf<double> amag_s_, ax_s_, ay_s_, az_s_, pot_s_, out_;
+    DBuf<uint32_t> first_child_, child_count_, first_, count_;
+    DBuf<uint8_t> depth_;
+    DBuf<WNode> nodes_;
+    DBuf<uint32_t> level_start_, tile_counters_;
+    DBuf<uint64_t> split_status_;
+    DBuf<double> bbox_part_;
+    DBuf<Cube> cube_;
+    DBuf<uint32_t> sinks_, sinks_alt_, n_sinks_, n_groups_;
+    DBuf<GroupRec> groups_;
+    DBuf<float4> accum_;
+    DBuf<unsigned long long> events_;
+    DBuf<uint64_t> queue_;
+    DBuf<uint32_t> qstate_, spill_, level_count_;
+    DBuf<uint64_t> group_inter_;
+    DBuf<DevFlags> flags_;
+    SortScratch sort_;
+    uint32_t queue_cap_ = 0;
+};
+
+// ---- rebuild auto-tuner: host restatement of rebuild_tuner.{hpp,cpp} ------------
+struct TunerConfigH {
+    size_t min_interval = 1, max_interval = 128, initial_interval = 8;
+};
+class RebuildTuner {
+public:
+    explicit RebuildTuner(TunerConfigH c = {});
+    size_t interval() const { return interval_; }
+    size_t steps_since_rebuild() const { return steps_; }
+    bool should_rebuild() const { return steps_ >= std::max<size_t>(interval_, 2); }  // rebuild_tuner.hpp:26
+    void record_build(double s) { build_time_ = s; }
+    void record_walk(double s) {
+        hist_.push_back(s);
+        ++steps_;
+    }
+    void on_rebuild();
+    void reset_cycle() {
+        hist_.clear();
+        steps_ = 0;
+    }
+    void set_interval(size_t i);
+    size_t autotune() const;  // autotune_rebuild (rebuild_tuner.cpp:28-61)
+    double build_time() const { return build_time_; }
+    const std::vector<double>& history() const { return hist_; }
+
+private:
+    TunerConfigH c_;
+    size_t interval_, steps_ = 0;
+    double build_time_ = 0.0;
+    std::vector<double> hist_;
+};
+
+struct StepSchemeH {  // integrator.hpp:18-23
+    double eta = 0.5, dt_max = 0.0625;
+    bool adaptive = true;
+    int fixed_level = 0;
+};
+struct PhaseTimingsH {
+    double walk_tree = 0, calc_node = 0, make_tree = 0, predict = 0, correct = 0;
+};
+struct StepResultH {
+    PhaseTimingsH timings;
+    EventsH events;
+    size_t active = 0, rebuild_interval = 0;
+    bool rebuilt = false;
+    double wall_seconds = 0.0;
+};
+
+// Multi-GPU hook: after the walk, each rank holds accelerations of its own
+// groups; the exchange makes all ranks hold all of them (one all-gather).
+struct Exchange {
+    virtual ~Exchange() = default;
+    virtual void allgather_acc(class Simulation& sim) = 0;
+};
+
+class Simulation {
+public:
+    Simulation(size_t n, const double* mass, const double* pos, const double* vel, GravParamsH p, StepSchemeH sc,
+               EngineConfigH ec, TunerConfigH tc, int device);
+    void init();
+    StepResultH step();
+    void set_fixed_rebuild_interval(size_t k) {
+        autotune_ = false;
+        tuner_.set_interval(k);
+    }
+    // orig-order host copies
+    void get_state(double* pos, double* vel, double* acc, double* acc_old_mag, uint8_t* level, double* time);
+    void set_state(const double* pos, const double* vel);  // overwrite pos/vel (orig order), keeps the rest
+    Engine& engine() { return eng_; }
+    RebuildTuner& tuner() { return tuner_; }
+    double time() const { return time_; }
+    bool initialized() const { return initialized_; }
+    size_t n() const { return n_; }
+    void set_rebuild_every_step(bool v) { rebuild_every_step_ = v; }
+    void set_shard(int rank, int world, Exchange* ex) {
+        rank_ = rank, world_ = world, exchange_ = ex;
+    }
+    // shard helpers for the exchange
+    uint32_t active_count() const { return last_active_; }
+    const uint32_t* sinks() const { return sinks_.p; }
+    uint32_t shard_lo() const { return shard_lo_; }
+    uint32_t shard_hi() const { return shard_hi_; }
+    const uint32_t* n_active_dev() const { return n_active_.p; }
+    size_t group_size() const { return eng_.config().group_size; }
+
+private:
+    StepState state();
+    void reorder(const uint32_t* src);
+    double elapsed(cudaEvent_t a, cudaEvent_t b);
+
+    Engine eng_;
+    GravParamsH p_;
+    StepSchemeH sc_;
+    RebuildTuner tuner_;
+    size_t n_;
+    bool initialized_ = false, autotune_ = true, rebuild_every_step_ = false;
+    uint64_t now_ = 0;
+    double tick_ = 0.0, time_ = 0.0;
+    uint32_t last_active_ = 0;
+    int rank_ = 0, world_ = 1;
+    Exchange* exchange_ = nullptr;
+    uint32_t shard_lo_ = 0, shard_hi_ = ~0u;
+
+    DBuf<double> vx_, vy_, vz_, ax_, ay_, az_, amag_;
+    DBuf<double> vx2_, vy2_, vz2_, ax2_, ay2_, az2_, amag2_;
+    DBuf<uint8_t> level_, level2_, active_;
+    DBuf<uint64_t> last_, last2_;
+    DBuf<uint32_t> ids_, ids2_, rank_cur_, sinks_, n_active_, compact_ctr_;
+    DBuf<uint64_t> compact_status_;
+    DBuf<unsigned long long> t_next_;
+    cudaEvent_t ev_[12];
+};
+
+}  // namespace g2

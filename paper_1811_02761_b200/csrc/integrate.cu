@@ -1,0 +1,254 @@
+// Block-time-step integrator (integrator.cpp:21-164), bootstrap direct sum
+// (gravity.cpp:18-43) and active-set compaction on sm_100a.  FP64 state,
+// explicit round-to-nearest intrinsics: given identical accelerations the
+// predictor/corrector/level updates are bit-identical to the reference.
+#include "kernels.cuh"
+
+namespace g2 {
+namespace {
+
+constexpr int kBlock = 256;
+inline unsigned grid_for(size_t n) { return std::max(1u, std::min<unsigned>(ceil_div(n, kBlock), kNumSMs * 16)); }
+
+// ---- direct_sum: one thread per sink, sources in index order (bit-exact) -----
+__global__ void __launch_bounds__(kBlock) direct_kernel(const double4* __restrict__ xyzm, uint32_t n, double G,
+                                                        double eps2, double* __restrict__ ax, double* __restrict__ ay,
+                                                        double* __restrict__ az, DevFlags* flags) {
+    __shared__ double4 tile[kBlock];
+    const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
+    const double4 ri = i < n ? xyzm[i] : make_double4(0, 0, 0, 0);
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    bool singular = false;
+    for (uint32_t base = 0; base < n; base += kBlock) {
+        __syncthreads();
+        if (base + threadIdx.x < n) tile[threadIdx.x] = xyzm[base + threadIdx.x];
+        __syncthreads();
+        const uint32_t m = min(uint32_t(kBlock), n - base);
+        if (i < n) {
+            for (uint32_t jj = 0; jj < m; ++jj) {
+                const uint32_t j = base + jj;
+                if (j == i) continue;
+                const double4 q = tile[jj];
+                const double dx = dsub(q.x, ri.x), dy = dsub(q.y, ri.y), dz = dsub(q.z, ri.z);
+                const double d2 = norm2(dx, dy, dz);
+                if (eps2 == 0.0 && d2 == 0.0) {
+                    singular = true;
+                    continue;
+                }
+                const double r2 = dadd(d2, eps2);  // softened_accel (gravity.hpp:15-20)
+                if (r2 == 0.0) continue;
+                const double inv = ddiv(1.0, dsqrt(r2));
+                const double f = dmul(dmul(dmul(dmul(G, q.w), inv), inv), inv);
+                sx = dadd(sx, dmul(dx, f));
+                sy = dadd(sy, dmul(dy, f));
+                sz = dadd(sz, dmul(dz, f));
+            }
+        }
+    }
+    if (singular) flags->singularity = 1;
+    if (i < n) ax[i] = sx, ay[i] = sy, az[i] = sz;
+}
+
+__global__ void __launch_bounds__(kBlock) norm3_kernel(const double* ax, const double* ay, const double* az,
+                                                       double* out, size_t n) {
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
+        out[i] = dsqrt(norm2(ax[i], ay[i], az[i]));
+}
+
+__device__ __forceinline__ uint64_t level_ticks(int level) { return 1ull << (kMaxBlockLevel - level); }
+
+// ---- t_next = min_i last_update + ticks(level) (integrator.cpp:103-105) -------
+__global__ void __launch_bounds__(kBlock) tnext_kernel(const uint8_t* __restrict__ level,
+                                                       const uint64_t* __restrict__ last, size_t n,
+                                                       unsigned long long* t_next) {
+    unsigned long long m = ~0ull;
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
+        m = min(m, (unsigned long long)(last[i] + level_ticks(level[i])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0 && m != ~0ull) atomicMin(t_next, m);
+}
+
+// ---- predict (integrator.cpp:40-45) on ALL particles + active flags (:107-110)
+__global__ void __launch_bounds__(kBlock) predict_kernel(StepState st, size_t n, const unsigned long long* t_next_p,
+                                                         uint64_t now, double tick, uint8_t* __restrict__ active) {
+    const uint64_t t_next = *t_next_p;
+    const double dt = dmul(double(t_next - now), tick);
+    const double h = dmul(dmul(0.5, dt), dt);
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock) {
+        double4 p = st.xyzm[i];
+        const double vx = st.vx[i], vy = st.vy[i], vz = st.vz[i];
+        const double ax = st.ax[i], ay = st.ay[i], az = st.az[i];
+        p.x = dadd(p.x, dadd(dmul(vx, dt), dmul(ax, h)));
+        p.y = dadd(p.y, dadd(dmul(vy, dt), dmul(ay, h)));
+        p.z = dadd(p.z, dadd(dmul(vz, dt), dmul(az, h)));
+        st.xyzm[i] = p;
+        st.vx[i] = dadd(vx, dmul(ax, dt));
+        st.vy[i] = dadd(vy, dmul(ay, dt));
+        st.vz[i] = dadd(vz, dmul(az, dt));
+        if (active) active[i] = (st.last_update[i] + level_ticks(st.level[i]) == t_next) ? 1 : 0;
+    }
+}
+
+// ---- block_level (integrator.cpp:21-33) ------------------------------------------
+__device__ int block_level_dev(double acc_mag, const SchemeDev& s) {
+    if (!s.adaptive) return max(0, min(s.fixed_level, kMaxBlockLevel));
+    if (acc_mag <= 0.0) return 0;
+    const double dt = dmul(s.eta, dsqrt(ddiv(s.eps, acc_mag)));
+    if (dt <= 0.0) return kMaxBlockLevel;
+    if (dt >= s.dt_max) return 0;
+    const double lg = ceil(log2(ddiv(s.dt_max, dt)));
+    int level = lg >= double(kMaxBlockLevel) ? kMaxBlockLevel : (lg <= 0.0 ? 0 : int(lg));
+    // the fix-up loops make the result independent of log2 rounding
+    while (level < kMaxBlockLevel && ddiv(s.dt_max, double(1ull << level)) > dt) ++level;
+    while (level > 0 && ddiv(s.dt_max, double(1ull << (level - 1))) <= dt) --level;
+    return level;
+}
+
+// ---- correct loop over active sinks (integrator.cpp:148-156, apply_level :86-95)
+__global__ void __launch_bounds__(kBlock) correct_kernel(StepState st, const uint32_t* __restrict__ sinks,
+                                                         const uint32_t* n_sinks, uint32_t cap,
+                                                         const double* __restrict__ nax, const double* __restrict__ nay,
+                                                         const double* __restrict__ naz,
+                                                         const unsigned long long* t_next_p, uint64_t now, double tick,
+                                                         SchemeDev sc) {
+    const uint32_t na = min(*n_sinks, cap);
+    const uint64_t t_next = *t_next_p;
+    for (uint32_t s = blockIdx.x * kBlock + threadIdx.x; s < na; s += gridDim.x * kBlock) {
+        const uint32_t i = sinks[s];
+        const double h = dmul(0.5, dmul(double(t_next - st.last_update[i]), tick));
+        const double ax = nax[i], ay = nay[i], az = naz[i];
+        st.vx[i] = dadd(st.vx[i], dmul(dsub(ax, st.ax[i]), h));
+        st.vy[i] = dadd(st.vy[i], dmul(dsub(ay, st.ay[i]), h));
+        st.vz[i] = dadd(st.vz[i], dmul(dsub(az, st.az[i]), h));
+        st.ax[i] = ax, st.ay[i] = ay, st.az[i] = az;
+        const double amag = dsqrt(norm2(ax, ay, az));
+        st.amag[i] = amag;
+        st.last_update[i] = t_next;
+        if (sc.adaptive) {
+            const int target = block_level_dev(amag, sc);
+            const int current = st.level[i];
+            int next = max(current - 1, min(target, current + 1));  // at most one level per step
+            next = max(0, min(next, kMaxBlockLevel));
+            if (next < current && now % level_ticks(next) != 0) next = current;  // uses the previous sync time
+            st.level[i] = uint8_t(next);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) assign_levels_kernel(StepState st, size_t n, SchemeDev sc) {
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
+        st.level[i] = uint8_t(block_level_dev(dsqrt(norm2(st.ax[i], st.ay[i], st.az[i])), sc));
+}
+
+// ---- order-preserving compaction of byte flags (decoupled look-back) ----------
+constexpr int kCItems = 16;
+constexpr int kCTile = kBlock * kCItems;
+
+__global__ void __launch_bounds__(kBlock) compact_kernel(const uint8_t* __restrict__ flags, size_t n,
+                                                         uint32_t* __restrict__ out, uint32_t* __restrict__ n_out,
+                                                         uint64_t* __restrict__ status, uint32_t* counter) {
+    __shared__ uint32_t s_tile, s_wsum[kBlock / 32];
+    __shared__ uint64_t s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const size_t base = size_t(tile) * kCTile + size_t(tid) * kCItems;  // blocked: thread owns 16 consecutive
+    uint32_t bits = 0;
+#pragma unroll
+    for (int k = 0; k < kCItems; ++k)
+        if (base + k < n && flags[base + k]) bits |= 1u << k;
+    const uint32_t x = __popc(bits);
+    uint32_t inc = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_wsum[w] = inc;
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < kBlock / 32; ++k) {
+        if (k < w) wpre += s_wsum[k];
+        tot += s_wsum[k];
+    }
+    if (w == 0) {
+        const uint64_t e = lookback_warp(status, tile, tot);
+        if (lane == 0) s_excl = e;
+    }
+    __syncthreads();
+    uint32_t o = uint32_t(s_excl) + wpre + inc - x;
+#pragma unroll
+    for (int k = 0; k < kCItems; ++k)
+        if (bits & (1u << k)) out[o++] = uint32_t(base + k);
+    const uint32_t ntiles = uint32_t((n + kCTile - 1) / kCTile);
+    if (tile == ntiles - 1 && tid == 0) *n_out = uint32_t(s_excl) + tot;
+}
+
+__global__ void __launch_bounds__(kBlock) block_levels_kernel(const double* amag, size_t n, SchemeDev sc, int* out) {
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
+        out[i] = block_level_dev(amag[i], sc);
+}
+
+// predict with an explicit dt on AoS arrays (the free function integrator.cpp:40-45)
+__global__ void __launch_bounds__(kBlock) predict_aos_kernel(double* pos, double* vel, const double* acc, size_t n,
+                                                             double dt) {
+    const double h = dmul(dmul(0.5, dt), dt);
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < 3 * n; i += size_t(gridDim.x) * kBlock) {
+        pos[i] = dadd(pos[i], dadd(dmul(vel[i], dt), dmul(acc[i], h)));
+        vel[i] = dadd(vel[i], dmul(acc[i], dt));
+    }
+}
+
+}  // namespace
+
+void launch_block_levels(const double* acc_mag, size_t n, SchemeDev sc, int* levels, cudaStream_t s) {
+    if (n) G2_COUNT(1), block_levels_kernel<<<grid_for(n), kBlock, 0, s>>>(acc_mag, n, sc, levels);
+}
+void launch_predict_aos(double* pos3, double* vel3, const double* acc3, size_t n, double dt, cudaStream_t s) {
+    if (n) G2_COUNT(1), predict_aos_kernel<<<grid_for(3 * n), kBlock, 0, s>>>(pos3, vel3, acc3, n, dt);
+}
+
+void launch_direct_sum(const double4* xyzm, size_t n, double G, double eps, double* ax, double* ay, double* az,
+                       DevFlags* flags, cudaStream_t s) {
+    G2_COUNT(1), direct_kernel<<<ceil_div(n, kBlock), kBlock, 0, s>>>(xyzm, uint32_t(n), G, eps * eps, ax, ay, az, flags);
+    G2_CUDA(cudaGetLastError());
+}
+
+void launch_norm3(const double* ax, const double* ay, const double* az, double* out, size_t n, cudaStream_t s) {
+    G2_COUNT(1), norm3_kernel<<<grid_for(n), kBlock, 0, s>>>(ax, ay, az, out, n);
+}
+
+void launch_tnext(const StepState& st, size_t n, unsigned long long* t_next, cudaStream_t s) {
+    G2_CUDA(cudaMemsetAsync(t_next, 0xff, sizeof(unsigned long long), s));
+    G2_COUNT(1), tnext_kernel<<<grid_for(n), kBlock, 0, s>>>(st.level, st.last_update, n, t_next);
+}
+
+void launch_predict(const StepState& st, size_t n, const unsigned long long* t_next, uint64_t now, double tick,
+                    uint8_t* active_flag, cudaStream_t s) {
+    G2_COUNT(1), predict_kernel<<<grid_for(n), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag);
+}
+
+void launch_compact(const uint8_t* flags, size_t n, uint32_t* out, uint32_t* n_out, uint64_t* status,
+                    uint32_t* counter, cudaStream_t s) {
+    const size_t tiles = (n + kCTile - 1) / kCTile;
+    G2_CUDA(cudaMemsetAsync(status, 0, tiles * sizeof(uint64_t), s));
+    G2_CUDA(cudaMemsetAsync(counter, 0, sizeof(uint32_t), s));
+    G2_COUNT(1), compact_kernel<<<unsigned(tiles), kBlock, 0, s>>>(flags, n, out, n_out, status, counter);
+    G2_CUDA(cudaGetLastError());
+}
+
+void launch_correct(const StepState& st, const uint32_t* sinks, const uint32_t* n_sinks, uint32_t n_cap,
+                    const double* nax, const double* nay, const double* naz, const unsigned long long* t_next,
+                    uint64_t now, double tick, SchemeDev sc, cudaStream_t s) {
+    G2_COUNT(1), correct_kernel<<<grid_for(n_cap), kBlock, 0, s>>>(st, sinks, n_sinks, n_cap, nax, nay, naz, t_next, now, tick,
+                                                      sc);
+}
+
+void launch_assign_levels(const StepState& st, size_t n, SchemeDev sc, cudaStream_t s) {
+    G2_COUNT(1), assign_levels_kernel<<<grid_for(n), kBlock, 0, s>>>(st, n, sc);
+}
+
+}  // namespace g2

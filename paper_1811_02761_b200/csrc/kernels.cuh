@@ -1,0 +1,130 @@
+// Kernel-launch entry points shared between the .cu translation units.
+#pragma once
+
+#include "common.cuh"
+
+namespace g2 {
+
+// Root cube (vec3.hpp:53-63) as computed by bounding_cube (octree.cpp:24-49).
+struct Cube {
+    double cx, cy, cz, half;
+};
+
+// Sink group (traversal.hpp:49-54): AABB centre, radius, a_min of its members,
+// which are sinks[first, first + count) (sorted particle indices).
+struct alignas(16) GroupRec {
+    double cx, cy, cz, radius, a_min;
+    uint32_t first, count;
+};
+
+// Device view of the octree.  Particle arrays are in Morton (rank) order of
+// the last build; xyzm packs position and mass.
+struct TreeView {
+    const double4* xyzm;   // [n] sorted
+    const WNode* nodes;    // [ncells]
+    uint32_t n;
+};
+
+// ---- tree.cu -----------------------------------------------------------------
+// bbox partials -> cube; then keys in ORIGINAL index order (key_by_id[id]).
+void launch_bbox(const double4* xyzm, size_t n, double* partials, Cube* cube, DevFlags* flags, cudaStream_t s);
+// key of the particle stored at position i goes to key_by_id[id_of_pos[i]] (nullptr: identity)
+void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const Cube* cube, uint64_t* key_by_id,
+                 DevFlags* flags, cudaStream_t s);
+
+struct SplitArgs {
+    const uint64_t* keys;     // sorted
+    uint32_t* first_child;
+    uint32_t* child_count;
+    uint32_t* first;
+    uint32_t* count;
+    uint8_t* depth;
+    uint32_t* level_start;    // [kMaxDepth + 3]
+    uint64_t* status;         // look-back words, zeroed
+    uint32_t* tile_counters;  // [kMaxDepth + 1], zeroed
+    uint32_t cell_cap;
+    uint32_t leaf_cap;
+    DevFlags* flags;
+};
+void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s);
+
+// calc_node over all levels, deepest first (octree.cpp:145-162)
+void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const uint32_t* child_count,
+                      const uint32_t* first, const uint32_t* count, const uint8_t* depth, const uint32_t* level_start,
+                      WNode* nodes, cudaStream_t s);
+
+// out[k] = in[src[k]] gathers
+void launch_gather_d4(const double4* in, const uint32_t* src, double4* out, size_t n, cudaStream_t s);
+void launch_gather_f64(const double* in, const uint32_t* src, double* out, size_t n, cudaStream_t s);
+void launch_gather_u64(const uint64_t* in, const uint32_t* src, uint64_t* out, size_t n, cudaStream_t s);
+void launch_gather_u8(const uint8_t* in, const uint32_t* src, uint8_t* out, size_t n, cudaStream_t s);
+void launch_gather_u32(const uint32_t* in, const uint32_t* src, uint32_t* out, size_t n, cudaStream_t s);
+// rank[perm[k]] = k
+void launch_invert_perm(const uint32_t* perm, uint32_t* rank, size_t n, cudaStream_t s);
+// xyzm[k] = (pos[3*id], ..., mass[id]) with id = perm[k] (host-order upload -> sorted)
+void launch_pack_sorted(const double* pos3, const double* mass, const uint32_t* perm, double4* xyzm, size_t n,
+                        cudaStream_t s);
+void launch_pack_identity(const double* pos3, const double* mass, double4* xyzm, size_t n, cudaStream_t s);
+void launch_iota(uint32_t* out, size_t n, cudaStream_t s);
+
+// ---- walk.cu ----------------------------------------------------------------
+struct WalkParams {
+    double G, eps, dacc, theta;
+    uint32_t frontier_cap;    // 0 = unchecked (cap cannot bind)
+    int count_ops;
+    int force_geometric;      // 1: geometric MAC for every group
+};
+struct WalkBuffers {
+    const uint32_t* sinks;    // [n_sinks] sorted particle indices
+    const uint32_t* n_sinks;  // device scalar
+    GroupRec* groups;         // [cap]
+    uint32_t* n_groups;       // device scalar (written by group setup)
+    float4* accum;            // [n_sinks] ax, ay, az, pot (zeroed by the walk launcher)
+    unsigned long long* events;  // [3]
+    uint64_t* queue;          // task queue
+    uint32_t queue_cap;
+    uint32_t* qstate;         // [4]: head, tail, pending, pad
+    uint32_t* spill;          // per-warp stack spill
+    uint32_t* level_count;    // [n_groups * 22] frontier-cap check (nullable)
+    uint64_t* group_inter;    // [n_groups] per-group interactions (nullable)
+    uint32_t group_lo, group_hi;  // shard of groups to walk (hi = ~0u: all)
+};
+size_t walk_spill_words();
+size_t walk_resident_warps();
+void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffers& b, uint32_t group_size,
+                   uint32_t n_sinks_cap, cudaStream_t s);
+void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
+                 DevFlags* flags, cudaStream_t s);
+// acc_out/pot_out in sorted order for the sinks (FP64)
+void launch_walk_finalize(const WalkBuffers& b, uint32_t n_sinks_cap, double* ax, double* ay, double* az,
+                          double* pot, cudaStream_t s);
+
+// ---- integrate.cu -------------------------------------------------------------
+void launch_direct_sum(const double4* xyzm, size_t n, double G, double eps, double* ax, double* ay, double* az,
+                       DevFlags* flags, cudaStream_t s);
+void launch_norm3(const double* ax, const double* ay, const double* az, double* out, size_t n, cudaStream_t s);
+struct StepState {
+    double4* xyzm;
+    double *vx, *vy, *vz, *ax, *ay, *az, *amag;
+    uint8_t* level;
+    uint64_t* last_update;
+};
+void launch_tnext(const StepState& st, size_t n, unsigned long long* t_next, cudaStream_t s);
+void launch_predict(const StepState& st, size_t n, const unsigned long long* t_next, uint64_t now, double tick,
+                    uint8_t* active_flag, cudaStream_t s);
+// stream compaction of flags into sinks (order preserving), count into *n_out
+void launch_compact(const uint8_t* flags, size_t n, uint32_t* out, uint32_t* n_out, uint64_t* status,
+                    uint32_t* counter, cudaStream_t s);
+struct SchemeDev {
+    double eta, dt_max, eps;
+    int adaptive, fixed_level;
+};
+void launch_correct(const StepState& st, const uint32_t* sinks, const uint32_t* n_sinks, uint32_t n_cap,
+                    const double* nax, const double* nay, const double* naz, const unsigned long long* t_next,
+                    uint64_t now, double tick, SchemeDev sc, cudaStream_t s);
+void launch_assign_levels(const StepState& st, size_t n, SchemeDev sc, cudaStream_t s);
+// free-function forms used by the C-ABI parity entry points
+void launch_block_levels(const double* acc_mag, size_t n, SchemeDev sc, int* levels, cudaStream_t s);
+void launch_predict_aos(double* pos3, double* vel3, const double* acc3, size_t n, double dt, cudaStream_t s);
+
+}  // namespace g2

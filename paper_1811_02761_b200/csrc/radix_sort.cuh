@@ -1,0 +1,34 @@
+// CUB-free stable LSD radix sort of (key, u32 payload) pairs for sm_100a.
+//
+// Replaces std::sort of (key, index) pairs in build_tree (octree.cpp:60-63):
+// a stable LSD sort from the identity order equals the lexicographic
+// (key, index) pair sort, so keys/perm are bit-identical to the reference.
+//
+// One histogram pass computes all digit histograms, then one "onesweep"
+// kernel per 8-bit digit: each CTA ranks a 4096-key tile in shared memory
+// (warp-striped loads, __match_any_sync ranking => stable), publishes its
+// per-digit counts through a decoupled look-back status array, and scatters
+// through shared memory so global writes are digit-contiguous.
+// Algorithmic traffic per pass: read key+value, write key+value (24 B per
+// u64 pair), plus 8 B per key for the histogram pass.
+#pragma once
+
+#include "common.cuh"
+
+namespace g2 {
+
+struct SortScratch {
+    DBuf<uint32_t> hist;    // passes * 256 digit counts
+    DBuf<uint32_t> status;  // tiles * 256 look-back words + tile counter
+    size_t tiles_cap = 0;
+};
+
+// Sorts keys[0,n) (bits [0, key_bits)) carrying vals (identity => the input
+// payload is 0..n-1 and `vals` is not read).  Ping-pongs between
+// (keys, vals) and (keys_alt, vals_alt), all four valid buffers of n
+// elements; returns true if the result ended in the *_alt buffers.
+template <typename K>
+bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, size_t n, int key_bits,
+                      bool identity, SortScratch& scratch, cudaStream_t stream);
+
+}  // namespace g2

@@ -1,0 +1,352 @@
+// makeTree and calcNode on sm_100a: bounding cube, Morton keys, level-by-level
+// split, deepest-first node attributes.  All FP64 arithmetic uses explicit
+// round-to-nearest intrinsics in the reference's operation order, so the
+// cube, keys, cells and node attributes are bit-identical to
+// gravitree's build_tree / calc_node (octree.cpp:24-162, morton.hpp:14-49).
+#include "kernels.cuh"
+
+namespace g2 {
+namespace {
+
+constexpr int kBlock = 256;
+
+// ---- bounding_cube (octree.cpp:24-49) ---------------------------------------
+__global__ void __launch_bounds__(kBlock) bbox_partial_kernel(const double4* __restrict__ xyzm, size_t n,
+                                                               double* __restrict__ partials, DevFlags* flags) {
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    bool bad = false;
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock) {
+        const double4 p = xyzm[i];
+        bad |= !(isfinite(p.x) && isfinite(p.y) && isfinite(p.z));
+        lo[0] = smin(lo[0], p.x), lo[1] = smin(lo[1], p.y), lo[2] = smin(lo[2], p.z);
+        hi[0] = smax(hi[0], p.x), hi[1] = smax(hi[1], p.y), hi[2] = smax(hi[2], p.z);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->data_error = 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = smin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = smax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+    __shared__ double sh[kBlock / 32][6];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+        for (int a = 0; a < 3; ++a) sh[w][a] = lo[a], sh[w][3 + a] = hi[a];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double v = sh[0][threadIdx.x];
+        for (int k = 1; k < kBlock / 32; ++k)
+            v = threadIdx.x < 3 ? smin(v, sh[k][threadIdx.x]) : smax(v, sh[k][threadIdx.x]);
+        partials[blockIdx.x * 6 + threadIdx.x] = v;
+    }
+}
+
+__global__ void bbox_final_kernel(const double* __restrict__ partials, int nb, Cube* cube) {
+    if (threadIdx.x != 0) return;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int b = 0; b < nb; ++b)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = smin(lo[a], partials[6 * b + a]);
+            hi[a] = smax(hi[a], partials[6 * b + 3 + a]);
+        }
+    double c[3];
+    for (int a = 0; a < 3; ++a) c[a] = dmul(dadd(lo[a], hi[a]), 0.5);  // 0.5 * (lo + hi)
+    const double d[6] = {dsub(lo[0], c[0]), dsub(hi[0], c[0]), dsub(lo[1], c[1]),
+                         dsub(hi[1], c[1]), dsub(lo[2], c[2]), dsub(hi[2], c[2])};
+    double h = 0.0;
+    for (int k = 0; k < 6; ++k) h = smax(h, fabs(d[k]));
+    double half = dmul(h, 1.0 + 1e-12);
+    if (half == 0.0) half = 1.0;  // all particles coincident
+    *cube = Cube{c[0], c[1], c[2], half};
+}
+
+// ---- morton_key (morton.hpp:14-44) --------------------------------------------
+__device__ __forceinline__ uint64_t expand_bits(uint64_t v) {
+    v &= 0x1fffff;
+    v = (v | v << 32) & 0x001f00000000ffffULL;
+    v = (v | v << 16) & 0x001f0000ff0000ffULL;
+    v = (v | v << 8) & 0x100f00f00f00f00fULL;
+    v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
+    v = (v | v << 2) & 0x1249249249249249ULL;
+    return v;
+}
+
+__device__ __forceinline__ uint64_t quantize(double v, double lo, double width) {
+    const double t = dmul(ddiv(dsub(v, lo), width), 2097152.0);
+    if (t <= 0.0) return 0;
+    const unsigned long long q = __double2ull_rz(t);
+    return q > 2097151ull ? 2097151ull : q;
+}
+
+__global__ void __launch_bounds__(kBlock) keys_kernel(const double4* __restrict__ xyzm,
+                                                      const uint32_t* __restrict__ id_of_pos, size_t n,
+                                                      const Cube* __restrict__ cube, uint64_t* __restrict__ key_by_id,
+                                                      DevFlags* flags) {
+    const Cube c = *cube;
+    const double lox = dsub(c.cx, c.half), loy = dsub(c.cy, c.half), loz = dsub(c.cz, c.half);
+    const double hix = dadd(c.cx, c.half), hiy = dadd(c.cy, c.half), hiz = dadd(c.cz, c.half);
+    const double width = dmul(2.0, c.half);
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock) {
+        const double4 p = xyzm[i];
+        const bool inside = p.x >= lox && p.x <= hix && p.y >= loy && p.y <= hiy && p.z >= loz && p.z <= hiz;
+        if (!inside) flags->data_error = 2;
+        const uint64_t key = (expand_bits(quantize(p.x, lox, width)) << 2) |
+                             (expand_bits(quantize(p.y, loy, width)) << 1) | expand_bits(quantize(p.z, loz, width));
+        key_by_id[id_of_pos ? id_of_pos[i] : i] = key;
+    }
+}
+
+// ---- level-by-level split (octree.cpp:74-102) ------------------------------------
+// One launch per depth d.  A tile is 32 cells x 8 digits (256 threads): the
+// 8 lanes of a cell each binary-search the end of one digit run, exactly the
+// reference's upper_bound per digit.  Children of level d are appended as
+// level d+1 in (parent, digit) order, which is the reference's BFS order;
+// their offsets come from a decoupled look-back scan over the tiles.
+__device__ __forceinline__ unsigned digit_at(uint64_t key, int depth) {
+    return unsigned(key >> (3 * (kMortonBits - 1 - depth))) & 7u;
+}
+
+__global__ void __launch_bounds__(kBlock) split_level_kernel(SplitArgs a, int d) {
+    __shared__ uint32_t s_tile, s_excl, s_wsum[kBlock / 32];
+    const uint32_t lvl_begin = a.level_start[d], lvl_end = a.level_start[d + 1];
+    const uint32_t ncell = lvl_end - lvl_begin;
+    const uint32_t ntiles = (ncell + 31) / 32;
+    if (lvl_end > a.cell_cap) {  // an earlier level overflowed: host grows the buffers and rebuilds
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.level_start[d + 2] = lvl_end;
+        return;
+    }
+    if (ncell == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.level_start[d + 2] = lvl_end;
+        return;
+    }
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, v = tid & 7;
+    uint64_t* status = a.status + (lvl_begin / 32 + d);  // disjoint slice per level
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(&a.tile_counters[d], 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        __syncthreads();
+        if (tile >= ntiles) break;
+        const uint32_t cell = lvl_begin + tile * 32 + (tid >> 3);
+        const bool in_range = cell < lvl_end;
+        uint32_t first = 0, cnt = 0;
+        if (in_range) first = a.first[cell], cnt = a.count[cell];
+        const bool split = in_range && cnt > a.leaf_cap && d < kMaxDepth;
+        uint32_t ub = first;
+        if (split) {  // upper_bound of digit v in keys[first, first+cnt)
+            uint32_t lo = first, hi = first + cnt;
+            while (lo < hi) {
+                const uint32_t mid = lo + (hi - lo) / 2;
+                if (unsigned(v) < digit_at(a.keys[mid], d))
+                    hi = mid;
+                else
+                    lo = mid + 1;
+            }
+            ub = lo;
+        }
+        uint32_t prev = __shfl_up_sync(0xffffffffu, ub, 1, 8);
+        if (v == 0) prev = first;
+        const bool nonempty = split && ub > prev;
+        const uint32_t bal = __ballot_sync(0xffffffffu, nonempty);
+        const uint32_t grp = (bal >> (lane & ~7)) & 0xffu;
+        const uint32_t nc = __popc(grp);
+        const uint32_t jth = __popc(grp & ((1u << v) - 1u));
+        // exclusive scan of child counts over the tile's 32 cells (value on lane v == 0)
+        uint32_t x = v == 0 ? nc : 0u, inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_wsum[w] = inc;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+#pragma unroll
+        for (int k = 0; k < kBlock / 32; ++k) {
+            const uint32_t t = s_wsum[k];
+            if (k < w) wpre += t;
+            tot += t;
+        }
+        const uint32_t cell_excl = __shfl_sync(0xffffffffu, wpre + inc - x, lane & ~7);
+        if (w == 0) {
+            const uint64_t e = lookback_warp(status, tile, tot);
+            if (lane == 0) s_excl = uint32_t(e);
+        }
+        __syncthreads();
+        const uint32_t base = lvl_end + s_excl + cell_excl;  // first child index
+        if (nonempty) {
+            const uint32_t idx = base + jth;
+            if (idx < a.cell_cap) {
+                a.first_child[idx] = 0;
+                a.child_count[idx] = 0;
+                a.first[idx] = prev;
+                a.count[idx] = ub - prev;
+                a.depth[idx] = uint8_t(d + 1);
+            } else {
+                a.flags->cell_overflow = 1;
+            }
+        }
+        if (in_range && v == 0) {
+            a.first_child[cell] = split ? base : 0u;
+            a.child_count[cell] = split ? nc : 0u;
+        }
+        if (tile == ntiles - 1 && tid == 0) a.level_start[d + 2] = lvl_end + s_excl + tot;
+    }
+}
+
+__global__ void split_init_kernel(SplitArgs a, uint32_t n) {
+    if (threadIdx.x == 0) {
+        a.first_child[0] = 0;
+        a.child_count[0] = 0;
+        a.first[0] = 0;
+        a.count[0] = n;
+        a.depth[0] = 0;
+        a.level_start[0] = 0;
+        a.level_start[1] = 1;
+    }
+}
+
+// ---- calc_node (octree.cpp:108-162), one launch per depth, deepest first ------
+__global__ void __launch_bounds__(kBlock) calc_node_level_kernel(
+    const double4* __restrict__ xyzm, const uint32_t* __restrict__ first_child,
+    const uint32_t* __restrict__ child_count, const uint32_t* __restrict__ first, const uint32_t* __restrict__ count,
+    const uint8_t* __restrict__ depth, const uint32_t* __restrict__ level_start, WNode* __restrict__ nodes, int d) {
+    const uint32_t b = level_start[d], e = level_start[d + 1];
+    for (uint32_t c = b + blockIdx.x * kBlock + threadIdx.x; c < e; c += gridDim.x * kBlock) {
+        const uint32_t cc = child_count[c];
+        WNode nd;
+        double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
+        if (cc == 0) {
+            const uint32_t f = first[c], k1 = f + count[c];
+            for (uint32_t k = f; k < k1; ++k) {
+                const double4 p = xyzm[k];
+                m = dadd(m, p.w);
+                wx = dadd(wx, dmul(p.w, p.x));
+                wy = dadd(wy, dmul(p.w, p.y));
+                wz = dadd(wz, dmul(p.w, p.z));
+            }
+            const double inv = ddiv(1.0, m);
+            nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+            double e2 = 0.0;
+            for (uint32_t k = f; k < k1; ++k) {
+                const double4 p = xyzm[k];
+                e2 = smax(e2, norm2(dsub(p.x, nd.cx), dsub(p.y, nd.cy), dsub(p.z, nd.cz)));
+            }
+            nd.extent = dsqrt(e2);
+            nd.link = f;
+            nd.info = (k1 - f) | kLeafBit;
+        } else {
+            const uint32_t f = first_child[c];
+            for (uint32_t ch = f; ch < f + cc; ++ch) {
+                const WNode q = nodes[ch];
+                m = dadd(m, q.mass);
+                wx = dadd(wx, dmul(q.mass, q.cx));
+                wy = dadd(wy, dmul(q.mass, q.cy));
+                wz = dadd(wz, dmul(q.mass, q.cz));
+            }
+            const double inv = ddiv(1.0, m);
+            nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+            double ext = 0.0;
+            for (uint32_t ch = f; ch < f + cc; ++ch) {
+                const WNode q = nodes[ch];
+                ext = smax(ext, dadd(dsqrt(norm2(dsub(q.cx, nd.cx), dsub(q.cy, nd.cy), dsub(q.cz, nd.cz))), q.extent));
+            }
+            nd.extent = ext;
+            nd.link = f;
+            nd.info = cc | (uint32_t(depth[c]) << 8);  // depth feeds the frontier-cap check
+        }
+        nd.mass = m;
+        nodes[c] = nd;
+    }
+}
+
+// ---- gathers / permutations ----------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(kBlock) gather_kernel(const T* __restrict__ in, const uint32_t* __restrict__ src,
+                                                        T* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
+        out[i] = in[src[i]];
+}
+
+__global__ void __launch_bounds__(kBlock) invert_perm_kernel(const uint32_t* __restrict__ perm,
+                                                             uint32_t* __restrict__ rank, size_t n) {
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
+        rank[perm[i]] = uint32_t(i);
+}
+
+__global__ void __launch_bounds__(kBlock) pack_kernel(const double* __restrict__ pos3, const double* __restrict__ mass,
+                                                      const uint32_t* __restrict__ perm, double4* __restrict__ xyzm,
+                                                      size_t n) {
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock) {
+        const size_t id = perm ? perm[i] : i;
+        xyzm[i] = make_double4(pos3[3 * id], pos3[3 * id + 1], pos3[3 * id + 2], mass[id]);
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) iota_kernel(uint32_t* out, size_t n) {
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
+        out[i] = uint32_t(i);
+}
+
+inline unsigned grid_for(size_t n) { return std::max(1u, std::min<unsigned>(ceil_div(n, kBlock), kNumSMs * 16)); }
+
+}  // namespace
+
+void launch_bbox(const double4* xyzm, size_t n, double* partials, Cube* cube, DevFlags* flags, cudaStream_t s) {
+    const unsigned nb = std::max(1u, std::min<unsigned>(ceil_div(n, kBlock * 4), kNumSMs * 4));
+    G2_COUNT(1), bbox_partial_kernel<<<nb, kBlock, 0, s>>>(xyzm, n, partials, flags);
+    G2_COUNT(1), bbox_final_kernel<<<1, 32, 0, s>>>(partials, int(nb), cube);
+    G2_CUDA(cudaGetLastError());
+}
+
+void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const Cube* cube, uint64_t* key_by_id,
+                 DevFlags* flags, cudaStream_t s) {
+    G2_COUNT(1), keys_kernel<<<grid_for(n), kBlock, 0, s>>>(xyzm, id_of_pos, n, cube, key_by_id, flags);
+    G2_CUDA(cudaGetLastError());
+}
+
+void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
+    G2_COUNT(1), split_init_kernel<<<1, 32, 0, s>>>(a, n);
+    // levels are sized on the device; a fixed persistent grid pulls tiles dynamically
+    for (int d = 0; d < kMaxDepth; ++d) G2_COUNT(1), split_level_kernel<<<kNumSMs * 8, kBlock, 0, s>>>(a, d);
+    G2_CUDA(cudaGetLastError());
+}
+
+void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const uint32_t* child_count,
+                      const uint32_t* first, const uint32_t* count, const uint8_t* depth, const uint32_t* level_start,
+                      WNode* nodes, cudaStream_t s) {
+    for (int d = kMaxDepth; d >= 0; --d)
+        G2_COUNT(1), calc_node_level_kernel<<<kNumSMs * 8, kBlock, 0, s>>>(xyzm, first_child, child_count, first, count, depth,
+                                                              level_start, nodes, d);
+    G2_CUDA(cudaGetLastError());
+}
+
+void launch_gather_d4(const double4* in, const uint32_t* src, double4* out, size_t n, cudaStream_t s) {
+    G2_COUNT(1), gather_kernel<double4><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
+}
+void launch_gather_f64(const double* in, const uint32_t* src, double* out, size_t n, cudaStream_t s) {
+    G2_COUNT(1), gather_kernel<double><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
+}
+void launch_gather_u64(const uint64_t* in, const uint32_t* src, uint64_t* out, size_t n, cudaStream_t s) {
+    G2_COUNT(1), gather_kernel<uint64_t><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
+}
+void launch_gather_u8(const uint8_t* in, const uint32_t* src, uint8_t* out, size_t n, cudaStream_t s) {
+    G2_COUNT(1), gather_kernel<uint8_t><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
+}
+void launch_gather_u32(const uint32_t* in, const uint32_t* src, uint32_t* out, size_t n, cudaStream_t s) {
+    G2_COUNT(1), gather_kernel<uint32_t><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
+}
+void launch_invert_perm(const uint32_t* perm, uint32_t* rank, size_t n, cudaStream_t s) {
+    G2_COUNT(1), invert_perm_kernel<<<grid_for(n), kBlock, 0, s>>>(perm, rank, n);
+}
+void launch_pack_sorted(const double* pos3, const double* mass, const uint32_t* perm, double4* xyzm, size_t n,
+                        cudaStream_t s) {
+    G2_COUNT(1), pack_kernel<<<grid_for(n), kBlock, 0, s>>>(pos3, mass, perm, xyzm, n);
+}
+void launch_pack_identity(const double* pos3, const double* mass, double4* xyzm, size_t n, cudaStream_t s) {
+    G2_COUNT(1), pack_kernel<<<grid_for(n), kBlock, 0, s>>>(pos3, mass, nullptr, xyzm, n);
+}
+void launch_iota(uint32_t* out, size_t n, cudaStream_t s) { G2_COUNT(1), iota_kernel<<<grid_for(n), kBlock, 0, s>>>(out, n); }
+
+}  // namespace g2
