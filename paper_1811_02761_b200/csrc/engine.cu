@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -82,9 +83,10 @@ Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), devic
     n_sinks_.reserve(1);
     n_groups_.reserve(1);
     events_.reserve(3);
-    qstate_.reserve(4);
-    queue_cap_ = 1u << 22;
+    qstate_.reserve(8);
+    queue_cap_ = 1u << 20;
     queue_.reserve(queue_cap_);
+    batch_.reserve(size_t(queue_cap_) * 32);
     G2_CUDA(cudaMemsetAsync(queue_.p, 0xff, size_t(queue_cap_) * sizeof(uint64_t), s_));
     spill_.reserve(walk_resident_warps() * walk_spill_words());
 }
@@ -249,6 +251,7 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     b.accum = accum_.p;
     b.events = events_.p;
     b.queue = queue_.p;
+    b.batch = batch_.p;
     b.queue_cap = queue_cap_;
     b.qstate = qstate_.p;
     b.spill = spill_.p;
@@ -260,6 +263,13 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
         b.level_count = level_count_.p;
     }
     b.group_inter = group_inter_.p;
+    static const char* trace_path = std::getenv("G2_WALK_TRACE");  // development: per-task timeline
+    if (trace_path) {
+        trace_.reserve(2 * (size_t(1) << 23));
+        trace_n_.reserve(1);
+        G2_CUDA(cudaMemsetAsync(trace_n_.p, 0, 4, s_));
+        b.trace = trace_.p, b.trace_n = trace_n_.p, b.trace_cap = 1u << 23;
+    }
     G2_CUDA(cudaMemsetAsync(group_inter_.p, 0, size_t(ng_cap) * 8, s_));
     launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
     WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
@@ -270,6 +280,18 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
             level_count_.p, size_t(ng_cap) * (kMaxDepth + 1), uint32_t(std::min<size_t>(cap, 0xffffffffu)),
             flags_.p);
     if (finalize) launch_walk_finalize(b, n_sinks_cap, ax_s_.p, ay_s_.p, az_s_.p, with_pot ? pot_s_.p : nullptr, s_);
+    if (trace_path) {
+        uint32_t nt = 0;
+        G2_CUDA(cudaMemcpyAsync(&nt, trace_n_.p, 4, cudaMemcpyDeviceToHost, s_));
+        G2_CUDA(cudaStreamSynchronize(s_));
+        nt = std::min(nt, 1u << 23);
+        std::vector<uint4> h(2 * size_t(nt));
+        G2_CUDA(cudaMemcpy(h.data(), trace_.p, h.size() * sizeof(uint4), cudaMemcpyDeviceToHost));
+        if (FILE* f = std::fopen(trace_path, "wb")) {
+            std::fwrite(h.data(), sizeof(uint4), h.size(), f);
+            std::fclose(f);
+        }
+    }
     if (sync_events) read_events(ev);
     return ev;
 }

@@ -116,8 +116,11 @@ private:
     DBuf<float4> accum_;
     DBuf<unsigned long long> events_;
     DBuf<uint64_t> queue_;
+    DBuf<uint32_t> batch_;
     DBuf<uint32_t> qstate_, spill_, level_count_;
     DBuf<uint64_t> group_inter_;
+    DBuf<uint4> trace_;
+    DBuf<uint32_t> trace_n_;
     DBuf<DevFlags> flags_;
     SortScratch sort_;
     uint32_t queue_cap_ = 0;

@@ -81,12 +81,17 @@ struct WalkBuffers {
     uint32_t* n_groups;       // device scalar (written by group setup)
     float4* accum;            // [n_sinks] ax, ay, az, pot (zeroed by the walk launcher)
     unsigned long long* events;  // [3]
-    uint64_t* queue;          // task queue
+    uint64_t* queue;          // donated-task slots: (group << 32) | cell count
+    uint32_t* batch;          // [queue_cap * 32] cells of each donated slot
+    const uint32_t* order;    // initial-task order (heaviest first), nullable
     uint32_t queue_cap;
-    uint32_t* qstate;         // [4]: head, tail, pending, pad
+    uint32_t* qstate;         // [8]: init claimed, donated reserved, pending, n_init, donated consumed
     uint32_t* spill;          // per-warp stack spill
     uint32_t* level_count;    // [n_groups * 22] frontier-cap check (nullable)
     uint64_t* group_inter;    // [n_groups] per-group interactions (nullable)
+    uint4* trace;             // optional per-task trace records (development), 2 x uint4 each
+    uint32_t* trace_n;
+    uint32_t trace_cap;
     uint32_t group_lo, group_hi;  // shard of groups to walk (hi = ~0u: all)
 };
 size_t walk_spill_words();

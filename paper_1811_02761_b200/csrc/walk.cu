@@ -29,16 +29,59 @@ namespace {
 
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
-constexpr int kLcap = 256;                 // interaction-list entries per warp
+constexpr int kLcap = 384;                 // interaction-list entries per warp
 constexpr int kScap = 384;                 // shared stack entries per warp
 constexpr uint32_t kSpillWords = 16384;    // global stack entries per warp
+constexpr int kDonateEvery = 64;           // rounds between donations of a long-running task
 constexpr uint64_t kEmpty = ~0ull;
 constexpr unsigned kFull = 0xffffffffu;
 
+// Interaction list in pair-interleaved layout so the flush runs on packed
+// f32x2 math (FADD2/FFMA2/FMUL2): entries 2p and 2p+1 live in
+//   la[p] = (x_2p, x_2p+1, y_2p, y_2p+1),  lb[p] = (z_2p, z_2p+1, m_2p, m_2p+1).
 struct WarpSmem {
-    float4 list[kLcap];
+    float4 la[kLcap / 2];
+    float4 lb[kLcap / 2];
     uint32_t stack[kScap];
+    uint32_t link[32], cpre[32], lpre[32];  // per-round scratch for the cooperative writers
 };
+
+__device__ __forceinline__ void put_entry(WarpSmem& sm, int pos, float x, float y, float z, float m) {
+    float* a = reinterpret_cast<float*>(&sm.la[pos >> 1]) + (pos & 1);
+    float* b = reinterpret_cast<float*>(&sm.lb[pos >> 1]) + (pos & 1);
+    a[0] = x, a[2] = y, b[0] = z, b[2] = m;
+}
+
+// ---- packed f32x2 helpers (sm_100a PTX) --------------------------------------
+using f2 = unsigned long long;
+__device__ __forceinline__ f2 pk(float lo, float hi) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+    return r;
+}
+__device__ __forceinline__ void upk(f2 v, float& lo, float& hi) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+    f2 d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {  // one MUFU.RSQ, no denormal fix-up
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 
 __device__ __forceinline__ uint32_t ld_vol(const uint32_t* p) {
     uint32_t v;
@@ -49,6 +92,14 @@ __device__ __forceinline__ uint64_t ld_vol64(const uint64_t* p) {
     uint64_t v;
     asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
+}
+__device__ __forceinline__ uint64_t ld_acq64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_rel64(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void st_vol64(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -68,93 +119,160 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t& total) 
 
 // All-pairs burst: every list entry acts on this lane's sink (flush_list,
 // traversal.cpp:61-84).  27 Flop per interaction by the reference convention.
+// Two entries per iteration on packed f32x2 lanes; accumulators are pairs that
+// the caller folds at the end.  cnt may be odd: the pad entry is (0,0,0,m=0).
+struct Acc2 {
+    f2 x, y, z;
+    float ph;
+};
+
 template <bool kPot, bool kEps0>
-__device__ __forceinline__ void flush_list(const float4* __restrict__ list, int cnt, float sx, float sy, float sz,
-                                           float eps2, float& ax, float& ay, float& az, float& ph) {
-#pragma unroll 4
-    for (int e = 0; e < cnt; ++e) {
-        const float4 q = list[e];
-        const float dx = q.x - sx, dy = q.y - sy, dz = q.z - sz;
-        float r2 = fmaf(dx, dx, eps2);
-        r2 = fmaf(dy, dy, r2);
-        r2 = fmaf(dz, dz, r2);
-        float inv = rsqrtf(r2);
-        if (kEps0) inv = r2 > 0.0f ? inv : 0.0f;  // r2 == 0 self term (traversal.cpp:73)
-        const float mi = q.w * inv;
-        const float f = mi * (inv * inv);
-        ax = fmaf(f, dx, ax);
-        ay = fmaf(f, dy, ay);
-        az = fmaf(f, dz, az);
-        if (kPot) {
-            const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            ph -= d2 > 0.0f ? mi : 0.0f;  // self potential excluded (traversal.cpp:78)
+__device__ __forceinline__ void flush_list(const WarpSmem& sm, int cnt, f2 sx, f2 sy, f2 sz, f2 eps2, Acc2& a) {
+    const int np = (cnt + 1) >> 1;
+#pragma unroll 2
+    for (int p = 0; p < np; ++p) {
+        const ulonglong2 A = *reinterpret_cast<const ulonglong2*>(&sm.la[p]);
+        const ulonglong2 B = *reinterpret_cast<const ulonglong2*>(&sm.lb[p]);
+        const f2 dx = sub2(A.x, sx), dy = sub2(A.y, sy), dz = sub2(B.x, sz);
+        f2 r2 = fma2(dx, dx, eps2);
+        r2 = fma2(dy, dy, r2);
+        r2 = fma2(dz, dz, r2);
+        float r0, r1;
+        upk(r2, r0, r1);
+        float i0 = rsqrt_ftz(r0), i1 = rsqrt_ftz(r1);
+        if (kEps0) {  // r2 == 0 self term contributes nothing (traversal.cpp:73)
+            i0 = r0 > 0.0f ? i0 : 0.0f;
+            i1 = r1 > 0.0f ? i1 : 0.0f;
+        }
+        const f2 inv = pk(i0, i1);
+        const f2 mi = mul2(B.y, inv);
+        const f2 f = mul2(mi, mul2(inv, inv));
+        a.x = fma2(f, dx, a.x);
+        a.y = fma2(f, dy, a.y);
+        a.z = fma2(f, dz, a.z);
+        if (kPot) {  // self potential excluded (traversal.cpp:78)
+            float m0, m1, e0, e1;
+            upk(mi, m0, m1);
+            upk(eps2, e0, e1);
+            a.ph -= (r0 - e0 > 0.0f ? m0 : 0.0f) + (r1 - e1 > 0.0f ? m1 : 0.0f);
         }
     }
 }
 
+// upper-bound search over a warp's 32 exclusive prefixes: the lane owning item o
+__device__ __forceinline__ int owner_lane(const uint32_t* pre, uint32_t o) {
+    int s = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+        if (pre[s + step] <= o) s += step;
+    return s;
+}
+
+// Exact FP64 MAC in the reference's operation order (traversal.cpp:40-56).
+__device__ __forceinline__ bool mac_exact(const WNode& nd, const GroupRec& g, const WalkParams& p, double rhs,
+                                          bool geom) {
+    const double dx = dsub(g.cx, nd.cx), dy = dsub(g.cy, nd.cy), dz = dsub(g.cz, nd.cz);
+    const double d = smax(0.0, dsub(dsqrt(norm2(dx, dy, dz)), g.radius));
+    if (d <= 0.0) return false;
+    if (geom) return nd.extent <= dmul(p.theta, d);
+    const double d2 = dmul(d, d);
+    const double lhs = ddiv(dmul(dmul(dmul(p.G, nd.mass), nd.extent), nd.extent), dmul(d2, d2));
+    return lhs <= rhs;
+}
+
 template <bool kPot, bool kEps0, bool kCheck>
-__global__ void __launch_bounds__(kThreads) walk_kernel(TreeView t, WalkParams p, WalkBuffers b, DevFlags* flags) {
+__global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParams p, WalkBuffers b, DevFlags* flags) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[w];
     uint32_t* spill = b.spill + (size_t(blockIdx.x) * kWarps + w) * kSpillWords;
-    uint32_t* q_head = b.qstate;
-    uint32_t* q_tail = b.qstate + 1;
+    // Task sources: the initial tasks (one per group, claimed by counter, in
+    // b.order when given: heaviest first) and the FIFO of donated batches of
+    // (group, up to 32 cells), which has priority so heavy groups are split
+    // while the initial tasks are still draining.
+    uint32_t* q_init = b.qstate;       // initial tasks claimed
+    uint32_t* q_dtail = b.qstate + 1;  // donated slots reserved
     uint32_t* q_pending = b.qstate + 2;
-    const uint32_t ng = b.qstate[3];  // initial tasks (written by walk_init)
+    uint32_t* q_dhead = b.qstate + 4;  // donated slots claimed
+    const uint32_t ng = b.qstate[3];   // initial tasks (written by walk_init)
     const uint32_t glo = b.group_lo;
     const float eps2 = float(p.eps * p.eps);
     const float G = float(p.G);
-    const int donate_below = int(gridDim.x) * kWarps / 4 + 1;
+    const float thetaf = float(p.theta);
 
+    // lane 0 may hold a claimed donated slot that is not written yet ("owed"):
+    // claims are fetch-adds (no CAS retry storms); an owed slot is serviced as
+    // soon as its donor writes it, and initial tasks are taken meanwhile.
+    long long owed = -1;
     while (true) {
         // ---------------- acquire a task
-        uint32_t ti = 0;
-        if (lane == 0) ti = atomicAdd(q_head, 1u);
-        ti = __shfl_sync(kFull, ti, 0);
-        uint32_t grp, root;
-        if (ti < ng) {
-            grp = glo + ti;
-            root = 0;
-        } else {
-            uint64_t e = kEmpty;
-            if (lane == 0) {
-                const uint32_t qi = ti - ng;
-                unsigned backoff = 32;
-                while (true) {
-                    if (qi < b.queue_cap) {
-                        e = ld_vol64(&b.queue[qi]);
-                        if (e != kEmpty) {
-                            st_vol64(&b.queue[qi], kEmpty);  // self-cleaning for the next launch
+        uint64_t e = kEmpty;
+        uint32_t slot = 0;
+        if (lane == 0) {
+            unsigned backoff = 32;
+            while (true) {
+                if (owed >= 0) {
+                    if (owed < (long long)b.queue_cap) {
+                        const uint64_t v = ld_acq64(&b.queue[owed]);
+                        if (v != kEmpty) {
+                            st_vol64(&b.queue[owed], kEmpty);  // self-cleaning for the next launch
+                            e = v;
+                            slot = uint32_t(owed);
+                            owed = -1;
                             break;
                         }
+                        if ((long long)ld_vol(q_dtail) > owed) continue;  // reserved: its donor writes it now
                     }
-                    if (ld_vol(q_pending) == 0) break;
-                    __nanosleep(backoff);
-                    backoff = backoff < 1024 ? backoff * 2 : 1024;
+                } else if (ld_vol(q_dhead) < ld_vol(q_dtail)) {
+                    owed = atomicAdd(q_dhead, 1u);  // donated work first
+                    continue;
                 }
+                if (ld_vol(q_init) < ng) {
+                    const uint32_t i = atomicAdd(q_init, 1u);
+                    if (i < ng) {
+                        e = uint64_t(glo + (b.order ? b.order[i] : i)) << 32;  // (group, root), count 0
+                        break;
+                    }
+                }
+                if (owed < 0) {  // nothing left: wait for the next donation
+                    owed = atomicAdd(q_dhead, 1u);
+                    continue;
+                }
+                if (ld_vol(q_pending) == 0) break;  // no task in flight: nothing can be donated any more
+                __nanosleep(backoff);
+                backoff = backoff < 256 ? backoff * 2 : 256;
             }
-            e = __shfl_sync(kFull, e, 0);
-            if (e == kEmpty) return;
-            grp = uint32_t(e >> 32);
-            root = uint32_t(e);
         }
+        e = __shfl_sync(kFull, e, 0);
+        if (e == kEmpty) return;
+        slot = __shfl_sync(kFull, slot, 0);
+        const uint32_t grp = uint32_t(e >> 32), nbatch = uint32_t(e) & 63u;
 
         // ---------------- group and sinks
+        uint64_t t_begin = 0;
+        if (b.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
         const GroupRec g = b.groups[grp];
         const bool geom = p.force_geometric || g.a_min <= 0.0;  // engine.cpp:66
         const double rhs = dmul(p.dacc, g.a_min);
+        const float rhsf = float(rhs), radf = float(g.radius);
         const bool has_sink = uint32_t(lane) < g.count;
         float sx = 0.f, sy = 0.f, sz = 0.f;
         if (has_sink) {
             const double4 q = t.xyzm[b.sinks[g.first + lane]];
             sx = float(dsub(q.x, g.cx)), sy = float(dsub(q.y, g.cy)), sz = float(dsub(q.z, g.cz));
         }
-        float ax = 0.f, ay = 0.f, az = 0.f, ph = 0.f;
+        const f2 sx2 = pk(sx, sx), sy2 = pk(sy, sy), sz2 = pk(sz, sz), e2 = pk(eps2, eps2);
+        Acc2 acc{0ull, 0ull, 0ull, 0.f};
         uint32_t macs = 0, pushes = 0;
         // logical LIFO = spill[gbase, gtop) (bottom, global) ++ sm.stack[0, ssize) (top, shared)
-        int ssize = 1, gbase = 0, gtop = 0, lsize = 0, iter = 0;
-        if (lane == 0) sm.stack[0] = root;
+        int ssize, gbase = 0, gtop = 0, lsize = 0, iter = 0, last_donation = 0;
+        if (nbatch == 0) {
+            if (lane == 0) sm.stack[0] = 0;  // root
+            ssize = 1;
+        } else {
+            if (uint32_t(lane) < nbatch) sm.stack[lane] = b.batch[size_t(slot) * 32 + lane];
+            ssize = int(nbatch);
+        }
         __syncwarp();
 
         while (ssize + gtop - gbase > 0) {
@@ -175,7 +293,7 @@ __global__ void __launch_bounds__(kThreads) walk_kernel(TreeView t, WalkParams p
             macs += take;
             const bool valid = lane < take;
 
-            // ---- acceleration / geometric MAC, FP64 exact (traversal.cpp:40-56)
+            // ---- MAC: FP32 screen with error bounds, exact FP64 only when undecided
             bool accept = false, leaf = false;
             uint32_t link = 0, info = 0;
             double ncx = 0, ncy = 0, ncz = 0, nm = 0;
@@ -184,24 +302,51 @@ __global__ void __launch_bounds__(kThreads) walk_kernel(TreeView t, WalkParams p
                 link = nd.link, info = nd.info;
                 leaf = (info & kLeafBit) != 0;
                 ncx = nd.cx, ncy = nd.cy, ncz = nd.cz, nm = nd.mass;
-                const double dx = dsub(g.cx, nd.cx), dy = dsub(g.cy, nd.cy), dz = dsub(g.cz, nd.cz);
-                const double d = smax(0.0, dsub(dsqrt(norm2(dx, dy, dz)), g.radius));
-                if (d > 0.0) {
+                const float fx = float(dsub(g.cx, nd.cx)), fy = float(dsub(g.cy, nd.cy)), fz = float(dsub(g.cz, nd.cz));
+                const float S = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
+                const float D = S > 0.f ? S * rsqrt_ftz(S) : 0.f;
+                const float d32 = D - radf;
+                // |d32 - d_fp64| <= ~6e-7 (D + R); 4e-6 leaves a 7x margin
+                const float tolabs = 4e-6f * (D + radf);
+                int verdict = 2;  // 0 reject, 1 accept, 2 undecided
+                if (d32 <= -tolabs) {
+                    verdict = 0;  // d <= 0: descend (traversal.cpp:46)
+                } else if (d32 > tolabs) {
+                    const float rel = tolabs / d32;
                     if (geom) {
-                        accept = nd.extent <= dmul(p.theta, d);
+                        const float lhs = float(nd.extent), r = thetaf * d32, tol = rel + 1e-6f;
+                        verdict = lhs <= r * (1.f - tol) ? 1 : (lhs > r * (1.f + tol) ? 0 : 2);
                     } else {
-                        const double d2 = dmul(d, d);
-                        const double lhs = ddiv(dmul(dmul(dmul(p.G, nd.mass), nd.extent), nd.extent), dmul(d2, d2));
-                        accept = lhs <= rhs;
+                        const float ext = float(nd.extent), d2 = d32 * d32;
+                        const float lhs = __fdividef(G * float(nd.mass) * ext * ext, d2 * d2);
+                        const float tol = 4.f * rel + 1e-5f;
+                        if (tol < 0.25f && lhs < 1e30f)
+                            verdict = lhs <= rhsf * (1.f - tol) ? 1 : (lhs > rhsf * (1.f + tol) ? 0 : 2);
                     }
                 }
+                accept = verdict == 2 ? mac_exact(nd, g, p, rhs, geom) : verdict == 1;
             }
-            const uint32_t npush = valid ? (accept ? 1u : (leaf ? (info & ~kLeafBit) : 0u)) : 0u;
+            const uint32_t nnode = (valid && accept) ? 1u : 0u;
+            const uint32_t nleaf = (valid && !accept && leaf) ? (info & ~kLeafBit) : 0u;
             const uint32_t nchild = (valid && !accept && !leaf) ? (info & 0xffu) : 0u;
+            const uint32_t nfast = nleaf <= 8u ? nleaf : 0u;  // oversized leaves take the slow path below
 
-            // ---- rejected internal cells: children onto the stack
-            uint32_t ctot;
-            const uint32_t cofs = warp_excl_scan(nchild, ctot);
+            // one packed scan: children | accepted nodes << 10 | leaf particles << 20
+            const uint32_t v = nchild | (nnode << 10) | (nfast << 20);
+            uint32_t inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(kFull, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const uint32_t tot = __shfl_sync(kFull, inc, 31), exc = inc - v;
+            const uint32_t ctot = tot & 1023u, ntot = (tot >> 10) & 1023u, ltot = tot >> 20;
+            sm.link[lane] = link;
+            sm.cpre[lane] = exc & 1023u;
+            sm.lpre[lane] = exc >> 20;
+            __syncwarp();
+
+            // ---- rejected internal cells: children onto the stack (cooperative)
             if (ctot) {
                 if (kCheck && nchild)
                     atomicAdd(&b.level_count[size_t(grp - glo) * (kMaxDepth + 1) + ((info >> 8) & 31u) + 1u], nchild);
@@ -211,9 +356,9 @@ __global__ void __launch_bounds__(kThreads) walk_kernel(TreeView t, WalkParams p
                     if (gtop + ssize > int(kSpillWords) && gbase > 0) {  // compact the deque
                         for (int i0 = 0; i0 < gtop - gbase; i0 += 32) {
                             const int i = i0 + lane;
-                            const uint32_t v = i < gtop - gbase ? spill[gbase + i] : 0u;
+                            const uint32_t x = i < gtop - gbase ? spill[gbase + i] : 0u;
                             __syncwarp();
-                            if (i < gtop - gbase) spill[i] = v;
+                            if (i < gtop - gbase) spill[i] = x;
                             __syncwarp();
                         }
                         gtop -= gbase;
@@ -229,37 +374,57 @@ __global__ void __launch_bounds__(kThreads) walk_kernel(TreeView t, WalkParams p
                     __syncwarp();
                 }
                 if (ssize + int(ctot) <= kScap) {
-                    for (uint32_t j = 0; j < nchild; ++j) sm.stack[ssize + cofs + j] = link + j;
+                    for (uint32_t o = lane; o < ctot; o += 32) {
+                        const int s = owner_lane(sm.cpre, o);
+                        sm.stack[ssize + o] = sm.link[s] + (o - sm.cpre[s]);
+                    }
                     ssize += int(ctot);
                 }
             }
 
-            // ---- accepted cells and opened leaves: interaction-list entries
-            uint32_t ptot;
-            const uint32_t pofs = warp_excl_scan(npush, ptot);
-            pushes += ptot;
-            if (ptot) {
-                int pos = lsize + int(pofs), end_all = lsize + int(ptot);
+            // ---- accepted cells (owner lanes) and opened leaves (cooperative): list entries
+            const uint32_t P = ntot + ltot;
+            if (P) {
+                if (lsize + int(P) > kLcap) {
+                    if ((lsize & 1) && lane == 0) put_entry(sm, lsize, 0.f, 0.f, 0.f, 0.f);
+                    __syncwarp();
+                    flush_list<kPot, kEps0>(sm, lsize, sx2, sy2, sz2, e2, acc);
+                    __syncwarp();
+                    lsize = 0;
+                }
+                if (nnode)
+                    put_entry(sm, lsize + int((exc >> 10) & 1023u), float(dsub(ncx, g.cx)), float(dsub(ncy, g.cy)),
+                              float(dsub(ncz, g.cz)), float(nm));
+                for (uint32_t o = lane; o < ltot; o += 32) {
+                    const int s = owner_lane(sm.lpre, o);
+                    const double4 q = t.xyzm[sm.link[s] + (o - sm.lpre[s])];
+                    put_entry(sm, lsize + int(ntot + o), float(dsub(q.x, g.cx)), float(dsub(q.y, g.cy)),
+                              float(dsub(q.z, g.cz)), float(q.w));
+                }
+                lsize += int(P);
+                pushes += P;
+            }
+            // ---- oversized leaves (coincident clusters at depth 21, or leaf_cap > 8): divergent writer
+            if (__any_sync(kFull, nleaf > 8u)) {
+                const uint32_t nb = nleaf > 8u ? nleaf : 0u;
+                uint32_t btot;
+                const uint32_t bofs = warp_excl_scan(nb, btot);
+                pushes += btot;
+                int pos = lsize + int(bofs), end_all = lsize + int(btot);
                 uint32_t j = 0;
+                __syncwarp();
                 while (true) {
-                    for (; j < npush && pos + int(j) < kLcap; ++j) {
-                        float4 en;
-                        if (accept) {
-                            en = make_float4(float(dsub(ncx, g.cx)), float(dsub(ncy, g.cy)), float(dsub(ncz, g.cz)),
-                                             float(nm));
-                        } else {
-                            const double4 q = t.xyzm[link + j];
-                            en = make_float4(float(dsub(q.x, g.cx)), float(dsub(q.y, g.cy)), float(dsub(q.z, g.cz)),
-                                             float(q.w));
-                        }
-                        sm.list[pos + j] = en;
+                    for (; j < nb && pos + int(j) < kLcap; ++j) {
+                        const double4 q = t.xyzm[link + j];
+                        put_entry(sm, pos + int(j), float(dsub(q.x, g.cx)), float(dsub(q.y, g.cy)),
+                                  float(dsub(q.z, g.cz)), float(q.w));
                     }
                     if (end_all < kLcap) {
                         lsize = end_all;
                         break;
                     }
                     __syncwarp();
-                    flush_list<kPot, kEps0>(sm.list, kLcap, sx, sy, sz, eps2, ax, ay, az, ph);
+                    flush_list<kPot, kEps0>(sm, kLcap, sx2, sy2, sz2, e2, acc);
                     __syncwarp();
                     pos -= kLcap;
                     end_all -= kLcap;
@@ -271,58 +436,65 @@ __global__ void __launch_bounds__(kThreads) walk_kernel(TreeView t, WalkParams p
             }
             __syncwarp();
 
-            // ---- donate from the logical bottom (shallowest cells = largest subtrees)
-            // when the queue runs dry: splits heavy groups across warps
+            // ---- donate one batch from the logical bottom (shallowest cells = largest
+            // subtrees) every kDonateEvery rounds of a long task, or when warps wait idle
             const int live = ssize + gtop - gbase;
             if ((++iter & 3) == 0 && live >= 64) {
                 int k = 0;
-                uint32_t r = 0;
+                uint32_t ds = 0;
                 if (lane == 0) {
-                    const int avail = int(ld_vol(q_tail)) - int(ld_vol(q_head));
-                    if (avail < donate_below) {
-                        k = min(live / 2, 32);
-                        if (gtop == gbase) k = min(k, ssize);
-                        else k = min(k, gtop - gbase);
-                        r = atomicAdd(q_tail, uint32_t(k));
-                        const long long room = (long long)ng + b.queue_cap - r;
-                        k = int(room < 0 ? 0 : (room < k ? room : k));
-                        if (k) {
-                            atomicAdd(q_pending, uint32_t(k));
-                            __threadfence();
+                    const bool heavy = iter - last_donation >= kDonateEvery;
+                    const bool dry = !heavy && ld_vol(q_init) >= ng && ld_vol(q_dhead) > ld_vol(q_dtail);
+                    if (heavy || dry) {
+                        ds = atomicAdd(q_dtail, 1u);
+                        if (ds < b.queue_cap) {
+                            k = min(live / 2, 32);
+                            k = gtop == gbase ? min(k, ssize) : min(k, gtop - gbase);
+                            atomicAdd(q_pending, 1u);
                         }
                     }
                 }
                 k = __shfl_sync(kFull, k, 0);
-                r = __shfl_sync(kFull, r, 0);
-                if (k && gtop > gbase) {
-                    if (lane < k) st_vol64(&b.queue[r - ng + lane], (uint64_t(grp) << 32) | spill[gbase + lane]);
-                    gbase += k;
-                    if (gbase == gtop) gbase = gtop = 0;
+                ds = __shfl_sync(kFull, ds, 0);
+                if (k) {
+                    last_donation = iter;
+                    const bool from_spill = gtop > gbase;
+                    if (lane < k) b.batch[size_t(ds) * 32 + lane] = from_spill ? spill[gbase + lane] : sm.stack[lane];
+                    __threadfence();
                     __syncwarp();
-                } else if (k) {
-                    if (lane < k) st_vol64(&b.queue[r - ng + lane], (uint64_t(grp) << 32) | sm.stack[lane]);
-                    __syncwarp();
-                    for (int base = 0; base < ssize - k; base += 32) {
-                        const int i = base + lane;
-                        const uint32_t v = i < ssize - k ? sm.stack[i + k] : 0u;
-                        __syncwarp();
-                        if (i < ssize - k) sm.stack[i] = v;
-                        __syncwarp();
+                    if (lane == 0) st_rel64(&b.queue[ds], (uint64_t(grp) << 32) | uint32_t(k));
+                    if (from_spill) {
+                        gbase += k;
+                        if (gbase == gtop) gbase = gtop = 0;
+                    } else {
+                        for (int base = 0; base < ssize - k; base += 32) {
+                            const int i = base + lane;
+                            const uint32_t x = i < ssize - k ? sm.stack[i + k] : 0u;
+                            __syncwarp();
+                            if (i < ssize - k) sm.stack[i] = x;
+                            __syncwarp();
+                        }
+                        ssize -= k;
                     }
-                    ssize -= k;
                 }
             }
         }
-        if (lsize) flush_list<kPot, kEps0>(sm.list, lsize, sx, sy, sz, eps2, ax, ay, az, ph);
+        if (lsize) {
+            if ((lsize & 1) && lane == 0) put_entry(sm, lsize, 0.f, 0.f, 0.f, 0.f);  // pad the last pair
+            __syncwarp();
+            flush_list<kPot, kEps0>(sm, lsize, sx2, sy2, sz2, e2, acc);
+        }
         __syncwarp();
 
         // ---------------- results and events
         if (has_sink) {
-            float4* acc = &b.accum[g.first + lane];
-            atomicAdd(&acc->x, G * ax);
-            atomicAdd(&acc->y, G * ay);
-            atomicAdd(&acc->z, G * az);
-            if (kPot) atomicAdd(&acc->w, G * ph);
+            float x0, x1, y0, y1, z0, z1;
+            upk(acc.x, x0, x1), upk(acc.y, y0, y1), upk(acc.z, z0, z1);
+            float4* out = &b.accum[g.first + lane];
+            atomicAdd(&out->x, G * (x0 + x1));
+            atomicAdd(&out->y, G * (y0 + y1));
+            atomicAdd(&out->z, G * (z0 + z1));
+            if (kPot) atomicAdd(&out->w, G * acc.ph);
         }
         if (lane == 0) {
             const unsigned long long inter = (unsigned long long)pushes * g.count;
@@ -332,6 +504,16 @@ __global__ void __launch_bounds__(kThreads) walk_kernel(TreeView t, WalkParams p
                 atomicAdd(&b.events[2], (unsigned long long)pushes);
             }
             if (b.group_inter) atomicAdd(reinterpret_cast<unsigned long long*>(&b.group_inter[grp]), inter);
+            if (b.trace) {
+                uint64_t t_end;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+                const uint32_t ts = atomicAdd(b.trace_n, 1u);
+                if (ts < b.trace_cap) {
+                    b.trace[2 * ts] = make_uint4(uint32_t(t_begin), uint32_t(t_begin >> 32), uint32_t(t_end),
+                                                 uint32_t(t_end >> 32));
+                    b.trace[2 * ts + 1] = make_uint4(grp, nbatch, macs, pushes);
+                }
+            }
             __threadfence();
             atomicSub(q_pending, 1u);
         }
@@ -385,10 +567,11 @@ __global__ void walk_init_kernel(WalkBuffers b) {
         const uint32_t n_groups = *b.n_groups;
         const uint32_t hi = min(b.group_hi, n_groups);
         const uint32_t ng = hi > b.group_lo ? hi - b.group_lo : 0u;
-        b.qstate[0] = 0;
-        b.qstate[1] = ng;
-        b.qstate[2] = ng;
-        b.qstate[3] = ng;
+        b.qstate[0] = 0;   // initial tasks claimed
+        b.qstate[1] = 0;   // donated slots reserved
+        b.qstate[2] = ng;  // tasks pending
+        b.qstate[3] = ng;  // initial tasks
+        b.qstate[4] = 0;   // donated slots consumed
     }
 }
 
