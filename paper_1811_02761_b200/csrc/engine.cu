@@ -51,6 +51,25 @@ __global__ void set_pos_kernel(double4* xyzm, const double* __restrict__ pos3, c
         xyzm[k] = q;
     }
 }
+// the whole per-particle state gathered into the new Morton order in one pass
+struct ReorderArgs {
+    const double* in[7];
+    double* out[7];
+    const uint8_t *lin, *ain;
+    uint8_t *lout, *aout;
+    const uint64_t* tin;
+    uint64_t* tout;
+};
+__global__ void __launch_bounds__(kB) reorder_kernel(ReorderArgs r, const uint32_t* __restrict__ src, size_t n) {
+    for (size_t i = blockIdx.x * size_t(kB) + threadIdx.x; i < n; i += size_t(gridDim.x) * kB) {
+        const uint32_t j = src[i];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) r.out[k][i] = r.in[k][j];
+        r.lout[i] = r.lin[j];
+        r.aout[i] = r.ain[j];
+        r.tout[i] = r.tin[j];
+    }
+}
 __global__ void fill_u8_kernel(uint8_t* p, uint8_t v, size_t n) {
     for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < n; j += size_t(gridDim.x) * kB) p[j] = v;
 }
@@ -167,11 +186,26 @@ void Engine::build(size_t n, const double* mass, const double* pos, bool with_no
     has_tree_ = true;
 }
 
+// development: G2_PHASE_DEBUG=1 prints device sub-phase times of each rebuild
+static bool phase_debug() {
+    static const bool on = std::getenv("G2_PHASE_DEBUG") != nullptr;
+    return on;
+}
+static cudaEvent_t dbg_ev[8];
+static void dbg_mark(int i, cudaStream_t s) {
+    if (!phase_debug()) return;
+    if (!dbg_ev[i]) cudaEventCreate(&dbg_ev[i]);
+    cudaEventRecord(dbg_ev[i], s);
+}
+
 const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur) {
     const size_t n = n_;
+    dbg_mark(0, s_);
     launch_bbox(xyzm_s_.p, n, bbox_part_.p, cube_.p, flags_.p, s_);
     launch_keys(xyzm_s_.p, ids, n, cube_.p, keys_a_.p, flags_.p, s_);  // keys by original id
+    dbg_mark(1, s_);
     sort_keys_identity_payload(n);                                      // perm = original ids in Morton order
+    dbg_mark(2, s_);
     launch_gather_u32(rank_cur, perm_.p, src_.p, n, s_);               // new k <- old position of perm[k]
     launch_gather_d4(xyzm_s_.p, src_.p, xyzm_alt_.p, n, s_);
     swap_xyzm();
@@ -183,15 +217,26 @@ void Engine::split_and_nodes(bool with_nodes) {
     while (true) {
         G2_CUDA(cudaMemsetAsync(level_start_.p, 0, (kMaxDepth + 3) * sizeof(uint32_t), s_));
         G2_CUDA(cudaMemsetAsync(tile_counters_.p, 0, (kMaxDepth + 1) * sizeof(uint32_t), s_));
-        G2_CUDA(cudaMemsetAsync(split_status_.p, 0, (cell_cap_ / 32 + 64) * sizeof(uint64_t), s_));
+        G2_CUDA(cudaMemsetAsync(split_status_.p, 0, (cell_cap_ / 256 + 64) * sizeof(uint64_t), s_));
         SplitArgs a{keys_a_.p,  first_child_.p, child_count_.p, first_.p,
                     count_.p,   depth_.p,       level_start_.p, split_status_.p,
                     tile_counters_.p, uint32_t(cell_cap_), uint32_t(std::min<size_t>(c_.leaf_cap, 0xffffffffu)),
                     flags_.p};
+        dbg_mark(3, s_);
         launch_split(a, uint32_t(n), s_);
+        dbg_mark(4, s_);
         uint32_t ls[kMaxDepth + 3];
         G2_CUDA(cudaMemcpyAsync(ls, level_start_.p, sizeof ls, cudaMemcpyDeviceToHost, s_));
         G2_CUDA(cudaStreamSynchronize(s_));
+        if (phase_debug() && dbg_ev[0]) {
+            float t[4] = {0, 0, 0, 0};
+            cudaEventElapsedTime(&t[0], dbg_ev[0], dbg_ev[1]);
+            cudaEventElapsedTime(&t[1], dbg_ev[1], dbg_ev[2]);
+            cudaEventElapsedTime(&t[2], dbg_ev[2], dbg_ev[3]);
+            cudaEventElapsedTime(&t[3], dbg_ev[3], dbg_ev[4]);
+            std::fprintf(stderr, "[g2 build] bbox+keys %.3f ms  sort %.3f ms  gathers %.3f ms  split %.3f ms\n", t[0],
+                         t[1], t[2], t[3]);
+        }
         const size_t total = ls[kMaxDepth + 1];
         if (total <= cell_cap_) {
             ncells_ = total;
@@ -456,7 +501,7 @@ Simulation::Simulation(size_t n, const double* mass, const double* pos, const do
     cudaStream_t s = eng_.stream();
     for (auto* b : {&vx_, &vy_, &vz_, &ax_, &ay_, &az_, &amag_, &vx2_, &vy2_, &vz2_, &ax2_, &ay2_, &az2_, &amag2_})
         b->reserve(n);
-    level_.reserve(n), level2_.reserve(n), active_.reserve(n);
+    level_.reserve(n), level2_.reserve(n), active_.reserve(n), active2_.reserve(n);
     last_.reserve(n), last2_.reserve(n);
     ids_.reserve(n), ids2_.reserve(n), rank_cur_.reserve(n), sinks_.reserve(n), n_active_.reserve(1);
     compact_ctr_.reserve(1);
@@ -488,16 +533,14 @@ void Simulation::reorder(const uint32_t* src) {
     const size_t n = n_;
     DBuf<double>* pairs[][2] = {{&vx_, &vx2_}, {&vy_, &vy2_}, {&vz_, &vz2_}, {&ax_, &ax2_},
                                 {&ay_, &ay2_}, {&az_, &az2_}, {&amag_, &amag2_}};
-    for (auto& pr : pairs) {
-        launch_gather_f64(pr[0]->p, src, pr[1]->p, n, s);
-        std::swap(pr[0]->p, pr[1]->p);
-    }
-    launch_gather_u8(level_.p, src, level2_.p, n, s);
+    ReorderArgs r;
+    for (int k = 0; k < 7; ++k) r.in[k] = pairs[k][0]->p, r.out[k] = pairs[k][1]->p;
+    r.lin = level_.p, r.lout = level2_.p, r.ain = active_.p, r.aout = active2_.p, r.tin = last_.p, r.tout = last2_.p;
+    G2_COUNT(1), reorder_kernel<<<gridn(n), kB, 0, s>>>(r, src, n);  // one pass over the index for all state
+    for (auto& pr : pairs) std::swap(pr[0]->p, pr[1]->p);
     std::swap(level_.p, level2_.p);
-    launch_gather_u64(last_.p, src, last2_.p, n, s);
+    std::swap(active_.p, active2_.p);
     std::swap(last_.p, last2_.p);
-    launch_gather_u8(active_.p, src, level2_.p, n, s);  // active flags ride along (level2_ as scratch)
-    std::swap(active_.p, level2_.p);
     G2_CUDA(cudaMemcpyAsync(ids_.p, eng_.perm(), n * 4, cudaMemcpyDeviceToDevice, s));
     G2_CUDA(cudaMemcpyAsync(rank_cur_.p, eng_.rank(), n * 4, cudaMemcpyDeviceToDevice, s));
 }

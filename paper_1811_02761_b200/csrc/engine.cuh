@@ -231,7 +231,7 @@ private:
 
     DBuf<double> vx_, vy_, vz_, ax_, ay_, az_, amag_;
     DBuf<double> vx2_, vy2_, vz2_, ax2_, ay2_, az2_, amag2_;
-    DBuf<uint8_t> level_, level2_, active_;
+    DBuf<uint8_t> level_, level2_, active_, active2_;
     DBuf<uint64_t> last_, last2_;
     DBuf<uint32_t> ids_, ids2_, rank_cur_, sinks_, n_active_, compact_ctr_;
     DBuf<uint64_t> compact_status_;

@@ -9,35 +9,7 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;                      // keys per thread
 constexpr int kTile = kThreads * kItems;        // 4096 keys per tile
 constexpr int kWarpItems = 32 * kItems;         // 512 consecutive keys per warp
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagInc = 2u << 30;
-constexpr uint32_t kValMask = (1u << 30) - 1;
 
-template <typename K>
-__global__ void __launch_bounds__(kThreads) histogram_kernel(const K* __restrict__ keys, size_t n, int passes,
-                                                              uint32_t* __restrict__ hist) {
-    __shared__ uint32_t sh[8][256];
-    for (int i = threadIdx.x; i < 8 * 256; i += kThreads) (&sh[0][0])[i] = 0;
-    __syncthreads();
-    for (size_t i = blockIdx.x * size_t(kThreads) + threadIdx.x; i < n; i += size_t(gridDim.x) * kThreads) {
-        const K k = keys[i];
-        for (int p = 0; p < passes; ++p) atomicAdd(&sh[p][(k >> (8 * p)) & 0xff], 1u);
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < passes * 256; i += kThreads) {
-        const uint32_t v = (&sh[0][0])[i];
-        if (v) atomicAdd(&hist[i], v);
-    }
-}
-
-__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_relaxed(uint32_t* p, uint32_t v) {
-    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
 
 // exclusive scan of one value per thread across the 256-thread block
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* warp_tot, uint32_t* total) {
@@ -61,25 +33,94 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t x, uint32_t* warp_t
     return wpre + inc - x;
 }
 
+// ---- per pass: (1) tile digit counts, (2) one exclusive scan over the
+// digit-major (digit, tile) matrix = global offsets, (3) stable scatter.
+// No look-back chains: every tile's offsets are known before it scatters.
+template <typename K>
+__global__ void __launch_bounds__(kThreads) count_kernel(const K* __restrict__ kin, size_t n, int shift,
+                                                         uint32_t* __restrict__ counts, uint32_t tiles) {
+    __shared__ uint32_t h[kWarps][256];  // per-warp histograms: no cross-warp contention
+    const int tid = threadIdx.x, w = tid >> 5;
+    for (int i = tid; i < kWarps * 256; i += kThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+    const size_t base = size_t(blockIdx.x) * kTile;
+    K k[kItems];
+#pragma unroll
+    for (int i = 0; i < kItems; ++i) {
+        const size_t idx = base + size_t(i) * kThreads + tid;
+        k[i] = idx < n ? kin[idx] : K(0);
+    }
+#pragma unroll
+    for (int i = 0; i < kItems; ++i)
+        if (base + size_t(i) * kThreads + tid < n) atomicAdd(&h[w][uint32_t((k[i] >> shift) & 0xff)], 1u);
+    __syncthreads();
+    uint32_t c = 0;
+#pragma unroll
+    for (int ww = 0; ww < kWarps; ++ww) c += h[ww][tid];
+    counts[size_t(tid) * tiles + blockIdx.x] = c;
+}
+
+// exclusive scan of counts[0, m) in place, single pass with decoupled look-back
+constexpr int kScanItems = 16;
+__global__ void __launch_bounds__(kThreads) scan_kernel(uint32_t* __restrict__ counts, size_t m,
+                                                        uint64_t* __restrict__ status, uint32_t* __restrict__ ctr) {
+    __shared__ uint32_t s_tile, s_wsum[kWarps];
+    __shared__ uint64_t s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (tid == 0) s_tile = atomicAdd(ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const size_t base = (size_t(tile) * kThreads + tid) * kScanItems;  // blocked
+    uint32_t v[kScanItems], sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = base + k < m ? counts[base + k] : 0u;
+        sum += v[k];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_wsum[w] = inc;
+    __syncthreads();
+    uint32_t wpre = 0, tot = 0;
+#pragma unroll
+    for (int k = 0; k < kWarps; ++k) {
+        if (k < w) wpre += s_wsum[k];
+        tot += s_wsum[k];
+    }
+    if (w == 0) {
+        const uint64_t e = lookback_warp(status, tile, tot);
+        if (lane == 0) s_excl = e;
+    }
+    __syncthreads();
+    uint32_t run = uint32_t(s_excl) + wpre + inc - sum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k < m) counts[base + k] = run;
+        run += v[k];
+    }
+}
+
 template <typename K, bool kIdentity>
-__global__ void __launch_bounds__(kThreads) onesweep_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
-                                                             K* __restrict__ kout, uint32_t* __restrict__ vout,
-                                                             size_t n, int shift, const uint32_t* __restrict__ hist,
-                                                             uint32_t* __restrict__ status,
-                                                             uint32_t* __restrict__ tile_counter) {
+__global__ void __launch_bounds__(kThreads) scatter_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+                                                           K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                           size_t n, int shift, const uint32_t* __restrict__ offsets,
+                                                           uint32_t tiles) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     K* skeys = reinterpret_cast<K*>(smem_raw);
     uint32_t* svals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * kTile);
     __shared__ uint32_t whist[kWarps][256];
     __shared__ uint32_t s_lofs[256], s_base[256];
     __shared__ uint32_t s_wtot[kWarps];
-    __shared__ uint32_t s_tile;
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
     for (int i = tid; i < kWarps * 256; i += kThreads) (&whist[0][0])[i] = 0;
+    const uint32_t tile = blockIdx.x;
+    s_base[tid] = offsets[size_t(tid) * tiles + tile];
     __syncthreads();
-    const uint32_t tile = s_tile;
     const size_t tile_base = size_t(tile) * kTile;
     const size_t wbase = tile_base + size_t(w) * kWarpItems;
 
@@ -105,7 +146,6 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(const K* __restrict_
         __syncwarp();
     }
     __syncthreads();
-    // per digit (thread = digit): exclusive prefix across warps, tile count
     uint32_t cnt = 0;
 #pragma unroll
     for (int ww = 0; ww < kWarps; ++ww) {
@@ -113,31 +153,8 @@ __global__ void __launch_bounds__(kThreads) onesweep_kernel(const K* __restrict_
         whist[ww][tid] = cnt;
         cnt += c;
     }
-    const uint32_t lofs = block_excl_scan(cnt, s_wtot, nullptr);
-    s_lofs[tid] = lofs;
+    s_lofs[tid] = block_excl_scan(cnt, s_wtot, nullptr);
     __syncthreads();
-    // global digit base for this pass
-    const uint32_t hbase = block_excl_scan(hist[tid], s_wtot + 0, nullptr);
-    // decoupled look-back, one chain per digit
-    uint32_t* st = status + size_t(tile) * 256 + tid;
-    uint32_t excl = 0;
-    if (tile == 0) {
-        st_relaxed(st, kFlagInc | cnt);
-    } else {
-        st_relaxed(st, kFlagAgg | cnt);
-        for (int64_t j = int64_t(tile) - 1; j >= 0; --j) {
-            uint32_t s;
-            do {
-                s = ld_relaxed(status + size_t(j) * 256 + tid);
-            } while ((s & ~kValMask) == 0);
-            excl += s & kValMask;
-            if (s & kFlagInc) break;
-        }
-        st_relaxed(st, kFlagInc | (excl + cnt));
-    }
-    s_base[tid] = hbase + excl;
-    __syncthreads();
-    // scatter into shared memory in digit order
 #pragma unroll
     for (int i = 0; i < kItems; ++i) {
         if (d[i] < 256u) {
@@ -162,8 +179,8 @@ void set_smem_attr() {
     static bool done = false;
     if (done) return;
     const int bytes = int((sizeof(K) + 4) * kTile);
-    G2_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    G2_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    G2_CUDA(cudaFuncSetAttribute(scatter_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    G2_CUDA(cudaFuncSetAttribute(scatter_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     done = true;
 }
 
@@ -175,28 +192,27 @@ bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, 
     if (n == 0) return false;
     set_smem_attr<K>();
     const int passes = (key_bits + 7) / 8;
-    const size_t tiles = (n + kTile - 1) / kTile;
-    sc.hist.reserve(8 * 256);
-    sc.status.reserve(tiles * 256 + 32);
-    G2_CUDA(cudaMemsetAsync(sc.hist.p, 0, 8 * 256 * sizeof(uint32_t), stream));
-    const unsigned hgrid = std::min<unsigned>(ceil_div(n, kThreads * 8), kNumSMs * 8);
-    G2_COUNT(1), histogram_kernel<K><<<hgrid, kThreads, 0, stream>>>(keys, n, passes, sc.hist.p);
-    G2_CUDA(cudaGetLastError());
+    const uint32_t tiles = uint32_t((n + kTile - 1) / kTile);
+    const size_t m = size_t(256) * tiles;                       // digit-major (digit, tile) matrix
+    const size_t stiles = (m + kThreads * kScanItems - 1) / (kThreads * kScanItems);
+    sc.hist.reserve(m);
+    sc.status.reserve(2 * stiles + 64);
+    uint64_t* status = reinterpret_cast<uint64_t*>(sc.status.p);
+    uint32_t* ctr = sc.status.p + 2 * stiles + 32;
     K *ki = keys, *ko = keys_alt;
     uint32_t *vi = vals, *vo = vals_alt;
     bool in_alt = false;
     const int smem = int((sizeof(K) + 4) * kTile);
-    uint32_t* counter = sc.status.p + tiles * 256;
     for (int p = 0; p < passes; ++p) {
-        G2_CUDA(cudaMemsetAsync(sc.status.p, 0, (tiles * 256 + 32) * sizeof(uint32_t), stream));
+        G2_COUNT(1), count_kernel<K><<<tiles, kThreads, 0, stream>>>(ki, n, 8 * p, sc.hist.p, tiles);
+        G2_CUDA(cudaMemsetAsync(sc.status.p, 0, (2 * stiles + 64) * sizeof(uint32_t), stream));
+        G2_COUNT(1), scan_kernel<<<unsigned(stiles), kThreads, 0, stream>>>(sc.hist.p, m, status, ctr);
         if (p == 0 && identity)
-            G2_COUNT(1), onesweep_kernel<K, true><<<unsigned(tiles), kThreads, smem, stream>>>(ki, nullptr, ko, vo, n, 8 * p,
-                                                                                 sc.hist.p + 256 * p, sc.status.p,
-                                                                                 counter);
+            G2_COUNT(1), scatter_kernel<K, true><<<tiles, kThreads, smem, stream>>>(ki, nullptr, ko, vo, n, 8 * p,
+                                                                                   sc.hist.p, tiles);
         else
-            G2_COUNT(1), onesweep_kernel<K, false><<<unsigned(tiles), kThreads, smem, stream>>>(ki, vi, ko, vo, n, 8 * p,
-                                                                                  sc.hist.p + 256 * p, sc.status.p,
-                                                                                  counter);
+            G2_COUNT(1), scatter_kernel<K, false><<<tiles, kThreads, smem, stream>>>(ki, vi, ko, vo, n, 8 * p,
+                                                                                    sc.hist.p, tiles);
         G2_CUDA(cudaGetLastError());
         std::swap(ki, ko);
         std::swap(vi, vo);

@@ -4,13 +4,12 @@
 // a stable LSD sort from the identity order equals the lexicographic
 // (key, index) pair sort, so keys/perm are bit-identical to the reference.
 //
-// One histogram pass computes all digit histograms, then one "onesweep"
-// kernel per 8-bit digit: each CTA ranks a 4096-key tile in shared memory
-// (warp-striped loads, __match_any_sync ranking => stable), publishes its
-// per-digit counts through a decoupled look-back status array, and scatters
-// through shared memory so global writes are digit-contiguous.
-// Algorithmic traffic per pass: read key+value, write key+value (24 B per
-// u64 pair), plus 8 B per key for the histogram pass.
+// Per 8-bit digit pass: a count kernel writes each 4096-key tile's digit
+// histogram into a digit-major matrix, one single-pass look-back scan turns
+// it into global offsets, and a scatter kernel ranks the tile in shared
+// memory (warp-striped loads, __match_any_sync ranking => stable) and writes
+// digit-contiguous runs.  Traffic per pass: read keys (8 B) for the count,
+// read key+value and write key+value (24 B) for the scatter.
 #pragma once
 
 #include "common.cuh"
@@ -18,8 +17,8 @@
 namespace g2 {
 
 struct SortScratch {
-    DBuf<uint32_t> hist;    // passes * 256 digit counts
-    DBuf<uint32_t> status;  // tiles * 256 look-back words + tile counter
+    DBuf<uint32_t> hist;    // 256 x tiles digit-count / offset matrix
+    DBuf<uint32_t> status;  // scan look-back words + tile counter
     size_t tiles_cap = 0;
 };
 

@@ -3,6 +3,8 @@
 // round-to-nearest intrinsics in the reference's operation order, so the
 // cube, keys, cells and node attributes are bit-identical to
 // gravitree's build_tree / calc_node (octree.cpp:24-162, morton.hpp:14-49).
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace g2 {
@@ -43,13 +45,21 @@ __global__ void __launch_bounds__(kBlock) bbox_partial_kernel(const double4* __r
 }
 
 __global__ void bbox_final_kernel(const double* __restrict__ partials, int nb, Cube* cube) {
-    if (threadIdx.x != 0) return;
+    // one warp: min/max are exact in any order
+    const int lane = threadIdx.x;
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int b = 0; b < nb; ++b)
+    for (int b = lane; b < nb; b += 32)
         for (int a = 0; a < 3; ++a) {
             lo[a] = smin(lo[a], partials[6 * b + a]);
             hi[a] = smax(hi[a], partials[6 * b + 3 + a]);
         }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = smin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = smax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+    if (lane != 0) return;
     double c[3];
     for (int a = 0; a < 3; ++a) c[a] = dmul(dadd(lo[a], hi[a]), 0.5);  // 0.5 * (lo + hi)
     const double d[6] = {dsub(lo[0], c[0]), dsub(hi[0], c[0]), dsub(lo[1], c[1]),
@@ -98,11 +108,15 @@ __global__ void __launch_bounds__(kBlock) keys_kernel(const double4* __restrict_
 }
 
 // ---- level-by-level split (octree.cpp:74-102) ------------------------------------
-// One launch per depth d.  A tile is 32 cells x 8 digits (256 threads): the
-// 8 lanes of a cell each binary-search the end of one digit run, exactly the
-// reference's upper_bound per digit.  Children of level d are appended as
-// level d+1 in (parent, digit) order, which is the reference's BFS order;
-// their offsets come from a decoupled look-back scan over the tiles.
+// One launch per depth d, one thread per cell, 256 cells per tile.  A cell is
+// split iff count > leaf_cap and d < 21; its children are the non-empty runs
+// of the depth-d digit among its (sorted) keys, exactly the reference's
+// upper_bound per digit: small cells count digits with one linear pass over
+// their keys, large cells binary-search the 8 run ends.  Children of level d
+// are appended as level d+1 in (parent, digit) order, which is the
+// reference's BFS order; their offsets come from a decoupled look-back scan.
+constexpr uint32_t kLinearMax = 128;  // per-digit counts fit the packed 8-bit fields
+
 __device__ __forceinline__ unsigned digit_at(uint64_t key, int depth) {
     return unsigned(key >> (3 * (kMortonBits - 1 - depth))) & 7u;
 }
@@ -111,49 +125,75 @@ __global__ void __launch_bounds__(kBlock) split_level_kernel(SplitArgs a, int d)
     __shared__ uint32_t s_tile, s_excl, s_wsum[kBlock / 32];
     const uint32_t lvl_begin = a.level_start[d], lvl_end = a.level_start[d + 1];
     const uint32_t ncell = lvl_end - lvl_begin;
-    const uint32_t ntiles = (ncell + 31) / 32;
-    if (lvl_end > a.cell_cap) {  // an earlier level overflowed: host grows the buffers and rebuilds
+    const uint32_t ntiles = (ncell + kBlock - 1) / kBlock;
+    if (lvl_end > a.cell_cap || ncell == 0) {  // overflow (host grows and rebuilds) or empty level
         if (blockIdx.x == 0 && threadIdx.x == 0) a.level_start[d + 2] = lvl_end;
         return;
     }
-    if (ncell == 0) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) a.level_start[d + 2] = lvl_end;
-        return;
-    }
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5, v = tid & 7;
-    uint64_t* status = a.status + (lvl_begin / 32 + d);  // disjoint slice per level
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int shift = 3 * (kMortonBits - 1 - d);
+    uint64_t* status = a.status + (lvl_begin / kBlock + d);  // disjoint slice per level
     while (true) {
         if (tid == 0) s_tile = atomicAdd(&a.tile_counters[d], 1u);
         __syncthreads();
         const uint32_t tile = s_tile;
         __syncthreads();
         if (tile >= ntiles) break;
-        const uint32_t cell = lvl_begin + tile * 32 + (tid >> 3);
+        const uint32_t cell = lvl_begin + tile * kBlock + tid;
         const bool in_range = cell < lvl_end;
         uint32_t first = 0, cnt = 0;
         if (in_range) first = a.first[cell], cnt = a.count[cell];
         const bool split = in_range && cnt > a.leaf_cap && d < kMaxDepth;
-        uint32_t ub = first;
-        if (split) {  // upper_bound of digit v in keys[first, first+cnt)
-            uint32_t lo = first, hi = first + cnt;
-            while (lo < hi) {
-                const uint32_t mid = lo + (hi - lo) / 2;
-                if (unsigned(v) < digit_at(a.keys[mid], d))
-                    hi = mid;
-                else
-                    lo = mid + 1;
+        uint32_t ub[8];  // end of each digit run
+        if (split && cnt <= kLinearMax) {
+            // one pass over the cell's keys, 8 independent loads in flight per chunk
+            uint64_t packed = 0;  // 8-bit count per digit
+            const uint32_t end = first + cnt;
+            for (uint32_t k0 = first; k0 < end; k0 += 8) {
+                uint64_t kk[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) kk[j] = k0 + j < end ? a.keys[k0 + j] : 0ull;
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    if (k0 + j < end) packed += 1ull << (8 * ((kk[j] >> shift) & 7u));
             }
-            ub = lo;
+            uint32_t run = first;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) ub[v] = (run += uint32_t(packed >> (8 * v)) & 0xffu);
+        } else if (split) {
+            // the 8 upper_bound searches advance in lockstep: 8 loads in flight per step
+            uint32_t lo[8], hi[8];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) lo[v] = first, hi[v] = first + cnt;
+            bool busy = true;
+            while (busy) {
+                busy = false;
+                uint64_t kk[8];
+#pragma unroll
+                for (int v = 0; v < 8; ++v) kk[v] = lo[v] < hi[v] ? a.keys[lo[v] + (hi[v] - lo[v]) / 2] : 0ull;
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    if (lo[v] < hi[v]) {
+                        const uint32_t mid = lo[v] + (hi[v] - lo[v]) / 2;
+                        if (unsigned(v) < unsigned((kk[v] >> shift) & 7u))
+                            hi[v] = mid;
+                        else
+                            lo[v] = mid + 1;
+                        busy |= lo[v] < hi[v];
+                    }
+                }
+            }
+#pragma unroll
+            for (int v = 0; v < 8; ++v) ub[v] = lo[v];
+        } else {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) ub[v] = first;
         }
-        uint32_t prev = __shfl_up_sync(0xffffffffu, ub, 1, 8);
-        if (v == 0) prev = first;
-        const bool nonempty = split && ub > prev;
-        const uint32_t bal = __ballot_sync(0xffffffffu, nonempty);
-        const uint32_t grp = (bal >> (lane & ~7)) & 0xffu;
-        const uint32_t nc = __popc(grp);
-        const uint32_t jth = __popc(grp & ((1u << v) - 1u));
-        // exclusive scan of child counts over the tile's 32 cells (value on lane v == 0)
-        uint32_t x = v == 0 ? nc : 0u, inc = x;
+        uint32_t nc = 0;
+#pragma unroll
+        for (int v = 0; v < 8; ++v) nc += ub[v] > (v ? ub[v - 1] : first) ? 1u : 0u;
+        // exclusive scan of child counts over the tile
+        uint32_t inc = nc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
@@ -168,26 +208,32 @@ __global__ void __launch_bounds__(kBlock) split_level_kernel(SplitArgs a, int d)
             if (k < w) wpre += t;
             tot += t;
         }
-        const uint32_t cell_excl = __shfl_sync(0xffffffffu, wpre + inc - x, lane & ~7);
         if (w == 0) {
             const uint64_t e = lookback_warp(status, tile, tot);
             if (lane == 0) s_excl = uint32_t(e);
         }
         __syncthreads();
-        const uint32_t base = lvl_end + s_excl + cell_excl;  // first child index
-        if (nonempty) {
-            const uint32_t idx = base + jth;
-            if (idx < a.cell_cap) {
-                a.first_child[idx] = 0;
-                a.child_count[idx] = 0;
-                a.first[idx] = prev;
-                a.count[idx] = ub - prev;
-                a.depth[idx] = uint8_t(d + 1);
-            } else {
-                a.flags->cell_overflow = 1;
+        const uint32_t base = lvl_end + s_excl + wpre + inc - nc;  // first child index
+        if (split) {
+            uint32_t j = 0, lo = first;
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                if (ub[v] > lo) {
+                    const uint32_t idx = base + j++;
+                    if (idx < a.cell_cap) {
+                        a.first_child[idx] = 0;
+                        a.child_count[idx] = 0;
+                        a.first[idx] = lo;
+                        a.count[idx] = ub[v] - lo;
+                        a.depth[idx] = uint8_t(d + 1);
+                    } else {
+                        a.flags->cell_overflow = 1;
+                    }
+                }
+                lo = ub[v];
             }
         }
-        if (in_range && v == 0) {
+        if (in_range) {
             a.first_child[cell] = split ? base : 0u;
             a.child_count[cell] = split ? nc : 0u;
         }
@@ -309,7 +355,25 @@ void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const
 void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
     G2_COUNT(1), split_init_kernel<<<1, 32, 0, s>>>(a, n);
     // levels are sized on the device; a fixed persistent grid pulls tiles dynamically
-    for (int d = 0; d < kMaxDepth; ++d) G2_COUNT(1), split_level_kernel<<<kNumSMs * 8, kBlock, 0, s>>>(a, d);
+    static const bool dbg = std::getenv("G2_SPLIT_DEBUG") != nullptr;  // development: per-level device times
+    static cudaEvent_t ev[kMaxDepth + 1];
+    if (dbg && !ev[0])
+        for (auto& e : ev) cudaEventCreate(&e);
+    for (int d = 0; d < kMaxDepth; ++d) {
+        if (dbg) cudaEventRecord(ev[d], s);
+        G2_COUNT(1), split_level_kernel<<<kNumSMs * 4, kBlock, 0, s>>>(a, d);
+    }
+    if (dbg) {
+        cudaEventRecord(ev[kMaxDepth], s);
+        cudaEventSynchronize(ev[kMaxDepth]);
+        uint32_t ls[kMaxDepth + 3];
+        cudaMemcpy(ls, a.level_start, sizeof ls, cudaMemcpyDeviceToHost);
+        for (int d = 0; d < kMaxDepth; ++d) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[d], ev[d + 1]);
+            std::fprintf(stderr, "[g2 split] depth %2d cells %8u  %.3f ms\n", d, ls[d + 1] - ls[d], ms);
+        }
+    }
     G2_CUDA(cudaGetLastError());
 }
 

@@ -77,6 +77,11 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
     return d;
 }
+__device__ __forceinline__ float rcp_ftz(float x) {  // one MUFU.RCP
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float rsqrt_ftz(float x) {  // one MUFU.RSQ, no denormal fix-up
     float r;
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -312,16 +317,17 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
                 if (d32 <= -tolabs) {
                     verdict = 0;  // d <= 0: descend (traversal.cpp:46)
                 } else if (d32 > tolabs) {
-                    const float rel = tolabs / d32;
+                    const float rel = tolabs * rcp_ftz(d32);
                     if (geom) {
                         const float lhs = float(nd.extent), r = thetaf * d32, tol = rel + 1e-6f;
                         verdict = lhs <= r * (1.f - tol) ? 1 : (lhs > r * (1.f + tol) ? 0 : 2);
                     } else {
+                        // G m b^2 / d^4 <= rhs  <=>  G m b^2 <= rhs d^4  (no division)
                         const float ext = float(nd.extent), d2 = d32 * d32;
-                        const float lhs = __fdividef(G * float(nd.mass) * ext * ext, d2 * d2);
+                        const float num = G * float(nd.mass) * ext * ext, den = rhsf * (d2 * d2);
                         const float tol = 4.f * rel + 1e-5f;
-                        if (tol < 0.25f && lhs < 1e30f)
-                            verdict = lhs <= rhsf * (1.f - tol) ? 1 : (lhs > rhsf * (1.f + tol) ? 0 : 2);
+                        if (tol < 0.25f && den > 1e-30f)
+                            verdict = num <= den * (1.f - tol) ? 1 : (num > den * (1.f + tol) ? 0 : 2);
                     }
                 }
                 accept = verdict == 2 ? mac_exact(nd, g, p, rhs, geom) : verdict == 1;
@@ -342,7 +348,6 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
             const uint32_t tot = __shfl_sync(kFull, inc, 31), exc = inc - v;
             const uint32_t ctot = tot & 1023u, ntot = (tot >> 10) & 1023u, ltot = tot >> 20;
             sm.link[lane] = link;
-            sm.cpre[lane] = exc & 1023u;
             sm.lpre[lane] = exc >> 20;
             __syncwarp();
 
@@ -373,11 +378,11 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
                     }
                     __syncwarp();
                 }
-                if (ssize + int(ctot) <= kScap) {
-                    for (uint32_t o = lane; o < ctot; o += 32) {
-                        const int s = owner_lane(sm.cpre, o);
-                        sm.stack[ssize + o] = sm.link[s] + (o - sm.cpre[s]);
-                    }
+                if (ssize + int(ctot) <= kScap) {  // <= 8 children per lane: a short predicated loop
+                    uint32_t* dst = sm.stack + ssize + (exc & 1023u);
+#pragma unroll
+                    for (uint32_t j = 0; j < 8; ++j)
+                        if (j < nchild) dst[j] = link + j;
                     ssize += int(ctot);
                 }
             }
