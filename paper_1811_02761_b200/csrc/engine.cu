@@ -35,9 +35,10 @@ __global__ void gather_scalar_kernel(const double* __restrict__ in, const uint32
     for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < n; j += size_t(gridDim.x) * kB)
         out[j] = in[idx ? idx[j] : j];
 }
-__global__ void xyzm_to_pos3_kernel(const double4* __restrict__ xyzm, double* pos3, size_t n) {
+__global__ void xyzm_to_pos3_kernel(const double4* __restrict__ xyzm, const uint32_t* __restrict__ idx, double* pos3,
+                                    size_t n) {
     for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < n; j += size_t(gridDim.x) * kB) {
-        const double4 q = xyzm[j];
+        const double4 q = xyzm[idx ? idx[j] : j];
         pos3[3 * j] = q.x, pos3[3 * j + 1] = q.y, pos3[3 * j + 2] = q.z;
     }
 }
@@ -666,39 +667,34 @@ StepResultH Simulation::step() {
 
 void Simulation::get_state(double* pos, double* vel, double* acc, double* acc_old_mag, uint8_t* level,
                            double* time) {
+    // gathers into the caller's (original) particle order on the device, then one
+    // D2H per array straight into the caller's buffer (pinned buffers stream at full speed)
     cudaStream_t s = eng_.stream();
     const size_t n = n_;
-    std::vector<uint32_t> ids(n);
-    G2_CUDA(cudaMemcpyAsync(ids.data(), ids_.p, n * 4, cudaMemcpyDeviceToHost, s));
-    DBuf<double> tmp;
-    tmp.reserve(3 * n);
-    std::vector<double> h(3 * n);
-    auto fetch3 = [&](const double* x, const double* y, const double* z, double* out) {
-        G2_COUNT(1), interleave_kernel<<<gridn(n), kB, 0, s>>>(x, y, z, nullptr, tmp.p, n);
-        G2_CUDA(cudaMemcpyAsync(h.data(), tmp.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));
-        G2_CUDA(cudaStreamSynchronize(s));
-        for (size_t k = 0; k < n; ++k)
-            for (int a = 0; a < 3; ++a) out[3 * size_t(ids[k]) + a] = h[3 * k + a];
-    };
+    io_.reserve(3 * n);
+    const uint32_t* at = rank_cur_.p;  // original id -> current position
     if (pos) {
-        G2_COUNT(1), xyzm_to_pos3_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), tmp.p, n);
-        G2_CUDA(cudaMemcpyAsync(h.data(), tmp.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));
+        G2_COUNT(1), xyzm_to_pos3_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), at, io_.p, n);
+        G2_CUDA(cudaMemcpyAsync(pos, io_.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));
         G2_CUDA(cudaStreamSynchronize(s));
-        for (size_t k = 0; k < n; ++k)
-            for (int a = 0; a < 3; ++a) pos[3 * size_t(ids[k]) + a] = h[3 * k + a];
     }
+    auto fetch3 = [&](const double* x, const double* y, const double* z, double* out) {
+        G2_COUNT(1), interleave_kernel<<<gridn(n), kB, 0, s>>>(x, y, z, at, io_.p, n);
+        G2_CUDA(cudaMemcpyAsync(out, io_.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));
+        G2_CUDA(cudaStreamSynchronize(s));
+    };
     if (vel) fetch3(vx_.p, vy_.p, vz_.p, vel);
     if (acc) fetch3(ax_.p, ay_.p, az_.p, acc);
     if (acc_old_mag) {
-        G2_CUDA(cudaMemcpyAsync(h.data(), amag_.p, n * 8, cudaMemcpyDeviceToHost, s));
+        G2_COUNT(1), gather_scalar_kernel<<<gridn(n), kB, 0, s>>>(amag_.p, at, io_.p, n);
+        G2_CUDA(cudaMemcpyAsync(acc_old_mag, io_.p, n * 8, cudaMemcpyDeviceToHost, s));
         G2_CUDA(cudaStreamSynchronize(s));
-        for (size_t k = 0; k < n; ++k) acc_old_mag[ids[k]] = h[k];
     }
     if (level) {
-        std::vector<uint8_t> lv(n);
-        G2_CUDA(cudaMemcpyAsync(lv.data(), level_.p, n, cudaMemcpyDeviceToHost, s));
+        launch_gather_u8(level_.p, at, reinterpret_cast<uint8_t*>(io_.p), n, s);
+        G2_COUNT(1);
+        G2_CUDA(cudaMemcpyAsync(level, io_.p, n, cudaMemcpyDeviceToHost, s));
         G2_CUDA(cudaStreamSynchronize(s));
-        for (size_t k = 0; k < n; ++k) level[ids[k]] = lv[k];
     }
     if (time) *time = time_;
 }
@@ -706,15 +702,15 @@ void Simulation::get_state(double* pos, double* vel, double* acc, double* acc_ol
 void Simulation::set_state(const double* pos, const double* vel) {
     cudaStream_t s = eng_.stream();
     const size_t n = n_;
-    DBuf<double> tmp;
-    tmp.reserve(3 * n);
+    io_.reserve(3 * n);
+    io2_.reserve(3 * n);
     if (pos) {
-        G2_CUDA(cudaMemcpyAsync(tmp.p, pos, 3 * n * 8, cudaMemcpyHostToDevice, s));
-        G2_COUNT(1), set_pos_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), tmp.p, ids_.p, n);
+        G2_CUDA(cudaMemcpyAsync(io_.p, pos, 3 * n * 8, cudaMemcpyHostToDevice, s));
+        G2_COUNT(1), set_pos_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), io_.p, ids_.p, n);
     }
     if (vel) {
-        G2_CUDA(cudaMemcpyAsync(tmp.p, vel, 3 * n * 8, cudaMemcpyHostToDevice, s));
-        G2_COUNT(1), deinterleave_kernel<<<gridn(n), kB, 0, s>>>(tmp.p, ids_.p, vx_.p, vy_.p, vz_.p, n);
+        G2_CUDA(cudaMemcpyAsync(io2_.p, vel, 3 * n * 8, cudaMemcpyHostToDevice, s));
+        G2_COUNT(1), deinterleave_kernel<<<gridn(n), kB, 0, s>>>(io2_.p, ids_.p, vx_.p, vy_.p, vz_.p, n);
     }
     G2_CUDA(cudaStreamSynchronize(s));
 }

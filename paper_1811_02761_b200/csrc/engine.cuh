@@ -236,6 +236,7 @@ private:
     DBuf<uint32_t> ids_, ids2_, rank_cur_, sinks_, n_active_, compact_ctr_;
     DBuf<uint64_t> compact_status_;
     DBuf<unsigned long long> t_next_;
+    DBuf<double> io_, io2_;  // host-transfer staging (original particle order)
     cudaEvent_t ev_[12];
 };
 

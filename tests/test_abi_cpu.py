@@ -78,3 +78,15 @@ def test_no_gpu_calls_fail_loudly():
     import paper_1811_02761_b200 as g2
     with pytest.raises(g2.InternalError):
         g2.GravityEngine()
+
+
+@pytest.mark.parametrize("model,n", [("m31", 20001), ("plummer", 3001), ("hernquist", 2048), ("nfw", 999),
+                                     ("disk", 4097)])
+def test_sampler_bit_identical_to_reference(ref, model, n):
+    """The bench input generator (csrc/ics.cpp, multithreaded) reproduces the reference's
+    sample_model (models.cpp:442-460) bit for bit."""
+    from paper_1811_02761_b200.gravitree import sample_model
+    a = ref.sample_model(model, n, 1)
+    b = sample_model(model, n, 1, threads=4)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
