@@ -255,6 +255,11 @@ def run_g2(args):
         per_step, walk_s = float(t[0]), float(t[1])
     r0 = results[-1]
     flops = g2.walk_flops(r0.events)
+    if world > 1:  # each rank counted its own shard of the groups
+        import torch.distributed as dist
+        t = torch.tensor([flops], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        flops = float(t[0])
     peaks = measured_peaks()
     f_max = float(peaks.get("sm_max_mhz", 1965.0))
     fp32_peak = 148 * 128 * 2 * f_max * 1e6 / 1e12  # TFLOP/s

@@ -150,6 +150,9 @@ int g2_nccl_unique_id(unsigned char id[128]);
 /* join a communicator; the simulation then walks only its shard of sink
  * groups and all-gathers the new accelerations each step */
 int g2_sim_set_mesh(g2_sim* s, int rank, int world, const unsigned char id[128]);
+/* in-process mesh: sims[0..world) (one host thread per step call, any devices)
+ * shard the sink groups and exchange accelerations by device copies */
+int g2_sim_set_mesh_local(g2_sim** sims, int world);
 
 #ifdef __cplusplus
 }

@@ -3,7 +3,10 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
+#include <vector>
 #include <memory>
 #include <string>
 
@@ -103,29 +106,79 @@ __global__ void unpack_kernel(const float4* __restrict__ gathered, float4* __res
     }
 }
 
-// One ncclAllGather of the walk's FP32 accumulator slots per step:
-// rank r owns slots [lo_r*gs, hi_r*gs); each sends a fixed-size window so the
-// collective has equal counts, then every rank scatters the windows back.
-struct NcclExchange final : g2::Exchange {
-    ncclComm_t comm = nullptr;
+// Sharded walk exchange: rank r owns accumulator slots
+// [lo_r*gs, hi_r*gs); each rank contributes a fixed-size window so the
+// gather has equal counts, then every rank scatters all windows back.  The
+// transport is one ncclAllGather (one process per GPU) or device copies
+// between Simulations of one process (LocalExchange).
+struct ShardExchange : g2::Exchange {
     int world = 1;
     g2::DBuf<float4> gathered;
+    static size_t window(const g2::Simulation& sim, int world) {
+        const size_t gs = sim.group_size(), ng_max = (sim.n() + gs - 1) / gs;
+        return ((ng_max + world - 1) / world) * gs;
+    }
+    void prepare(g2::Simulation& sim) {  // before the first step: the accumulator must not move later
+        sim.engine().reserve_accum(2 * sim.n() + 64 * sim.group_size());
+        gathered.reserve(window(sim, world) * world);
+    }
+    virtual void transport(g2::Simulation& sim, const float4* send, size_t per_rank) = 0;
+    void allgather_acc(g2::Simulation& sim) override {
+        auto& eng = sim.engine();
+        const size_t per_rank = window(sim, world);
+        transport(sim, eng.accum() + size_t(sim.shard_lo()) * sim.group_size(), per_rank);
+        G2_COUNT(1), unpack_kernel<<<256, 256, 0, eng.stream()>>>(gathered.p, eng.accum(), sim.n_active_dev(),
+                                                                 uint32_t(sim.group_size()), uint32_t(world),
+                                                                 uint32_t(per_rank));
+        G2_CUDA(cudaGetLastError());
+    }
+};
+
+struct NcclExchange final : ShardExchange {
+    ncclComm_t comm = nullptr;
     ~NcclExchange() override {
         if (comm) nccl().comm_destroy(comm);
     }
-    void allgather_acc(g2::Simulation& sim) override {
-        auto& eng = sim.engine();
-        cudaStream_t s = eng.stream();
-        const uint32_t gs = uint32_t(sim.group_size());
-        const size_t n = sim.n();
-        const size_t ng_max = (n + gs - 1) / gs;
-        const size_t per_rank = ((ng_max + world - 1) / world) * gs;  // slots per rank window
-        eng.reserve_accum(size_t(sim.shard_lo()) * gs + per_rank + n);
-        gathered.reserve(per_rank * world);
-        float4* send = eng.accum() + size_t(sim.shard_lo()) * gs;
-        G2_NCCL(nccl().all_gather(send, gathered.p, per_rank * 4, ncclFloat32, comm, s));
-        G2_COUNT(1), unpack_kernel<<<256, 256, 0, s>>>(gathered.p, eng.accum(), sim.n_active_dev(), gs, uint32_t(world),
-                                          uint32_t(per_rank));
+    void transport(g2::Simulation& sim, const float4* send, size_t per_rank) override {
+        G2_NCCL(nccl().all_gather(send, gathered.p, per_rank * 4, ncclFloat32, comm, sim.engine().stream()));
+    }
+};
+
+// In-process mesh: several Simulations (one host thread each, any devices)
+// exchange through device-to-device copies between two barriers.
+struct LocalMesh {
+    std::vector<g2::Simulation*> sims;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t phase = 0;
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const uint64_t ph = phase;
+        if (++arrived == int(sims.size())) {
+            arrived = 0;
+            ++phase;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return phase != ph; });
+        }
+    }
+};
+
+struct LocalExchange final : ShardExchange {
+    std::shared_ptr<LocalMesh> mesh;
+    void transport(g2::Simulation& sim, const float4*, size_t per_rank) override {
+        cudaStream_t s = sim.engine().stream();
+        G2_CUDA(cudaStreamSynchronize(s));  // own walk done
+        mesh->barrier();                    // every rank's walk done
+        for (int q = 0; q < world; ++q) {
+            g2::Simulation* o = mesh->sims[q];
+            G2_CUDA(cudaMemcpyAsync(gathered.p + size_t(q) * per_rank,
+                                    o->engine().accum() + size_t(o->shard_lo()) * o->group_size(),
+                                    per_rank * sizeof(float4), cudaMemcpyDefault, s));
+        }
+        G2_CUDA(cudaStreamSynchronize(s));
+        mesh->barrier();  // nobody reuses its accumulator before everyone copied
     }
 };
 
@@ -133,7 +186,7 @@ struct NcclExchange final : g2::Exchange {
 
 struct g2_sim {
     std::unique_ptr<g2::Simulation> s;
-    std::unique_ptr<NcclExchange> ex;
+    std::unique_ptr<ShardExchange> ex;
 };
 
 
@@ -336,8 +389,29 @@ int g2_sim_set_mesh(g2_sim* s, int rank, int world, const unsigned char id[128])
         std::memcpy(&u, id, 128);
         G2_NCCL(nccl().comm_init_rank(&ex->comm, world, u, rank));
         ex->world = world;
+        ex->prepare(*s->s);
         s->s->set_shard(rank, world, ex.get());
         s->ex = std::move(ex);
+    });
+}
+
+int g2_sim_set_mesh_local(g2_sim** sims, int world) {
+    return guarded([&] {
+        if (world < 1) throw g2::Error(G2_DATA_ERROR, "set_mesh_local: world must be >= 1");
+        auto mesh = std::make_shared<LocalMesh>();
+        for (int r = 0; r < world; ++r) mesh->sims.push_back(sims[r]->s.get());
+        for (int r = 0; r < world; ++r) {
+            if (world == 1) {
+                sims[r]->s->set_shard(0, 1, nullptr);
+                continue;
+            }
+            auto ex = std::make_unique<LocalExchange>();
+            ex->world = world;
+            ex->mesh = mesh;
+            ex->prepare(*sims[r]->s);
+            sims[r]->s->set_shard(r, world, ex.get());
+            sims[r]->ex = std::move(ex);
+        }
     });
 }
 

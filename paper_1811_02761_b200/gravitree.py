@@ -387,8 +387,16 @@ class Simulation:
         _chk(_lib.g2_sim_set_state(self._h, _ptr(p), _ptr(v)))
 
     def set_mesh(self, rank: int, world: int, unique_id: bytes):
+        """Join an NCCL mesh (one process per GPU): walk only this rank's shard of sink groups."""
         buf = (C.c_ubyte * 128).from_buffer_copy(unique_id)
         _chk(_lib.g2_sim_set_mesh(self._h, C.c_int(rank), C.c_int(world), buf))
+
+    @staticmethod
+    def set_mesh_local(sims):
+        """In-process mesh: sims[r] walks shard r and the accelerations are exchanged by
+        device copies; step the sims concurrently (one Python thread each)."""
+        arr = (C.c_void_p * len(sims))(*[s._h.value for s in sims])
+        _chk(_lib.g2_sim_set_mesh_local(arr, C.c_int(len(sims))))
 
 
 def nccl_unique_id() -> bytes:
