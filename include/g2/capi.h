@@ -108,6 +108,10 @@ int g2_engine_set_params(g2_engine* e, const g2_grav_params* p);
 /* ---- free functions -------------------------------------------------------- */
 /* direct_sum (gravity.cpp:18-43), on the device, FP64, bit-identical order */
 int g2_direct_sum(size_t n, const double* mass, const double* pos, double G, double eps, int device, double* acc_out);
+/* direct summation onto a subset of targets (accuracy oracle at large N, §8f):
+ * acc_out[3*n_targets] in target order; FP64, chunked over sources */
+int g2_direct_sum_targets(size_t n, const double* mass, const double* pos, double G, double eps, size_t n_targets,
+                          const uint32_t* targets, int device, double* acc_out);
 /* block_level (integrator.cpp:21-33) evaluated by the device kernel */
 int g2_block_level(size_t n, const double* acc_mag, const g2_step_scheme* s, double eps, int device, int* levels);
 /* predict (integrator.cpp:40-45) on the device; pos/vel updated in place */

@@ -278,6 +278,26 @@ int g2_direct_sum(size_t n, const double* mass, const double* pos, double G, dou
     });
 }
 
+int g2_direct_sum_targets(size_t n, const double* mass, const double* pos, double G, double eps, size_t n_targets,
+                          const uint32_t* targets, int device, double* acc_out) {
+    return guarded([&] {
+        G2_CUDA(cudaSetDevice(device));
+        for (size_t j = 0; j < n_targets; ++j)
+            if (targets[j] >= n) throw g2::Error(G2_DATA_ERROR, "direct_sum_targets: target out of range");
+        g2::DBuf<double> p3, m, out;
+        g2::DBuf<double4> xyzm;
+        g2::DBuf<uint32_t> tg;
+        p3.reserve(3 * n + 3), m.reserve(n + 1), xyzm.reserve(n + 1), tg.reserve(n_targets + 1);
+        out.reserve(3 * n_targets + 3);
+        G2_CUDA(cudaMemcpy(p3.p, pos, 3 * n * 8, cudaMemcpyHostToDevice));
+        G2_CUDA(cudaMemcpy(m.p, mass, n * 8, cudaMemcpyHostToDevice));
+        G2_CUDA(cudaMemcpy(tg.p, targets, n_targets * 4, cudaMemcpyHostToDevice));
+        g2::launch_pack_identity(p3.p, m.p, xyzm.p, n, nullptr);
+        g2::launch_direct_targets(xyzm.p, n, tg.p, n_targets, G, eps, out.p, nullptr);
+        G2_CUDA(cudaMemcpy(acc_out, out.p, 3 * n_targets * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
 int g2_block_level(size_t n, const double* acc_mag, const g2_step_scheme* s, double eps, int device, int* levels) {
     return guarded([&] {
         G2_CUDA(cudaSetDevice(device));

@@ -202,7 +202,53 @@ __global__ void __launch_bounds__(kBlock) predict_aos_kernel(double* pos, double
     }
 }
 
+// Direct summation onto a target subset (accuracy oracle for large N, SURVEY §8f
+// rank 2): FP64 pair terms, sources split into chunks across blocks and combined
+// with FP64 atomics (summation order differs from the reference's serial loop by
+// ~1e-16 relative, far below the tree errors it measures).
+constexpr int kDsTargets = 128, kDsChunk = 16384;
+__global__ void __launch_bounds__(kDsTargets) direct_targets_kernel(const double4* __restrict__ xyzm, uint32_t n,
+                                                                    const uint32_t* __restrict__ targets, uint32_t nt,
+                                                                    double G, double eps2, double* __restrict__ acc3) {
+    __shared__ double4 tile[kDsTargets];
+    const uint32_t t = blockIdx.x * kDsTargets + threadIdx.x;
+    const uint32_t me = t < nt ? targets[t] : 0xffffffffu;
+    const double4 ri = t < nt ? xyzm[me] : make_double4(0, 0, 0, 0);
+    const uint32_t j0 = blockIdx.y * kDsChunk, j1 = min(n, j0 + kDsChunk);
+    double sx = 0.0, sy = 0.0, sz = 0.0;
+    for (uint32_t base = j0; base < j1; base += kDsTargets) {
+        __syncthreads();
+        if (base + threadIdx.x < j1) tile[threadIdx.x] = xyzm[base + threadIdx.x];
+        __syncthreads();
+        const uint32_t m = min(uint32_t(kDsTargets), j1 - base);
+        for (uint32_t k = 0; k < m; ++k) {
+            if (base + k == me) continue;
+            const double4 q = tile[k];
+            const double dx = q.x - ri.x, dy = q.y - ri.y, dz = q.z - ri.z;
+            const double r2 = dx * dx + dy * dy + dz * dz + eps2;
+            if (r2 == 0.0) continue;
+            const double inv = rsqrt(r2);
+            const double f = G * q.w * inv * inv * inv;
+            sx += f * dx, sy += f * dy, sz += f * dz;
+        }
+    }
+    if (t < nt) {
+        atomicAdd(&acc3[3 * t], sx);
+        atomicAdd(&acc3[3 * t + 1], sy);
+        atomicAdd(&acc3[3 * t + 2], sz);
+    }
+}
+
 }  // namespace
+
+void launch_direct_targets(const double4* xyzm, size_t n, const uint32_t* targets, size_t nt, double G, double eps,
+                           double* acc3, cudaStream_t s) {
+    G2_CUDA(cudaMemsetAsync(acc3, 0, 3 * nt * sizeof(double), s));
+    const dim3 grid(ceil_div(nt, kDsTargets), ceil_div(n, kDsChunk));
+    G2_COUNT(1), direct_targets_kernel<<<grid, kDsTargets, 0, s>>>(xyzm, uint32_t(n), targets, uint32_t(nt), G,
+                                                                  eps * eps, acc3);
+    G2_CUDA(cudaGetLastError());
+}
 
 void launch_block_levels(const double* acc_mag, size_t n, SchemeDev sc, int* levels, cudaStream_t s) {
     if (n) G2_COUNT(1), block_levels_kernel<<<grid_for(n), kBlock, 0, s>>>(acc_mag, n, sc, levels);

@@ -107,6 +107,8 @@ void launch_walk_finalize(const WalkBuffers& b, uint32_t n_sinks_cap, double* ax
 // ---- integrate.cu -------------------------------------------------------------
 void launch_direct_sum(const double4* xyzm, size_t n, double G, double eps, double* ax, double* ay, double* az,
                        DevFlags* flags, cudaStream_t s);
+void launch_direct_targets(const double4* xyzm, size_t n, const uint32_t* targets, size_t nt, double G, double eps,
+                           double* acc3, cudaStream_t s);
 void launch_norm3(const double* ax, const double* ay, const double* az, double* out, size_t n, cudaStream_t s);
 struct StepState {
     double4* xyzm;

@@ -33,6 +33,7 @@ constexpr int kLcap = 384;                 // interaction-list entries per warp
 constexpr int kScap = 384;                 // shared stack entries per warp
 constexpr uint32_t kSpillWords = 16384;    // global stack entries per warp
 constexpr int kDonateEvery = 64;           // rounds between donations of a long-running task
+constexpr int kQueuedEnough = 4096;        // queued donated batches above which heavy tasks keep their work
 constexpr uint64_t kEmpty = ~0ull;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -448,8 +449,11 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
                 int k = 0;
                 uint32_t ds = 0;
                 if (lane == 0) {
-                    const bool heavy = iter - last_donation >= kDonateEvery;
-                    const bool dry = !heavy && ld_vol(q_init) >= ng && ld_vol(q_dhead) > ld_vol(q_dtail);
+                    // heavy: a long task donates every kDonateEvery rounds unless enough
+                    // donated work is already queued (keeps the slot budget for tight dacc)
+                    const uint32_t dh = ld_vol(q_dhead), dt = ld_vol(q_dtail);
+                    const bool heavy = iter - last_donation >= kDonateEvery && int(dt - dh) < kQueuedEnough;
+                    const bool dry = !heavy && ld_vol(q_init) >= ng && dh > dt;
                     if (heavy || dry) {
                         ds = atomicAdd(q_dtail, 1u);
                         if (ds < b.queue_cap) {

@@ -415,6 +415,16 @@ def direct_sum(system: ParticleSystem, params: GravParams = None, device: int = 
     return acc
 
 
+def direct_sum_targets(system: ParticleSystem, targets, params: GravParams = None, device: int = 0) -> np.ndarray:
+    """Direct summation onto `targets` only (FP64 on the device; accuracy oracle at large N)."""
+    p = params or GravParams()
+    tg = np.ascontiguousarray(targets, dtype=np.uint32)
+    acc = np.empty((len(tg), 3))
+    _chk(_lib.g2_direct_sum_targets(C.c_size_t(system.n()), _ptr(system.mass), _ptr(system.pos), C.c_double(p.G),
+                                    C.c_double(p.eps), C.c_size_t(len(tg)), _ptr(tg), C.c_int(device), _ptr(acc)))
+    return acc
+
+
 def block_level(acc_mag, scheme: StepScheme = None, eps: float = 0.0, device: int = 0):
     """block_level (integrator.cpp:21-33), vectorised over acc_mag, on the device."""
     a = np.atleast_1d(np.ascontiguousarray(acc_mag, dtype=np.float64))

@@ -256,3 +256,13 @@ def test_simulation_step_parity(g2, ref):
     assert g1.time == r1["time"]
     assert np.max(np.abs(g1.pos - r1["pos"])) < 1e-8
     assert np.max(np.abs(g1.vel - r1["vel"])) < 1e-6
+
+
+def test_direct_sum_targets(g2, oracle):
+    from paper_1811_02761_b200.gravitree import direct_sum_targets
+    mass, pos, _ = plummer(40000, seed=21)
+    tg = np.random.default_rng(1).choice(len(mass), 500, replace=False)
+    a = direct_sum_targets(g2.ParticleSystem(mass, pos), tg, g2.GravParams(1.0, 2.0 ** -5))
+    ref = oracle.direct_sum(mass, pos, eps=2.0 ** -5)[tg]
+    rel = np.linalg.norm(a - ref, axis=1) / np.linalg.norm(ref, axis=1)
+    assert rel.max() < 1e-12
