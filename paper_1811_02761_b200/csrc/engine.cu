@@ -104,7 +104,7 @@ Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), devic
     n_groups_.reserve(1);
     events_.reserve(3);
     qstate_.reserve(8);
-    queue_cap_ = 1u << 20;
+    queue_cap_ = 1u << 20;  // ring size of the walk's donated-task queue (walk.cu kRing)
     queue_.reserve(queue_cap_);
     batch_.reserve(size_t(queue_cap_) * 32);
     G2_CUDA(cudaMemsetAsync(queue_.p, 0xff, size_t(queue_cap_) * sizeof(uint64_t), s_));

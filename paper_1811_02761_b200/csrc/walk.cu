@@ -35,6 +35,9 @@ constexpr uint32_t kSpillWords = 16384;    // global stack entries per warp
 constexpr int kDonateEvery = 64;           // rounds between donations of a long-running task
 constexpr int kQueuedEnough = 4096;        // queued donated batches above which heavy tasks keep their work
 constexpr uint64_t kEmpty = ~0ull;
+constexpr int kRingBits = 20;              // donated-task ring: 2^20 slots, reused
+constexpr uint32_t kRing = 1u << kRingBits;
+constexpr uint64_t kGenMask = (1ull << 26) - 1;  // generation tag of a slot (ticket >> kRingBits)
 constexpr unsigned kFull = 0xffffffffu;
 
 // Interaction list in pair-interleaved layout so the flush runs on packed
@@ -218,16 +221,16 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
             unsigned backoff = 32;
             while (true) {
                 if (owed >= 0) {
-                    if (owed < (long long)b.queue_cap) {
-                        const uint64_t v = ld_acq64(&b.queue[owed]);
-                        if (v != kEmpty) {
-                            st_vol64(&b.queue[owed], kEmpty);  // self-cleaning for the next launch
-                            e = v;
-                            slot = uint32_t(owed);
+                    {  // ring slot of ticket `owed`; the generation tag tells a stale occupant apart
+                        const uint32_t sl = uint32_t(owed) & (kRing - 1);
+                        const uint64_t v = ld_acq64(&b.queue[sl]);
+                        if (v != kEmpty && ((v >> 6) & kGenMask) == ((uint64_t(owed) >> kRingBits) & kGenMask)) {
+                            e = v;  // the slot is released after the batch has been copied
+                            slot = sl;
                             owed = -1;
                             break;
                         }
-                        if ((long long)ld_vol(q_dtail) > owed) continue;  // reserved: its donor writes it now
+                        if (int(ld_vol(q_dtail) - uint32_t(owed)) > 0) continue;  // reserved: its donor writes it now
                     }
                 } else if (ld_vol(q_dhead) < ld_vol(q_dtail)) {
                     owed = atomicAdd(q_dhead, 1u);  // donated work first
@@ -278,6 +281,11 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
         } else {
             if (uint32_t(lane) < nbatch) sm.stack[lane] = b.batch[size_t(slot) * 32 + lane];
             ssize = int(nbatch);
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence();
+                st_vol64(&b.queue[slot], kEmpty);  // release the ring slot for reuse
+            }
         }
         __syncwarp();
 
@@ -455,12 +463,12 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
                     const bool heavy = iter - last_donation >= kDonateEvery && int(dt - dh) < kQueuedEnough;
                     const bool dry = !heavy && ld_vol(q_init) >= ng && dh > dt;
                     if (heavy || dry) {
-                        ds = atomicAdd(q_dtail, 1u);
-                        if (ds < b.queue_cap) {
-                            k = min(live / 2, 32);
-                            k = gtop == gbase ? min(k, ssize) : min(k, gtop - gbase);
-                            atomicAdd(q_pending, 1u);
-                        }
+                        ds = atomicAdd(q_dtail, 1u);  // ticket; slot = ticket mod ring size
+                        k = min(live / 2, 32);
+                        k = gtop == gbase ? min(k, ssize) : min(k, gtop - gbase);
+                        atomicAdd(q_pending, 1u);
+                        // wait for the slot's previous occupant to be consumed (ring of 2^20)
+                        while (ld_vol64(&b.queue[ds & (kRing - 1)]) != kEmpty) __nanosleep(64);
                     }
                 }
                 k = __shfl_sync(kFull, k, 0);
@@ -468,10 +476,13 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
                 if (k) {
                     last_donation = iter;
                     const bool from_spill = gtop > gbase;
-                    if (lane < k) b.batch[size_t(ds) * 32 + lane] = from_spill ? spill[gbase + lane] : sm.stack[lane];
+                    const uint32_t sl = ds & (kRing - 1);
+                    if (lane < k) b.batch[size_t(sl) * 32 + lane] = from_spill ? spill[gbase + lane] : sm.stack[lane];
                     __threadfence();
                     __syncwarp();
-                    if (lane == 0) st_rel64(&b.queue[ds], (uint64_t(grp) << 32) | uint32_t(k));
+                    if (lane == 0)
+                        st_rel64(&b.queue[sl], (uint64_t(grp) << 32) | ((uint64_t(ds >> kRingBits) & kGenMask) << 6) |
+                                                   uint32_t(k));
                     if (from_spill) {
                         gbase += k;
                         if (gbase == gtop) gbase = gtop = 0;
