@@ -6,9 +6,9 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;                      // keys per thread
-constexpr int kTile = kThreads * kItems;        // 4096 keys per tile
-constexpr int kWarpItems = 32 * kItems;         // 512 consecutive keys per warp
+constexpr int kItems = 8;                       // keys per thread
+constexpr int kTile = kThreads * kItems;        // 2048 keys per tile
+constexpr int kWarpItems = 32 * kItems;         // 256 consecutive keys per warp
 
 
 // exclusive scan of one value per thread across the 256-thread block
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(uint32_t* __restrict__ c
 }
 
 template <typename K, bool kIdentity>
-__global__ void __launch_bounds__(kThreads) scatter_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(kThreads, 4) scatter_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                            K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                            size_t n, int shift, const uint32_t* __restrict__ offsets,
                                                            uint32_t tiles) {

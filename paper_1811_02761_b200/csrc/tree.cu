@@ -121,25 +121,25 @@ __device__ __forceinline__ unsigned digit_at(uint64_t key, int depth) {
     return unsigned(key >> (3 * (kMortonBits - 1 - depth))) & 7u;
 }
 
+// Warp-granular tiles (32 cells, no block barriers): each warp pulls tiles and
+// chains its child offsets through the warp-parallel look-back.
 __global__ void __launch_bounds__(kBlock) split_level_kernel(SplitArgs a, int d) {
-    __shared__ uint32_t s_tile, s_excl, s_wsum[kBlock / 32];
     const uint32_t lvl_begin = a.level_start[d], lvl_end = a.level_start[d + 1];
     const uint32_t ncell = lvl_end - lvl_begin;
-    const uint32_t ntiles = (ncell + kBlock - 1) / kBlock;
+    const uint32_t ntiles = (ncell + 31) / 32;
     if (lvl_end > a.cell_cap || ncell == 0) {  // overflow (host grows and rebuilds) or empty level
         if (blockIdx.x == 0 && threadIdx.x == 0) a.level_start[d + 2] = lvl_end;
         return;
     }
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int lane = threadIdx.x & 31;
     const int shift = 3 * (kMortonBits - 1 - d);
-    uint64_t* status = a.status + (lvl_begin / kBlock + d);  // disjoint slice per level
+    uint64_t* status = a.status + (lvl_begin / 32 + d);  // disjoint slice per level
     while (true) {
-        if (tid == 0) s_tile = atomicAdd(&a.tile_counters[d], 1u);
-        __syncthreads();
-        const uint32_t tile = s_tile;
-        __syncthreads();
+        uint32_t tile = 0;
+        if (lane == 0) tile = atomicAdd(&a.tile_counters[d], 1u);
+        tile = __shfl_sync(0xffffffffu, tile, 0);
         if (tile >= ntiles) break;
-        const uint32_t cell = lvl_begin + tile * kBlock + tid;
+        const uint32_t cell = lvl_begin + tile * 32 + lane;
         const bool in_range = cell < lvl_end;
         uint32_t first = 0, cnt = 0;
         if (in_range) first = a.first[cell], cnt = a.count[cell];
@@ -192,28 +192,16 @@ __global__ void __launch_bounds__(kBlock) split_level_kernel(SplitArgs a, int d)
         uint32_t nc = 0;
 #pragma unroll
         for (int v = 0; v < 8; ++v) nc += ub[v] > (v ? ub[v - 1] : first) ? 1u : 0u;
-        // exclusive scan of child counts over the tile
+        // exclusive scan of child counts over the warp's tile, then the look-back
         uint32_t inc = nc;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        if (lane == 31) s_wsum[w] = inc;
-        __syncthreads();
-        uint32_t wpre = 0, tot = 0;
-#pragma unroll
-        for (int k = 0; k < kBlock / 32; ++k) {
-            const uint32_t t = s_wsum[k];
-            if (k < w) wpre += t;
-            tot += t;
-        }
-        if (w == 0) {
-            const uint64_t e = lookback_warp(status, tile, tot);
-            if (lane == 0) s_excl = uint32_t(e);
-        }
-        __syncthreads();
-        const uint32_t base = lvl_end + s_excl + wpre + inc - nc;  // first child index
+        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+        const uint32_t excl = uint32_t(lookback_warp(status, tile, tot));
+        const uint32_t base = lvl_end + excl + inc - nc;  // first child index
         if (split) {
             uint32_t j = 0, lo = first;
 #pragma unroll
@@ -237,7 +225,7 @@ __global__ void __launch_bounds__(kBlock) split_level_kernel(SplitArgs a, int d)
             a.first_child[cell] = split ? base : 0u;
             a.child_count[cell] = split ? nc : 0u;
         }
-        if (tile == ntiles - 1 && tid == 0) a.level_start[d + 2] = lvl_end + s_excl + tot;
+        if (tile == ntiles - 1 && lane == 0) a.level_start[d + 2] = lvl_end + excl + tot;
     }
 }
 

@@ -266,3 +266,36 @@ def test_direct_sum_targets(g2, oracle):
     ref = oracle.direct_sum(mass, pos, eps=2.0 ** -5)[tg]
     rel = np.linalg.norm(a - ref, axis=1) / np.linalg.norm(ref, axis=1)
     assert rel.max() < 1e-12
+
+
+def test_config1_plummer_2e16_full_step(g2, ref):
+    """BASELINE config 1: Plummer 2^16, one full step (build_structure + refresh + evaluate(all))
+    on the bootstrapped state, against the reference library on the same input."""
+    m, p, _ = ref.sample_model("plummer", 1 << 16, 1)
+    e = ref.engine(eps=2.0 ** -5, dacc=2.0 ** -9, threads=0)
+    _, amag, _ = e.bootstrap(m, p)  # direct summation (n <= 65536), FP64
+    e.build(m, p)
+    acc_r, _, ev_r = e.evaluate(m, p, amag)
+    s = g2.ParticleSystem(m, p)
+    eng = g2.GravityEngine(g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9))
+    eng.bootstrap(s)
+    assert np.array_equal(s.acc_old_mag, amag)  # bit-exact bootstrap
+    eng.build_structure(s)
+    eng.refresh(s)
+    ev = eng.evaluate(s)
+    assert (ev.interactions, ev.mac_evals, ev.list_pushes) == (ev_r["interactions"], ev_r["mac_evals"],
+                                                               ev_r["list_pushes"])
+    err = g2.force_error(s.acc, acc_r)
+    assert err["median"] <= MED_TOL and err["p99"] <= P99_TOL, err
+
+
+@pytest.mark.slow
+def test_full_size_tree_bitexact_m31_2e23(g2, ref):
+    """BASELINE config 3 input at full size: the bench's M31 N=2^23 tree (keys, perm, cells,
+    nodes) equals the reference build_tree bit for bit."""
+    from paper_1811_02761_b200.gravitree import sample_model
+    m, p, _ = sample_model("m31", 1 << 23, 1)
+    t = gpu_tree(g2, m, p)
+    rt = ref.build_tree(m, p)
+    for k in ("bbox", "keys", "perm", "rank", "cells", "depth", "nodes"):
+        assert np.array_equal(getattr(t, k), getattr(rt, k)), k
