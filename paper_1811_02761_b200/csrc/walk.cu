@@ -27,6 +27,9 @@
 namespace g2 {
 namespace {
 
+#ifndef G2_WALK_MINB
+#define G2_WALK_MINB 7  // resident CTAs per SM the register budget is tuned for
+#endif
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kLcap = 384;                 // interaction-list entries per warp
@@ -47,13 +50,23 @@ struct WarpSmem {
     float4 la[kLcap / 2];
     float4 lb[kLcap / 2];
     uint32_t stack[kScap];
-    uint32_t link[32], cpre[32], lpre[32];  // per-round scratch for the cooperative writers
 };
 
+__device__ __forceinline__ float* entry_ptr(WarpSmem& sm, int pos) {
+    return reinterpret_cast<float*>(sm.la) + 2 * (pos & ~1) + (pos & 1);
+}
+// entry pos: x, y at la[pos/2] lanes (pos&1) and 2 + (pos&1); z, m likewise in lb
 __device__ __forceinline__ void put_entry(WarpSmem& sm, int pos, float x, float y, float z, float m) {
-    float* a = reinterpret_cast<float*>(&sm.la[pos >> 1]) + (pos & 1);
-    float* b = reinterpret_cast<float*>(&sm.lb[pos >> 1]) + (pos & 1);
-    a[0] = x, a[2] = y, b[0] = z, b[2] = m;
+    float* a = entry_ptr(sm, pos);
+    a[0] = x, a[2] = y, a[2 * kLcap] = z, a[2 * kLcap + 2] = m;
+}
+// Opened-leaf particles are staged as particle indices in the m slot of their
+// own list entry, then each lane replaces the slot(s) it owns by the entry.
+__device__ __forceinline__ void put_index(WarpSmem& sm, int pos, uint32_t k) {
+    reinterpret_cast<uint32_t*>(entry_ptr(sm, pos))[2 * kLcap + 2] = k;
+}
+__device__ __forceinline__ uint32_t get_index(WarpSmem& sm, int pos) {
+    return reinterpret_cast<const uint32_t*>(entry_ptr(sm, pos))[2 * kLcap + 2];
 }
 
 // ---- packed f32x2 helpers (sm_100a PTX) --------------------------------------
@@ -138,7 +151,7 @@ struct Acc2 {
 template <bool kPot, bool kEps0>
 __device__ __forceinline__ void flush_list(const WarpSmem& sm, int cnt, f2 sx, f2 sy, f2 sz, f2 eps2, Acc2& a) {
     const int np = (cnt + 1) >> 1;
-#pragma unroll 2
+#pragma unroll 4
     for (int p = 0; p < np; ++p) {
         const ulonglong2 A = *reinterpret_cast<const ulonglong2*>(&sm.la[p]);
         const ulonglong2 B = *reinterpret_cast<const ulonglong2*>(&sm.lb[p]);
@@ -168,15 +181,6 @@ __device__ __forceinline__ void flush_list(const WarpSmem& sm, int cnt, f2 sx, f
     }
 }
 
-// upper-bound search over a warp's 32 exclusive prefixes: the lane owning item o
-__device__ __forceinline__ int owner_lane(const uint32_t* pre, uint32_t o) {
-    int s = 0;
-#pragma unroll
-    for (int step = 16; step > 0; step >>= 1)
-        if (pre[s + step] <= o) s += step;
-    return s;
-}
-
 // Exact FP64 MAC in the reference's operation order (traversal.cpp:40-56).
 __device__ __forceinline__ bool mac_exact(const WNode& nd, const GroupRec& g, const WalkParams& p, double rhs,
                                           bool geom) {
@@ -190,11 +194,11 @@ __device__ __forceinline__ bool mac_exact(const WNode& nd, const GroupRec& g, co
 }
 
 template <bool kPot, bool kEps0, bool kCheck>
-__global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParams p, WalkBuffers b, DevFlags* flags) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[w];
-    uint32_t* spill = b.spill + (size_t(blockIdx.x) * kWarps + w) * kSpillWords;
+__global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t, WalkParams p, WalkBuffers b, DevFlags* flags) {
+    __shared__ WarpSmem smem[kWarps];
+    const int lane = threadIdx.x & 31;
+    WarpSmem& sm = smem[threadIdx.x >> 5];
+    uint32_t* spill = b.spill + (size_t(blockIdx.x) * kWarps + (threadIdx.x >> 5)) * kSpillWords;
     // Task sources: the initial tasks (one per group, claimed by counter, in
     // b.order when given: heaviest first) and the FIFO of donated batches of
     // (group, up to 32 cells), which has priority so heavy groups are split
@@ -275,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
         uint32_t macs = 0, pushes = 0;
         // logical LIFO = spill[gbase, gtop) (bottom, global) ++ sm.stack[0, ssize) (top, shared)
         int ssize, gbase = 0, gtop = 0, lsize = 0, iter = 0, last_donation = 0;
+        uint32_t pv_dh = 0, pv_dt = 0, pv_init = 0;  // lane 0: queue counters read at the previous check
         if (nbatch == 0) {
             if (lane == 0) sm.stack[0] = 0;  // root
             ssize = 1;
@@ -310,13 +315,13 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
             // ---- MAC: FP32 screen with error bounds, exact FP64 only when undecided
             bool accept = false, leaf = false;
             uint32_t link = 0, info = 0;
-            double ncx = 0, ncy = 0, ncz = 0, nm = 0;
+            float fx = 0.f, fy = 0.f, fz = 0.f, fm = 0.f;  // group centre - com (FP64 difference rounded), mass
             if (valid) {
                 const WNode nd = t.nodes[c];
                 link = nd.link, info = nd.info;
                 leaf = (info & kLeafBit) != 0;
-                ncx = nd.cx, ncy = nd.cy, ncz = nd.cz, nm = nd.mass;
-                const float fx = float(dsub(g.cx, nd.cx)), fy = float(dsub(g.cy, nd.cy)), fz = float(dsub(g.cz, nd.cz));
+                fx = float(dsub(g.cx, nd.cx)), fy = float(dsub(g.cy, nd.cy)), fz = float(dsub(g.cz, nd.cz));
+                fm = float(nd.mass);
                 const float S = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
                 const float D = S > 0.f ? S * rsqrt_ftz(S) : 0.f;
                 const float d32 = D - radf;
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
                     } else {
                         // G m b^2 / d^4 <= rhs  <=>  G m b^2 <= rhs d^4  (no division)
                         const float ext = float(nd.extent), d2 = d32 * d32;
-                        const float num = G * float(nd.mass) * ext * ext, den = rhsf * (d2 * d2);
+                        const float num = G * fm * ext * ext, den = rhsf * (d2 * d2);
                         const float tol = 4.f * rel + 1e-5f;
                         if (tol < 0.25f && den > 1e-30f)
                             verdict = num <= den * (1.f - tol) ? 1 : (num > den * (1.f + tol) ? 0 : 2);
@@ -356,9 +361,6 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
             }
             const uint32_t tot = __shfl_sync(kFull, inc, 31), exc = inc - v;
             const uint32_t ctot = tot & 1023u, ntot = (tot >> 10) & 1023u, ltot = tot >> 20;
-            sm.link[lane] = link;
-            sm.lpre[lane] = exc >> 20;
-            __syncwarp();
 
             // ---- rejected internal cells: children onto the stack (cooperative)
             if (ctot) {
@@ -406,14 +408,23 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
                     __syncwarp();
                     lsize = 0;
                 }
-                if (nnode)
-                    put_entry(sm, lsize + int((exc >> 10) & 1023u), float(dsub(ncx, g.cx)), float(dsub(ncy, g.cy)),
-                              float(dsub(ncz, g.cz)), float(nm));
-                for (uint32_t o = lane; o < ltot; o += 32) {
-                    const int s = owner_lane(sm.lpre, o);
-                    const double4 q = t.xyzm[sm.link[s] + (o - sm.lpre[s])];
-                    put_entry(sm, lsize + int(ntot + o), float(dsub(q.x, g.cx)), float(dsub(q.y, g.cy)),
-                              float(dsub(q.z, g.cz)), float(q.w));
+                // entry = com - group centre = -(group centre - com): the same rounded FP64 difference
+                if (nnode) put_entry(sm, lsize + int((exc >> 10) & 1023u), -fx, -fy, -fz, fm);
+                if (ltot) {
+                    const int lbase = lsize + int(ntot);
+                    if (nfast) {
+                        const int pos = lbase + int(exc >> 20);
+#pragma unroll
+                        for (uint32_t j = 0; j < 8; ++j)
+                            if (j < nfast) put_index(sm, pos + int(j), link + j);
+                    }
+                    __syncwarp();
+                    for (uint32_t o = lane; o < ltot; o += 32) {
+                        const int pos = lbase + int(o);
+                        const double4 q = t.xyzm[get_index(sm, pos)];
+                        put_entry(sm, pos, float(dsub(q.x, g.cx)), float(dsub(q.y, g.cy)), float(dsub(q.z, g.cz)),
+                                  float(q.w));
+                    }
                 }
                 lsize += int(P);
                 pushes += P;
@@ -458,10 +469,13 @@ __global__ void __launch_bounds__(kThreads, 7) walk_kernel(TreeView t, WalkParam
                 uint32_t ds = 0;
                 if (lane == 0) {
                     // heavy: a long task donates every kDonateEvery rounds unless enough
-                    // donated work is already queued (keeps the slot budget for tight dacc)
-                    const uint32_t dh = ld_vol(q_dhead), dt = ld_vol(q_dtail);
+                    // donated work is already queued (keeps the slot budget for tight dacc).
+                    // The queue counters are read one check ahead (the loads overlap four
+                    // rounds of work instead of stalling this one); they only steer the heuristic.
+                    const uint32_t dh = pv_dh, dt = pv_dt;
                     const bool heavy = iter - last_donation >= kDonateEvery && int(dt - dh) < kQueuedEnough;
-                    const bool dry = !heavy && ld_vol(q_init) >= ng && dh > dt;
+                    const bool dry = !heavy && pv_init >= ng && dh > dt;
+                    pv_dh = ld_vol(q_dhead), pv_dt = ld_vol(q_dtail), pv_init = ld_vol(q_init);
                     if (heavy || dry) {
                         ds = atomicAdd(q_dtail, 1u);  // ticket; slot = ticket mod ring size
                         k = min(live / 2, 32);
@@ -617,10 +631,7 @@ template <bool kPot, bool kEps0, bool kCheck>
 int walk_blocks_per_sm() {
     static int v = 0;
     if (!v) {
-        const int smem = kWarps * int(sizeof(WarpSmem));
-        G2_CUDA(cudaFuncSetAttribute(walk_kernel<kPot, kEps0, kCheck>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     smem));
-        G2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, walk_kernel<kPot, kEps0, kCheck>, kThreads, smem));
+        G2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, walk_kernel<kPot, kEps0, kCheck>, kThreads, 0));
         if (v < 1) v = 1;
     }
     return v;
@@ -630,7 +641,7 @@ template <bool kPot, bool kEps0, bool kCheck>
 void walk_launch_t(const TreeView& t, const WalkParams& p, const WalkBuffers& b, DevFlags* flags, cudaStream_t s) {
     const int per_sm = walk_blocks_per_sm<kPot, kEps0, kCheck>();
     const unsigned grid = unsigned(per_sm * kNumSMs);
-    G2_COUNT(1), walk_kernel<kPot, kEps0, kCheck><<<grid, kThreads, kWarps * sizeof(WarpSmem), s>>>(t, p, b, flags);
+    G2_COUNT(1), walk_kernel<kPot, kEps0, kCheck><<<grid, kThreads, 0, s>>>(t, p, b, flags);
 }
 
 }  // namespace

@@ -19,7 +19,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_build", "libg2.so")
+# G2_LIB_PATH: development override (A/B experiments with alternative builds)
+LIB_PATH = os.environ.get("G2_LIB_PATH") or os.path.join(_HERE, "_build", "libg2.so")
 
 
 # ---- errors (errors.hpp:8-23) ---------------------------------------------------
