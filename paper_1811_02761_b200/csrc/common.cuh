@@ -53,6 +53,19 @@ struct alignas(16) WNode {
 };
 constexpr uint32_t kLeafBit = 0x80000000u;
 
+// Compact walk record (32 B, one 256-bit load): the FP32-rounded centre of mass,
+// mass, extent and q = m b^2 for the FP32 MAC screen, and the same link/info as
+// WNode.  The exact FP64 WNode is read only for undecided MAC evaluations.
+struct alignas(32) WNode32 {
+    float cx, cy, cz, m;
+    float b, q;
+    uint32_t link, info;
+};
+// Leaf particles are read by the walk as float4 rel[k] = (x_k - c, m_k): the
+// position relative to the leaf's FP32-rounded centre of mass c (one FP64
+// difference, rounded).  An opened leaf then yields list entries
+// (c - group centre) + rel in FP32 with no FP64 work per particle.
+
 // ---- exact FP64 helpers: explicit _rn intrinsics are never contracted into FMA,
 // so device results match the reference's x86-64 SSE2 arithmetic bit for bit.
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }

@@ -127,7 +127,7 @@ void Engine::reserve(size_t n) {
         tgt_rank_.reserve(n);
     amag_s_.reserve(n), ax_s_.reserve(n), ay_s_.reserve(n), az_s_.reserve(n), pot_s_.reserve(n), out_.reserve(3 * n);
     sinks_.reserve(n), sinks_alt_.reserve(n);
-    groups_.reserve(n), accum_.reserve(n), group_inter_.reserve(n);
+    groups_.reserve(n), accum_.reserve(n), group_inter_.reserve(n), rel_.reserve(n), leaf_of_.reserve(n);
     ensure_cells(std::max<size_t>(n + 64, 1024));
     cap_ = n;
 }
@@ -135,7 +135,7 @@ void Engine::reserve(size_t n) {
 void Engine::ensure_cells(size_t cap) {
     if (cap <= cell_cap_) return;
     first_child_.reserve(cap), child_count_.reserve(cap), first_.reserve(cap), count_.reserve(cap);
-    depth_.reserve(cap), nodes_.reserve(cap);
+    depth_.reserve(cap), nodes_.reserve(cap), nodes32_.reserve(cap);
     split_status_.reserve(cap / 32 + 64);
     cell_cap_ = cap;
 }
@@ -252,7 +252,7 @@ void Engine::split_and_nodes(bool with_nodes) {
 
 void Engine::calc_nodes() {
     launch_calc_node(xyzm_s_.p, first_child_.p, child_count_.p, first_.p, count_.p, depth_.p, level_start_.p,
-                     nodes_.p, s_);
+                     nodes_.p, nodes32_.p, rel_.p, leaf_of_.p, s_);
 }
 
 void Engine::refresh(size_t n, const double* mass, const double* pos) {
@@ -288,7 +288,7 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     const uint32_t ng_cap = (n_sinks_cap + gs - 1) / gs;
     const size_t cap = c_.frontier_cap ? c_.frontier_cap : 8 * n_;
     const bool check = cap < max_level_width_;
-    TreeView tv{xyzm_s_.p, nodes_.p, uint32_t(n_)};
+    TreeView tv{xyzm_s_.p, nodes_.p, uint32_t(n_), nodes32_.p, rel_.p, leaf_of_.p};
     WalkBuffers b{};
     b.sinks = sinks;
     b.n_sinks = n_sinks_dev;
@@ -353,6 +353,8 @@ EventsH Engine::evaluate(size_t n, const double* mass, const double* pos, const 
             if (targets[j] >= n) throw Error(kDataError, "GravityEngine::evaluate: target index out of range");
     upload_orig(n, mass, pos);
     launch_pack_sorted(pos3_.p, mass_.p, perm_.p, xyzm_s_.p, n, s_);
+    // leaf particles at the positions given here, node attributes of the last build/refresh
+    launch_leaf_rel(xyzm_s_.p, child_count_.p, first_.p, count_.p, nodes32_.p, uint32_t(ncells_), rel_.p, s_);
     G2_CUDA(cudaMemcpyAsync(amag_o_.p, acc_old_mag, n * sizeof(double), cudaMemcpyHostToDevice, s_));
     launch_gather_f64(amag_o_.p, perm_.p, amag_s_.p, n, s_);
     const uint32_t* out_idx;

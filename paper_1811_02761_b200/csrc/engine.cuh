@@ -107,6 +107,9 @@ private:
     DBuf<uint32_t> first_child_, child_count_, first_, count_;
     DBuf<uint8_t> depth_;
     DBuf<WNode> nodes_;
+    DBuf<WNode32> nodes32_;
+    DBuf<float4> rel_;
+    DBuf<uint32_t> leaf_of_;
     DBuf<uint32_t> level_start_, tile_counters_;
     DBuf<uint64_t> split_status_;
     DBuf<double> bbox_part_;

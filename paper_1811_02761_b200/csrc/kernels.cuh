@@ -23,6 +23,9 @@ struct TreeView {
     const double4* xyzm;   // [n] sorted
     const WNode* nodes;    // [ncells]
     uint32_t n;
+    const WNode32* nodes32;  // [ncells] compact walk records
+    const float4* rel;       // [n] leaf-relative positions + mass (sorted order)
+    const uint32_t* leaf_of; // [n] leaf cell of each particle
 };
 
 // ---- tree.cu -----------------------------------------------------------------
@@ -49,9 +52,14 @@ struct SplitArgs {
 void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s);
 
 // calc_node over all levels, deepest first (octree.cpp:145-162)
+// also writes the compact walk records and the leaf-relative particle offsets
 void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const uint32_t* child_count,
                       const uint32_t* first, const uint32_t* count, const uint8_t* depth, const uint32_t* level_start,
-                      WNode* nodes, cudaStream_t s);
+                      WNode* nodes, WNode32* nodes32, float4* rel, uint32_t* leaf_of, cudaStream_t s);
+// leaf-relative offsets of the CURRENT positions against the existing nodes (GravityEngine::evaluate
+// walks fresh positions with the node attributes of the last build/refresh, engine.cpp:31-81)
+void launch_leaf_rel(const double4* xyzm, const uint32_t* child_count, const uint32_t* first, const uint32_t* count,
+                     const WNode32* nodes32, uint32_t ncells, float4* rel, cudaStream_t s);
 
 // out[k] = in[src[k]] gathers
 void launch_gather_d4(const double4* in, const uint32_t* src, double4* out, size_t n, cudaStream_t s);

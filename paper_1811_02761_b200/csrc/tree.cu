@@ -245,7 +245,8 @@ __global__ void split_init_kernel(SplitArgs a, uint32_t n) {
 __global__ void __launch_bounds__(kBlock) calc_node_level_kernel(
     const double4* __restrict__ xyzm, const uint32_t* __restrict__ first_child,
     const uint32_t* __restrict__ child_count, const uint32_t* __restrict__ first, const uint32_t* __restrict__ count,
-    const uint8_t* __restrict__ depth, const uint32_t* __restrict__ level_start, WNode* __restrict__ nodes, int d) {
+    const uint8_t* __restrict__ depth, const uint32_t* __restrict__ level_start, WNode* __restrict__ nodes,
+    WNode32* __restrict__ nodes32, float4* __restrict__ rel, uint32_t* __restrict__ leaf_of, int d) {
     const uint32_t b = level_start[d], e = level_start[d + 1];
     for (uint32_t c = b + blockIdx.x * kBlock + threadIdx.x; c < e; c += gridDim.x * kBlock) {
         const uint32_t cc = child_count[c];
@@ -262,10 +263,13 @@ __global__ void __launch_bounds__(kBlock) calc_node_level_kernel(
             }
             const double inv = ddiv(1.0, m);
             nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+            const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
             double e2 = 0.0;
             for (uint32_t k = f; k < k1; ++k) {
                 const double4 p = xyzm[k];
                 e2 = smax(e2, norm2(dsub(p.x, nd.cx), dsub(p.y, nd.cy), dsub(p.z, nd.cz)));
+                rel[k] = make_float4(float(dsub(p.x, c32x)), float(dsub(p.y, c32y)), float(dsub(p.z, c32z)), float(p.w));
+                leaf_of[k] = c;
             }
             nd.extent = dsqrt(e2);
             nd.link = f;
@@ -292,6 +296,26 @@ __global__ void __launch_bounds__(kBlock) calc_node_level_kernel(
         }
         nd.mass = m;
         nodes[c] = nd;
+        const float fm = float(m), fb = float(nd.extent);
+        nodes32[c] = WNode32{float(nd.cx), float(nd.cy), float(nd.cz), fm, fb, fm * fb * fb, nd.link, nd.info};
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) leaf_rel_kernel(const double4* __restrict__ xyzm,
+                                                          const uint32_t* __restrict__ child_count,
+                                                          const uint32_t* __restrict__ first,
+                                                          const uint32_t* __restrict__ count,
+                                                          const WNode32* __restrict__ nodes32, uint32_t ncells,
+                                                          float4* __restrict__ rel) {
+    for (uint32_t c = blockIdx.x * kBlock + threadIdx.x; c < ncells; c += gridDim.x * kBlock) {
+        if (child_count[c]) continue;
+        const WNode32 nd = nodes32[c];
+        const double cx = nd.cx, cy = nd.cy, cz = nd.cz;
+        const uint32_t f = first[c], k1 = f + count[c];
+        for (uint32_t k = f; k < k1; ++k) {
+            const double4 p = xyzm[k];
+            rel[k] = make_float4(float(dsub(p.x, cx)), float(dsub(p.y, cy)), float(dsub(p.z, cz)), float(p.w));
+        }
     }
 }
 
@@ -367,10 +391,16 @@ void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
 
 void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const uint32_t* child_count,
                       const uint32_t* first, const uint32_t* count, const uint8_t* depth, const uint32_t* level_start,
-                      WNode* nodes, cudaStream_t s) {
+                      WNode* nodes, WNode32* nodes32, float4* rel, uint32_t* leaf_of, cudaStream_t s) {
     for (int d = kMaxDepth; d >= 0; --d)
         G2_COUNT(1), calc_node_level_kernel<<<kNumSMs * 8, kBlock, 0, s>>>(xyzm, first_child, child_count, first, count, depth,
-                                                              level_start, nodes, d);
+                                                              level_start, nodes, nodes32, rel, leaf_of, d);
+    G2_CUDA(cudaGetLastError());
+}
+
+void launch_leaf_rel(const double4* xyzm, const uint32_t* child_count, const uint32_t* first, const uint32_t* count,
+                     const WNode32* nodes32, uint32_t ncells, float4* rel, cudaStream_t s) {
+    G2_COUNT(1), leaf_rel_kernel<<<grid_for(ncells), kBlock, 0, s>>>(xyzm, child_count, first, count, nodes32, ncells, rel);
     G2_CUDA(cudaGetLastError());
 }
 

@@ -33,7 +33,7 @@ namespace {
 constexpr int kWarps = 4;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kLcap = 384;                 // interaction-list entries per warp
-constexpr int kScap = 384;                 // shared stack entries per warp
+constexpr int kScap = 256;                 // shared stack entries per warp
 constexpr uint32_t kSpillWords = 16384;    // global stack entries per warp
 constexpr int kDonateEvery = 64;           // rounds between donations of a long-running task
 constexpr int kQueuedEnough = 4096;        // queued donated batches above which heavy tasks keep their work
@@ -50,6 +50,7 @@ struct WarpSmem {
     float4 la[kLcap / 2];
     float4 lb[kLcap / 2];
     uint32_t stack[kScap];
+    float4 leaf[32];  // per lane: (leaf com - group centre, first particle) of the leaf it opened this round
 };
 
 __device__ __forceinline__ float* entry_ptr(WarpSmem& sm, int pos) {
@@ -60,8 +61,8 @@ __device__ __forceinline__ void put_entry(WarpSmem& sm, int pos, float x, float 
     float* a = entry_ptr(sm, pos);
     a[0] = x, a[2] = y, a[2 * kLcap] = z, a[2 * kLcap + 2] = m;
 }
-// Opened-leaf particles are staged as particle indices in the m slot of their
-// own list entry, then each lane replaces the slot(s) it owns by the entry.
+// Opened-leaf particles are staged as (owner lane | j << 5) in the m slot of
+// their own list entry, then each lane replaces the slot(s) it owns by the entry.
 __device__ __forceinline__ void put_index(WarpSmem& sm, int pos, uint32_t k) {
     reinterpret_cast<uint32_t*>(entry_ptr(sm, pos))[2 * kLcap + 2] = k;
 }
@@ -104,6 +105,17 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {  // one MUFU.RSQ, no denor
     asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+
+// one 256-bit load per node record, one 128-bit load per leaf particle (read-only path)
+__device__ __forceinline__ WNode32 ld_node32(const WNode32* p) {
+    uint32_t w[8];
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+        : "l"(p));
+    return WNode32{__uint_as_float(w[0]), __uint_as_float(w[1]), __uint_as_float(w[2]), __uint_as_float(w[3]),
+                   __uint_as_float(w[4]), __uint_as_float(w[5]), w[6], w[7]};
+}
+__device__ __forceinline__ float4 ld_rel(const float4* p) { return __ldg(p); }
 
 __device__ __forceinline__ uint32_t ld_vol(const uint32_t* p) {
     uint32_t v;
@@ -268,11 +280,25 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         const bool geom = p.force_geometric || g.a_min <= 0.0;  // engine.cpp:66
         const double rhs = dmul(p.dacc, g.a_min);
         const float rhsf = float(rhs), radf = float(g.radius);
+        // group centre as an unevaluated FP32 sum hi + lo: (hi - c) + lo is the FP32 difference to a
+        // node's FP32 centre c with error <= 2^-24 (|c| + 2|d|) per axis (no FP64 in the screen)
+        const float gxh = float(g.cx), gyh = float(g.cy), gzh = float(g.cz);
+        const float gxl = float(dsub(g.cx, double(gxh))), gyl = float(dsub(g.cy, double(gyh))),
+                    gzl = float(dsub(g.cz, double(gzh)));
+        // absolute screen-error term from the FP32 rounding of node centres (|c| <= |g| + D)
+        const float tolc = 5e-7f * (fabsf(gxh) + fabsf(gyh) + fabsf(gzh));
         const bool has_sink = uint32_t(lane) < g.count;
+        // sinks by the SAME FP32 expression as their own list entries, (leaf centre - group
+        // centre) + rel: the self pair then has dx == 0 exactly (with eps > 0 any residue
+        // would act as m dx / eps^3; with eps == 0 the r2 == 0 skip needs it)
         float sx = 0.f, sy = 0.f, sz = 0.f;
         if (has_sink) {
-            const double4 q = t.xyzm[b.sinks[g.first + lane]];
-            sx = float(dsub(q.x, g.cx)), sy = float(dsub(q.y, g.cy)), sz = float(dsub(q.z, g.cz));
+            const uint32_t k = b.sinks[g.first + lane];
+            const WNode32 lf = ld_node32(t.nodes32 + t.leaf_of[k]);
+            const float4 r = ld_rel(t.rel + k);
+            sx = -((gxh - lf.cx) + gxl) + r.x;
+            sy = -((gyh - lf.cy) + gyl) + r.y;
+            sz = -((gzh - lf.cz) + gzl) + r.z;
         }
         const f2 sx2 = pk(sx, sx), sy2 = pk(sy, sy), sz2 = pk(sz, sz), e2 = pk(eps2, eps2);
         Acc2 acc{0ull, 0ull, 0ull, 0.f};
@@ -315,36 +341,36 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             // ---- MAC: FP32 screen with error bounds, exact FP64 only when undecided
             bool accept = false, leaf = false;
             uint32_t link = 0, info = 0;
-            float fx = 0.f, fy = 0.f, fz = 0.f, fm = 0.f;  // group centre - com (FP64 difference rounded), mass
+            float fx = 0.f, fy = 0.f, fz = 0.f, fm = 0.f;  // group centre - node centre (FP32), node mass
             if (valid) {
-                const WNode nd = t.nodes[c];
-                link = nd.link, info = nd.info;
+                const WNode32 nd = ld_node32(t.nodes32 + c);
+                link = nd.link, info = nd.info, fm = nd.m;
                 leaf = (info & kLeafBit) != 0;
-                fx = float(dsub(g.cx, nd.cx)), fy = float(dsub(g.cy, nd.cy)), fz = float(dsub(g.cz, nd.cz));
-                fm = float(nd.mass);
+                fx = (gxh - nd.cx) + gxl, fy = (gyh - nd.cy) + gyl, fz = (gzh - nd.cz) + gzl;
                 const float S = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
                 const float D = S > 0.f ? S * rsqrt_ftz(S) : 0.f;
                 const float d32 = D - radf;
-                // |d32 - d_fp64| <= ~6e-7 (D + R); 4e-6 leaves a 7x margin
-                const float tolabs = 4e-6f * (D + radf);
+                // |d32 - d_fp64| <= ~6e-7 (D + R) + 2.4e-7 (|gx|+|gy|+|gz|): 7x / 2x margins
+                const float tolabs = fmaf(4e-6f, D + radf, tolc);
                 int verdict = 2;  // 0 reject, 1 accept, 2 undecided
                 if (d32 <= -tolabs) {
                     verdict = 0;  // d <= 0: descend (traversal.cpp:46)
                 } else if (d32 > tolabs) {
                     const float rel = tolabs * rcp_ftz(d32);
                     if (geom) {
-                        const float lhs = float(nd.extent), r = thetaf * d32, tol = rel + 1e-6f;
-                        verdict = lhs <= r * (1.f - tol) ? 1 : (lhs > r * (1.f + tol) ? 0 : 2);
+                        const float r = thetaf * d32, tol = rel + 1e-6f;
+                        verdict = nd.b <= r * (1.f - tol) ? 1 : (nd.b > r * (1.f + tol) ? 0 : 2);
                     } else {
                         // G m b^2 / d^4 <= rhs  <=>  G m b^2 <= rhs d^4  (no division)
-                        const float ext = float(nd.extent), d2 = d32 * d32;
-                        const float num = G * fm * ext * ext, den = rhsf * (d2 * d2);
+                        const float d2 = d32 * d32;
+                        const float num = G * nd.q, den = rhsf * (d2 * d2);
                         const float tol = 4.f * rel + 1e-5f;
                         if (tol < 0.25f && den > 1e-30f)
                             verdict = num <= den * (1.f - tol) ? 1 : (num > den * (1.f + tol) ? 0 : 2);
                     }
                 }
-                accept = verdict == 2 ? mac_exact(nd, g, p, rhs, geom) : verdict == 1;
+                if (verdict == 2) verdict = mac_exact(t.nodes[c], g, p, rhs, geom) ? 1 : 0;
+                accept = verdict == 1;
             }
             const uint32_t nnode = (valid && accept) ? 1u : 0u;
             const uint32_t nleaf = (valid && !accept && leaf) ? (info & ~kLeafBit) : 0u;
@@ -413,17 +439,20 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 if (ltot) {
                     const int lbase = lsize + int(ntot);
                     if (nfast) {
+                        // entry = (leaf centre - group centre) + (particle - leaf centre), all FP32
+                        sm.leaf[lane] = make_float4(-fx, -fy, -fz, __uint_as_float(link));
                         const int pos = lbase + int(exc >> 20);
 #pragma unroll
                         for (uint32_t j = 0; j < 8; ++j)
-                            if (j < nfast) put_index(sm, pos + int(j), link + j);
+                            if (j < nfast) put_index(sm, pos + int(j), uint32_t(lane) | (j << 5));
                     }
                     __syncwarp();
                     for (uint32_t o = lane; o < ltot; o += 32) {
                         const int pos = lbase + int(o);
-                        const double4 q = t.xyzm[get_index(sm, pos)];
-                        put_entry(sm, pos, float(dsub(q.x, g.cx)), float(dsub(q.y, g.cy)), float(dsub(q.z, g.cz)),
-                                  float(q.w));
+                        const uint32_t v = get_index(sm, pos);
+                        const float4 L = sm.leaf[v & 31u];
+                        const float4 r = ld_rel(t.rel + (__float_as_uint(L.w) + (v >> 5)));
+                        put_entry(sm, pos, L.x + r.x, L.y + r.y, L.z + r.z, r.w);
                     }
                 }
                 lsize += int(P);
@@ -440,9 +469,8 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 __syncwarp();
                 while (true) {
                     for (; j < nb && pos + int(j) < kLcap; ++j) {
-                        const double4 q = t.xyzm[link + j];
-                        put_entry(sm, pos + int(j), float(dsub(q.x, g.cx)), float(dsub(q.y, g.cy)),
-                                  float(dsub(q.z, g.cz)), float(q.w));
+                        const float4 r = ld_rel(t.rel + (link + j));
+                        put_entry(sm, pos + int(j), r.x - fx, r.y - fy, r.z - fz, r.w);
                     }
                     if (end_all < kLcap) {
                         lsize = end_all;
