@@ -1,5 +1,5 @@
-// walkTree on sm_100a: warp-cooperative sink-group traversal with a shared
-// interaction list, acceleration MAC and FP32 rsqrtf force flush.
+// walkTree on sm_100a: warp-specialised sink-group traversal with
+// double-buffered interaction lists, acceleration MAC and FP32 rsqrt flush.
 //
 // Reference semantics (traversal.cpp:16-156, engine.cpp:31-81):
 //   * sinks in Morton-rank order are chunked into groups of group_size; each
@@ -9,32 +9,37 @@
 //     visiting order; events (interactions, mac_evals, list_pushes) are
 //     therefore reproduced exactly by any order, and accelerations differ only
 //     by FP32 summation order;
-//   * MAC decisions are evaluated in FP64 with the reference's operation
-//     order (exact), forces in FP32 on group-relative coordinates.
+//   * MAC decisions equal the reference's FP64 ones: an FP32 screen with
+//     rigorous error margins decides, the FP64 expression settles the rest.
 //
-// Execution model:
-//   * one warp = one task (group, subtree root); lane l owns sink l;
-//   * per-warp shared memory holds the interaction list (float4 x,y,z,m) and
-//     the top of a depth-first cell stack (32 cells popped per round, one per
-//     lane), spilling to a per-warp global stack;
+// Execution model (per CTA: kPairs producer/consumer warp pairs):
+//   * a PRODUCER warp runs one task (group, subtree root) at a time: it pops
+//     32 cells per round from a depth-first stack (shared top, global spill
+//     bottom), screens them, pushes children and writes list entries (FP32,
+//     relative to the group centre) into one of two shared list buffers;
+//   * its CONSUMER warp (lane l = sink l) flushes each full buffer into its
+//     FP32 accumulators: every entry acts on every sink (flush_list,
+//     traversal.cpp:61-84); buffers change hands through shared mbarriers,
+//     so traversal latency and the FP32/MUFU-bound flush overlap, and each
+//     side keeps its registers for its own work (ILP in the flush);
 //   * persistent grid, dynamic task queue: initially one task per group; a
-//     warp holding a large stack while the queue runs dry donates the
-//     shallow half of its stack as (group, cell) tasks — this splits the
-//     heavy-tailed "whole-system" groups across warps.  Partial
-//     accelerations are combined with FP32 atomics.
+//     producer holding a long stack donates its shallowest pending cells as
+//     (group, cells) batches, which split the heavy-tailed "whole-system"
+//     groups across warps.  Partial accelerations are combined
+//     with FP32 atomics.
 #include "kernels.cuh"
 
 namespace g2 {
 namespace {
 
+constexpr int kPairs = 4;                  // producer/consumer warp pairs per CTA
+constexpr int kThreads = 64 * kPairs;      // producers are warps 0..kPairs-1, consumers kPairs..2kPairs-1
 #ifndef G2_WALK_MINB
-#define G2_WALK_MINB 7  // resident CTAs per SM the register budget is tuned for
+#define G2_WALK_MINB 4  // resident CTAs per SM the register budget is tuned for
 #endif
-constexpr int kWarps = 4;
-constexpr int kThreads = 32 * kWarps;
-constexpr int kLcap = 384;                 // interaction-list entries per warp
-constexpr int kScap = 256;                 // shared stack entries per warp
-constexpr uint32_t kSpillWords = 16384;    // global stack entries per warp
+constexpr int kLcap = 384;                 // interaction-list entries per buffer
+constexpr int kScap = 256;                 // shared stack entries per producer
+constexpr uint32_t kSpillWords = 16384;    // global stack entries per producer
 constexpr int kDonateEvery = 64;           // rounds between donations of a long-running task
 constexpr int kQueuedEnough = 4096;        // queued donated batches above which heavy tasks keep their work
 constexpr uint64_t kEmpty = ~0ull;
@@ -42,32 +47,63 @@ constexpr int kRingBits = 20;              // donated-task ring: 2^20 slots, reu
 constexpr uint32_t kRing = 1u << kRingBits;
 constexpr uint64_t kGenMask = (1ull << 26) - 1;  // generation tag of a slot (ticket >> kRingBits)
 constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kFirst = 1, kLast = 2;  // buffer header flags: first / last buffer of a task
+constexpr uint32_t kStop = ~0u;            // header group id that retires the consumer
 
 // Interaction list in pair-interleaved layout so the flush runs on packed
 // f32x2 math (FADD2/FFMA2/FMUL2): entries 2p and 2p+1 live in
 //   la[p] = (x_2p, x_2p+1, y_2p, y_2p+1),  lb[p] = (z_2p, z_2p+1, m_2p, m_2p+1).
-struct WarpSmem {
+struct ListBuf {
     float4 la[kLcap / 2];
     float4 lb[kLcap / 2];
+};
+struct alignas(16) PairSmem {
+    ListBuf buf[2];
     uint32_t stack[kScap];
-    float4 leaf[32];  // per lane: (leaf com - group centre, first particle) of the leaf it opened this round
+    float4 leaf[32];      // per producer lane: (leaf com - group centre, first particle) of the leaf it opened
+    uint32_t hdr[2][4];   // per buffer: entry count, group, flags
+    uint64_t full[2];     // mbarriers: buffer written (producer -> consumer)
+    uint64_t empty[2];    // mbarriers: buffer flushed (consumer -> producer)
 };
 
-__device__ __forceinline__ float* entry_ptr(WarpSmem& sm, int pos) {
-    return reinterpret_cast<float*>(sm.la) + 2 * (pos & ~1) + (pos & 1);
+__device__ __forceinline__ float* entry_ptr(ListBuf& lb, int pos) {
+    return reinterpret_cast<float*>(lb.la) + 2 * (pos & ~1) + (pos & 1);
 }
 // entry pos: x, y at la[pos/2] lanes (pos&1) and 2 + (pos&1); z, m likewise in lb
-__device__ __forceinline__ void put_entry(WarpSmem& sm, int pos, float x, float y, float z, float m) {
-    float* a = entry_ptr(sm, pos);
+__device__ __forceinline__ void put_entry(ListBuf& lb, int pos, float x, float y, float z, float m) {
+    float* a = entry_ptr(lb, pos);
     a[0] = x, a[2] = y, a[2 * kLcap] = z, a[2 * kLcap + 2] = m;
 }
 // Opened-leaf particles are staged as (owner lane | j << 5) in the m slot of
 // their own list entry, then each lane replaces the slot(s) it owns by the entry.
-__device__ __forceinline__ void put_index(WarpSmem& sm, int pos, uint32_t k) {
-    reinterpret_cast<uint32_t*>(entry_ptr(sm, pos))[2 * kLcap + 2] = k;
+__device__ __forceinline__ void put_index(ListBuf& lb, int pos, uint32_t k) {
+    reinterpret_cast<uint32_t*>(entry_ptr(lb, pos))[2 * kLcap + 2] = k;
 }
-__device__ __forceinline__ uint32_t get_index(WarpSmem& sm, int pos) {
-    return reinterpret_cast<const uint32_t*>(entry_ptr(sm, pos))[2 * kLcap + 2];
+__device__ __forceinline__ uint32_t get_index(ListBuf& lb, int pos) {
+    return reinterpret_cast<const uint32_t*>(entry_ptr(lb, pos))[2 * kLcap + 2];
+}
+
+// ---- shared-memory mbarriers (one phase per buffer hand-over, all 32 lanes arrive)
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    const uint32_t a = smem_addr(bar);
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity)
+            : "memory");
+    } while (!ok);
 }
 
 // ---- packed f32x2 helpers (sm_100a PTX) --------------------------------------
@@ -153,44 +189,56 @@ __device__ __forceinline__ uint32_t warp_excl_scan(uint32_t x, uint32_t& total) 
 
 // All-pairs burst: every list entry acts on this lane's sink (flush_list,
 // traversal.cpp:61-84).  27 Flop per interaction by the reference convention.
-// Two entries per iteration on packed f32x2 lanes; accumulators are pairs that
-// the caller folds at the end.  cnt may be odd: the pad entry is (0,0,0,m=0).
+// Entries are processed two pairs at a time on packed f32x2 lanes (two
+// independent dependency chains per iteration); accumulators are pairs that
+// are folded at the end.  cnt is even (the producer pads with (0,0,0,m=0)).
 struct Acc2 {
     f2 x, y, z;
     float ph;
 };
 
 template <bool kPot, bool kEps0>
-__device__ __forceinline__ void flush_list(const WarpSmem& sm, int cnt, f2 sx, f2 sy, f2 sz, f2 eps2, Acc2& a) {
-    const int np = (cnt + 1) >> 1;
-#pragma unroll 4
-    for (int p = 0; p < np; ++p) {
-        const ulonglong2 A = *reinterpret_cast<const ulonglong2*>(&sm.la[p]);
-        const ulonglong2 B = *reinterpret_cast<const ulonglong2*>(&sm.lb[p]);
-        const f2 dx = sub2(A.x, sx), dy = sub2(A.y, sy), dz = sub2(B.x, sz);
-        f2 r2 = fma2(dx, dx, eps2);
-        r2 = fma2(dy, dy, r2);
-        r2 = fma2(dz, dz, r2);
-        float r0, r1;
-        upk(r2, r0, r1);
-        float i0 = rsqrt_ftz(r0), i1 = rsqrt_ftz(r1);
-        if (kEps0) {  // r2 == 0 self term contributes nothing (traversal.cpp:73)
-            i0 = r0 > 0.0f ? i0 : 0.0f;
-            i1 = r1 > 0.0f ? i1 : 0.0f;
-        }
-        const f2 inv = pk(i0, i1);
-        const f2 mi = mul2(B.y, inv);
-        const f2 f = mul2(mi, mul2(inv, inv));
-        a.x = fma2(f, dx, a.x);
-        a.y = fma2(f, dy, a.y);
-        a.z = fma2(f, dz, a.z);
-        if (kPot) {  // self potential excluded (traversal.cpp:78)
-            float m0, m1, e0, e1;
-            upk(mi, m0, m1);
-            upk(eps2, e0, e1);
-            a.ph -= (r0 - e0 > 0.0f ? m0 : 0.0f) + (r1 - e1 > 0.0f ? m1 : 0.0f);
-        }
+__device__ __forceinline__ void pair_force(const ulonglong2 A, const ulonglong2 B, f2 sx, f2 sy, f2 sz, f2 eps2,
+                                           Acc2& a) {
+    const f2 dx = sub2(A.x, sx), dy = sub2(A.y, sy), dz = sub2(B.x, sz);
+    f2 r2 = fma2(dx, dx, eps2);
+    r2 = fma2(dy, dy, r2);
+    r2 = fma2(dz, dz, r2);
+    float r0, r1;
+    upk(r2, r0, r1);
+    float i0 = rsqrt_ftz(r0), i1 = rsqrt_ftz(r1);
+    if (kEps0) {  // r2 == 0 self term contributes nothing (traversal.cpp:73)
+        i0 = r0 > 0.0f ? i0 : 0.0f;
+        i1 = r1 > 0.0f ? i1 : 0.0f;
     }
+    const f2 inv = pk(i0, i1);
+    const f2 mi = mul2(B.y, inv);
+    const f2 f = mul2(mi, mul2(inv, inv));
+    a.x = fma2(f, dx, a.x);
+    a.y = fma2(f, dy, a.y);
+    a.z = fma2(f, dz, a.z);
+    if (kPot) {  // self potential excluded (traversal.cpp:78)
+        float m0, m1, e0, e1;
+        upk(mi, m0, m1);
+        upk(eps2, e0, e1);
+        a.ph -= (r0 - e0 > 0.0f ? m0 : 0.0f) + (r1 - e1 > 0.0f ? m1 : 0.0f);
+    }
+}
+
+template <bool kPot, bool kEps0>
+__device__ __forceinline__ void flush_list(const ListBuf& lb, int cnt, f2 sx, f2 sy, f2 sz, f2 eps2, Acc2& a,
+                                           Acc2& b) {
+    const int np = cnt >> 1;
+    const ulonglong2* pa = reinterpret_cast<const ulonglong2*>(lb.la);
+    const ulonglong2* pb = reinterpret_cast<const ulonglong2*>(lb.lb);
+    int p = 0;
+#pragma unroll 2
+    for (; p + 1 < np; p += 2) {
+        const ulonglong2 A0 = pa[p], B0 = pb[p], A1 = pa[p + 1], B1 = pb[p + 1];
+        pair_force<kPot, kEps0>(A0, B0, sx, sy, sz, eps2, a);
+        pair_force<kPot, kEps0>(A1, B1, sx, sy, sz, eps2, b);
+    }
+    if (p < np) pair_force<kPot, kEps0>(pa[p], pb[p], sx, sy, sz, eps2, a);
 }
 
 // Exact FP64 MAC in the reference's operation order (traversal.cpp:40-56).
@@ -207,10 +255,72 @@ __device__ __forceinline__ bool mac_exact(const WNode& nd, const GroupRec& g, co
 
 template <bool kPot, bool kEps0, bool kCheck>
 __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t, WalkParams p, WalkBuffers b, DevFlags* flags) {
-    __shared__ WarpSmem smem[kWarps];
-    const int lane = threadIdx.x & 31;
-    WarpSmem& sm = smem[threadIdx.x >> 5];
-    uint32_t* spill = b.spill + (size_t(blockIdx.x) * kWarps + (threadIdx.x >> 5)) * kSpillWords;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    PairSmem* const pairs = reinterpret_cast<PairSmem*>(smem_raw);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < kPairs) {
+        PairSmem& ps = pairs[threadIdx.x];
+        for (int i = 0; i < 2; ++i) mbar_init(&ps.full[i], 32), mbar_init(&ps.empty[i], 32);
+    }
+    __syncthreads();
+    const float G = float(p.G);
+
+    if (warp >= kPairs) {
+        // ================================ consumer: flush buffers into the sinks' accumulators
+        PairSmem& ps = pairs[warp - kPairs];
+        const float eps2 = float(p.eps * p.eps);
+        const f2 e2 = pk(eps2, eps2);
+        f2 sx2 = 0, sy2 = 0, sz2 = 0;
+        Acc2 a0{0ull, 0ull, 0ull, 0.f}, a1{0ull, 0ull, 0ull, 0.f};
+        uint32_t gfirst = 0;
+        bool has_sink = false;
+        for (uint32_t it = 0;; ++it) {
+            const int bi = int(it & 1);
+            mbar_wait(&ps.full[bi], (it >> 1) & 1);
+            const uint32_t cnt = ps.hdr[bi][0], grp = ps.hdr[bi][1], fl = ps.hdr[bi][2];
+            if (grp == kStop) break;
+            if (fl & kFirst) {
+                // sinks by the SAME FP32 expression as their own list entries, (leaf centre - group
+                // centre) + rel: the self pair then has dx == 0 exactly (with eps > 0 any residue
+                // would act as m dx / eps^3; with eps == 0 the r2 == 0 skip needs it)
+                const GroupRec g = b.groups[grp];
+                const float gxh = float(g.cx), gyh = float(g.cy), gzh = float(g.cz);
+                const float gxl = float(dsub(g.cx, double(gxh))), gyl = float(dsub(g.cy, double(gyh))),
+                            gzl = float(dsub(g.cz, double(gzh)));
+                has_sink = uint32_t(lane) < g.count;
+                gfirst = g.first;
+                float sx = 0.f, sy = 0.f, sz = 0.f;
+                if (has_sink) {
+                    const uint32_t k = b.sinks[g.first + lane];
+                    const WNode32 lf = ld_node32(t.nodes32 + t.leaf_of[k]);
+                    const float4 r = ld_rel(t.rel + k);
+                    sx = -((gxh - lf.cx) + gxl) + r.x;
+                    sy = -((gyh - lf.cy) + gyl) + r.y;
+                    sz = -((gzh - lf.cz) + gzl) + r.z;
+                }
+                sx2 = pk(sx, sx), sy2 = pk(sy, sy), sz2 = pk(sz, sz);
+                a0 = Acc2{0ull, 0ull, 0ull, 0.f}, a1 = a0;
+            }
+            flush_list<kPot, kEps0>(ps.buf[bi], int(cnt), sx2, sy2, sz2, e2, a0, a1);
+            __syncwarp();
+            mbar_arrive(&ps.empty[bi]);
+            if ((fl & kLast) && has_sink) {
+                float x0, x1, y0, y1, z0, z1, u0, u1, v0, v1, w0, w1;
+                upk(a0.x, x0, x1), upk(a0.y, y0, y1), upk(a0.z, z0, z1);
+                upk(a1.x, u0, u1), upk(a1.y, v0, v1), upk(a1.z, w0, w1);
+                float4* out = &b.accum[gfirst + lane];
+                atomicAdd(&out->x, G * ((x0 + x1) + (u0 + u1)));
+                atomicAdd(&out->y, G * ((y0 + y1) + (v0 + v1)));
+                atomicAdd(&out->z, G * ((z0 + z1) + (w0 + w1)));
+                if (kPot) atomicAdd(&out->w, G * (a0.ph + a1.ph));
+            }
+        }
+        return;
+    }
+
+    // ==================================== producer: traversal
+    PairSmem& sm = pairs[warp];
+    uint32_t* spill = b.spill + (size_t(blockIdx.x) * kPairs + warp) * kSpillWords;
     // Task sources: the initial tasks (one per group, claimed by counter, in
     // b.order when given: heaviest first) and the FIFO of donated batches of
     // (group, up to 32 cells), which has priority so heavy groups are split
@@ -221,9 +331,20 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
     uint32_t* q_dhead = b.qstate + 4;  // donated slots claimed
     const uint32_t ng = b.qstate[3];   // initial tasks (written by walk_init)
     const uint32_t glo = b.group_lo;
-    const float eps2 = float(p.eps * p.eps);
-    const float G = float(p.G);
     const float thetaf = float(p.theta);
+    uint32_t hand = 0;  // buffers handed to the consumer so far: buffer = hand & 1
+
+    // hand the current buffer (lsize entries, padded to even) to the consumer, then
+    // wait until the next buffer has been flushed (phase parity of its previous use)
+    auto handoff = [&](int lsize, uint32_t grp, uint32_t fl) {
+        const int bi = int(hand & 1);
+        if ((lsize & 1) && lane == 0) put_entry(sm.buf[bi], lsize, 0.f, 0.f, 0.f, 0.f);
+        if (lane == 0) sm.hdr[bi][0] = uint32_t(lsize + (lsize & 1)), sm.hdr[bi][1] = grp, sm.hdr[bi][2] = fl;
+        __syncwarp();
+        mbar_arrive(&sm.full[bi]);
+        ++hand;
+        mbar_wait(&sm.empty[hand & 1], ((hand >> 1) & 1) ^ 1);
+    };
 
     // lane 0 may hold a claimed donated slot that is not written yet ("owed"):
     // claims are fetch-adds (no CAS retry storms); an owed slot is serviced as
@@ -269,11 +390,11 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             }
         }
         e = __shfl_sync(kFull, e, 0);
-        if (e == kEmpty) return;
+        if (e == kEmpty) break;
         slot = __shfl_sync(kFull, slot, 0);
         const uint32_t grp = uint32_t(e >> 32), nbatch = uint32_t(e) & 63u;
 
-        // ---------------- group and sinks
+        // ---------------- group
         uint64_t t_begin = 0;
         if (b.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
         const GroupRec g = b.groups[grp];
@@ -287,22 +408,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                     gzl = float(dsub(g.cz, double(gzh)));
         // absolute screen-error term from the FP32 rounding of node centres (|c| <= |g| + D)
         const float tolc = 5e-7f * (fabsf(gxh) + fabsf(gyh) + fabsf(gzh));
-        const bool has_sink = uint32_t(lane) < g.count;
-        // sinks by the SAME FP32 expression as their own list entries, (leaf centre - group
-        // centre) + rel: the self pair then has dx == 0 exactly (with eps > 0 any residue
-        // would act as m dx / eps^3; with eps == 0 the r2 == 0 skip needs it)
-        float sx = 0.f, sy = 0.f, sz = 0.f;
-        if (has_sink) {
-            const uint32_t k = b.sinks[g.first + lane];
-            const WNode32 lf = ld_node32(t.nodes32 + t.leaf_of[k]);
-            const float4 r = ld_rel(t.rel + k);
-            sx = -((gxh - lf.cx) + gxl) + r.x;
-            sy = -((gyh - lf.cy) + gyl) + r.y;
-            sz = -((gzh - lf.cz) + gzl) + r.z;
-        }
-        const f2 sx2 = pk(sx, sx), sy2 = pk(sy, sy), sz2 = pk(sz, sz), e2 = pk(eps2, eps2);
-        Acc2 acc{0ull, 0ull, 0ull, 0.f};
-        uint32_t macs = 0, pushes = 0;
+        uint32_t macs = 0, pushes = 0, tflags = kFirst;
         // logical LIFO = spill[gbase, gtop) (bottom, global) ++ sm.stack[0, ssize) (top, shared)
         int ssize, gbase = 0, gtop = 0, lsize = 0, iter = 0, last_donation = 0;
         uint32_t pv_dh = 0, pv_dt = 0, pv_init = 0;  // lane 0: queue counters read at the previous check
@@ -321,6 +427,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         __syncwarp();
 
         while (ssize + gtop - gbase > 0) {
+            ListBuf& lb = sm.buf[hand & 1];
             // ---- pop up to 32 cells, one per lane
             int take;
             uint32_t c = 0;
@@ -426,16 +533,16 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
 
             // ---- accepted cells (owner lanes) and opened leaves (cooperative): list entries
             const uint32_t P = ntot + ltot;
+            ListBuf* lbp = &lb;
             if (P) {
                 if (lsize + int(P) > kLcap) {
-                    if ((lsize & 1) && lane == 0) put_entry(sm, lsize, 0.f, 0.f, 0.f, 0.f);
-                    __syncwarp();
-                    flush_list<kPot, kEps0>(sm, lsize, sx2, sy2, sz2, e2, acc);
-                    __syncwarp();
+                    handoff(lsize, grp, tflags);
+                    tflags = 0;
                     lsize = 0;
+                    lbp = &sm.buf[hand & 1];
                 }
-                // entry = com - group centre = -(group centre - com): the same rounded FP64 difference
-                if (nnode) put_entry(sm, lsize + int((exc >> 10) & 1023u), -fx, -fy, -fz, fm);
+                // entry = node centre - group centre = -(group centre - node centre)
+                if (nnode) put_entry(*lbp, lsize + int((exc >> 10) & 1023u), -fx, -fy, -fz, fm);
                 if (ltot) {
                     const int lbase = lsize + int(ntot);
                     if (nfast) {
@@ -444,15 +551,15 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                         const int pos = lbase + int(exc >> 20);
 #pragma unroll
                         for (uint32_t j = 0; j < 8; ++j)
-                            if (j < nfast) put_index(sm, pos + int(j), uint32_t(lane) | (j << 5));
+                            if (j < nfast) put_index(*lbp, pos + int(j), uint32_t(lane) | (j << 5));
                     }
                     __syncwarp();
                     for (uint32_t o = lane; o < ltot; o += 32) {
                         const int pos = lbase + int(o);
-                        const uint32_t v = get_index(sm, pos);
+                        const uint32_t v = get_index(*lbp, pos);
                         const float4 L = sm.leaf[v & 31u];
                         const float4 r = ld_rel(t.rel + (__float_as_uint(L.w) + (v >> 5)));
-                        put_entry(sm, pos, L.x + r.x, L.y + r.y, L.z + r.z, r.w);
+                        put_entry(*lbp, pos, L.x + r.x, L.y + r.y, L.z + r.z, r.w);
                     }
                 }
                 lsize += int(P);
@@ -470,15 +577,16 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 while (true) {
                     for (; j < nb && pos + int(j) < kLcap; ++j) {
                         const float4 r = ld_rel(t.rel + (link + j));
-                        put_entry(sm, pos + int(j), r.x - fx, r.y - fy, r.z - fz, r.w);
+                        put_entry(*lbp, pos + int(j), r.x - fx, r.y - fy, r.z - fz, r.w);
                     }
                     if (end_all < kLcap) {
                         lsize = end_all;
                         break;
                     }
                     __syncwarp();
-                    flush_list<kPot, kEps0>(sm, kLcap, sx2, sy2, sz2, e2, acc);
-                    __syncwarp();
+                    handoff(kLcap, grp, tflags);
+                    tflags = 0;
+                    lbp = &sm.buf[hand & 1];
                     pos -= kLcap;
                     end_all -= kLcap;
                     if (end_all == 0) {
@@ -541,23 +649,10 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 }
             }
         }
-        if (lsize) {
-            if ((lsize & 1) && lane == 0) put_entry(sm, lsize, 0.f, 0.f, 0.f, 0.f);  // pad the last pair
-            __syncwarp();
-            flush_list<kPot, kEps0>(sm, lsize, sx2, sy2, sz2, e2, acc);
-        }
-        __syncwarp();
+        // the last buffer of the task (possibly empty) tells the consumer to write out
+        handoff(lsize, grp, tflags | kLast);
 
-        // ---------------- results and events
-        if (has_sink) {
-            float x0, x1, y0, y1, z0, z1;
-            upk(acc.x, x0, x1), upk(acc.y, y0, y1), upk(acc.z, z0, z1);
-            float4* out = &b.accum[g.first + lane];
-            atomicAdd(&out->x, G * (x0 + x1));
-            atomicAdd(&out->y, G * (y0 + y1));
-            atomicAdd(&out->z, G * (z0 + z1));
-            if (kPot) atomicAdd(&out->w, G * acc.ph);
-        }
+        // ---------------- events
         if (lane == 0) {
             const unsigned long long inter = (unsigned long long)pushes * g.count;
             if (p.count_ops) {
@@ -580,6 +675,10 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             atomicSub(q_pending, 1u);
         }
     }
+    // retire the consumer
+    if (lane == 0) sm.hdr[hand & 1][0] = 0, sm.hdr[hand & 1][1] = kStop, sm.hdr[hand & 1][2] = 0;
+    __syncwarp();
+    mbar_arrive(&sm.full[hand & 1]);
 }
 
 // one warp per group: AABB centre, radius and a_min (make_group, traversal.cpp:16-38)
@@ -655,12 +754,18 @@ __global__ void finalize_kernel(WalkBuffers b, uint32_t cap, double* ax, double*
     }
 }
 
+constexpr int kWalkSmem = kPairs * int(sizeof(PairSmem));
+constexpr int kMaxBlocksPerSM = 8;  // bound for the spill area (occupancy is smem-limited well below)
+
 template <bool kPot, bool kEps0, bool kCheck>
 int walk_blocks_per_sm() {
     static int v = 0;
     if (!v) {
-        G2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, walk_kernel<kPot, kEps0, kCheck>, kThreads, 0));
-        if (v < 1) v = 1;
+        G2_CUDA(cudaFuncSetAttribute(walk_kernel<kPot, kEps0, kCheck>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kWalkSmem));
+        G2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, walk_kernel<kPot, kEps0, kCheck>, kThreads,
+                                                              kWalkSmem));
+        v = std::max(1, std::min(v, kMaxBlocksPerSM));
     }
     return v;
 }
@@ -669,15 +774,15 @@ template <bool kPot, bool kEps0, bool kCheck>
 void walk_launch_t(const TreeView& t, const WalkParams& p, const WalkBuffers& b, DevFlags* flags, cudaStream_t s) {
     const int per_sm = walk_blocks_per_sm<kPot, kEps0, kCheck>();
     const unsigned grid = unsigned(per_sm * kNumSMs);
-    G2_COUNT(1), walk_kernel<kPot, kEps0, kCheck><<<grid, kThreads, 0, s>>>(t, p, b, flags);
+    G2_COUNT(1), walk_kernel<kPot, kEps0, kCheck><<<grid, kThreads, kWalkSmem, s>>>(t, p, b, flags);
 }
 
 }  // namespace
 
 size_t walk_spill_words() { return kSpillWords; }
 size_t walk_resident_warps() {
-    // upper bound over the template variants (same smem, similar registers)
-    return size_t(kNumSMs) * 16 * kWarps;
+    // producer warps (one spill stack each) of the largest grid walk_launch_t can use
+    return size_t(kNumSMs) * kMaxBlocksPerSM * kPairs;
 }
 
 void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffers& b, uint32_t group_size,
