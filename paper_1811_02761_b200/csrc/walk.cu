@@ -37,8 +37,8 @@ constexpr int kThreads = 64 * kPairs;      // producers are warps 0..kPairs-1, c
 #ifndef G2_WALK_MINB
 #define G2_WALK_MINB 4  // resident CTAs per SM the register budget is tuned for
 #endif
-constexpr int kLcap = 384;                 // interaction-list entries per buffer
-constexpr int kScap = 256;                 // shared stack entries per producer
+constexpr int kLcap = 336;                 // interaction-list entries per buffer (4 CTAs x 4 pairs fit 228 KB)
+constexpr int kScap = 512;                 // shared stack entries per producer (>= 64 cells x 8 children)
 constexpr uint32_t kSpillWords = 16384;    // global stack entries per producer
 constexpr int kDonateEvery = 64;           // rounds between donations of a long-running task
 constexpr int kQueuedEnough = 4096;        // queued donated batches above which heavy tasks keep their work
@@ -60,7 +60,7 @@ struct ListBuf {
 struct alignas(16) PairSmem {
     ListBuf buf[2];
     uint32_t stack[kScap];
-    float4 leaf[32];      // per producer lane: (leaf com - group centre, first particle) of the leaf it opened
+    float4 leaf[64];      // per popped cell: (leaf com - group centre, first particle) of an opened leaf
     uint32_t hdr[2][4];   // per buffer: entry count, group, flags
     uint64_t full[2];     // mbarriers: buffer written (producer -> consumer)
     uint64_t empty[2];    // mbarriers: buffer flushed (consumer -> producer)
@@ -253,6 +253,53 @@ __device__ __forceinline__ bool mac_exact(const WNode& nd, const GroupRec& g, co
     return lhs <= rhs;
 }
 
+// FP32 MAC screen of one cell against the group (FP32 centre split hi + lo), with
+// rigorous error margins; the exact FP64 expression settles undecided cells.
+struct Screen {
+    float fx, fy, fz, fm;  // group centre - node centre (FP32), node mass
+    uint32_t link, info;
+    bool accept;
+    __device__ __forceinline__ bool leaf() const { return (info & kLeafBit) != 0; }
+    __device__ __forceinline__ uint32_t nchild() const { return (!accept && !leaf()) ? (info & 0xffu) : 0u; }
+    __device__ __forceinline__ uint32_t nleaf() const { return (!accept && leaf()) ? (info & ~kLeafBit) : 0u; }
+};
+
+__device__ __forceinline__ Screen screen(const TreeView& t, const GroupRec& g, const WalkParams& p, uint32_t c,
+                                         bool valid, float gxh, float gyh, float gzh, float gxl, float gyl, float gzl,
+                                         float tolc, float radf, float rhsf, double rhs, float G, float thetaf,
+                                         bool geom) {
+    Screen s{0.f, 0.f, 0.f, 0.f, 0u, 0u, false};
+    if (!valid) return s;  // info 0: internal with no children, not accepted -> contributes nothing
+    const WNode32 nd = ld_node32(t.nodes32 + c);
+    s.link = nd.link, s.info = nd.info, s.fm = nd.m;
+    s.fx = (gxh - nd.cx) + gxl, s.fy = (gyh - nd.cy) + gyl, s.fz = (gzh - nd.cz) + gzl;
+    const float S = fmaf(s.fx, s.fx, fmaf(s.fy, s.fy, s.fz * s.fz));
+    const float D = S > 0.f ? S * rsqrt_ftz(S) : 0.f;
+    const float d32 = D - radf;
+    // |d32 - d_fp64| <= ~6e-7 (D + R) + 2.4e-7 (|gx|+|gy|+|gz|): 7x / 2x margins
+    const float tolabs = fmaf(4e-6f, D + radf, tolc);
+    int verdict = 2;  // 0 reject, 1 accept, 2 undecided
+    if (d32 <= -tolabs) {
+        verdict = 0;  // d <= 0: descend (traversal.cpp:46)
+    } else if (d32 > tolabs) {
+        const float rel = tolabs * rcp_ftz(d32);
+        if (geom) {
+            const float r = thetaf * d32, tol = rel + 1e-6f;
+            verdict = nd.b <= r * (1.f - tol) ? 1 : (nd.b > r * (1.f + tol) ? 0 : 2);
+        } else {
+            // G m b^2 / d^4 <= rhs  <=>  G m b^2 <= rhs d^4  (no division)
+            const float d2 = d32 * d32;
+            const float num = G * nd.q, den = rhsf * (d2 * d2);
+            const float tol = 4.f * rel + 1e-5f;
+            if (tol < 0.25f && den > 1e-30f)
+                verdict = num <= den * (1.f - tol) ? 1 : (num > den * (1.f + tol) ? 0 : 2);
+        }
+    }
+    if (verdict == 2) verdict = mac_exact(t.nodes[c], g, p, rhs, geom) ? 1 : 0;
+    s.accept = verdict == 1;
+    return s;
+}
+
 template <bool kPot, bool kEps0, bool kCheck>
 __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t, WalkParams p, WalkBuffers b, DevFlags* flags) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -427,65 +474,36 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         __syncwarp();
 
         while (ssize + gtop - gbase > 0) {
-            ListBuf& lb = sm.buf[hand & 1];
-            // ---- pop up to 32 cells, one per lane
+            ListBuf* lbp = &sm.buf[hand & 1];
+            // ---- pop up to 64 cells, two per lane (two independent MAC chains per lane)
             int take;
-            uint32_t c = 0;
+            uint32_t c0 = 0, c1 = 0;
             if (ssize > 0) {
-                take = min(ssize, 32);
-                if (lane < take) c = sm.stack[ssize - 1 - lane];
+                take = min(ssize, 64);
+                if (lane < take) c0 = sm.stack[ssize - 1 - lane];
+                if (lane + 32 < take) c1 = sm.stack[ssize - 33 - lane];
                 ssize -= take;
             } else {
-                take = min(gtop - gbase, 32);
-                if (lane < take) c = spill[gtop - 1 - lane];
+                take = min(gtop - gbase, 64);
+                if (lane < take) c0 = spill[gtop - 1 - lane];
+                if (lane + 32 < take) c1 = spill[gtop - 33 - lane];
                 gtop -= take;
                 if (gtop == gbase) gtop = gbase = 0;
             }
             __syncwarp();
             macs += take;
-            const bool valid = lane < take;
+            const bool valid0 = lane < take, valid1 = lane + 32 < take;
+            const Screen s0 = screen(t, g, p, c0, valid0, gxh, gyh, gzh, gxl, gyl, gzl, tolc, radf, rhsf, rhs, G, thetaf,
+                                     geom);
+            const Screen s1 = screen(t, g, p, c1, valid1, gxh, gyh, gzh, gxl, gyl, gzl, tolc, radf, rhsf, rhs, G, thetaf,
+                                     geom);
+            const uint32_t nchild0 = s0.nchild(), nchild1 = s1.nchild();
+            const uint32_t nleaf0 = s0.nleaf(), nleaf1 = s1.nleaf();
+            const uint32_t nfast0 = nleaf0 <= 8u ? nleaf0 : 0u, nfast1 = nleaf1 <= 8u ? nleaf1 : 0u;
+            const uint32_t nnode0 = s0.accept ? 1u : 0u, nnode1 = s1.accept ? 1u : 0u;
 
-            // ---- MAC: FP32 screen with error bounds, exact FP64 only when undecided
-            bool accept = false, leaf = false;
-            uint32_t link = 0, info = 0;
-            float fx = 0.f, fy = 0.f, fz = 0.f, fm = 0.f;  // group centre - node centre (FP32), node mass
-            if (valid) {
-                const WNode32 nd = ld_node32(t.nodes32 + c);
-                link = nd.link, info = nd.info, fm = nd.m;
-                leaf = (info & kLeafBit) != 0;
-                fx = (gxh - nd.cx) + gxl, fy = (gyh - nd.cy) + gyl, fz = (gzh - nd.cz) + gzl;
-                const float S = fmaf(fx, fx, fmaf(fy, fy, fz * fz));
-                const float D = S > 0.f ? S * rsqrt_ftz(S) : 0.f;
-                const float d32 = D - radf;
-                // |d32 - d_fp64| <= ~6e-7 (D + R) + 2.4e-7 (|gx|+|gy|+|gz|): 7x / 2x margins
-                const float tolabs = fmaf(4e-6f, D + radf, tolc);
-                int verdict = 2;  // 0 reject, 1 accept, 2 undecided
-                if (d32 <= -tolabs) {
-                    verdict = 0;  // d <= 0: descend (traversal.cpp:46)
-                } else if (d32 > tolabs) {
-                    const float rel = tolabs * rcp_ftz(d32);
-                    if (geom) {
-                        const float r = thetaf * d32, tol = rel + 1e-6f;
-                        verdict = nd.b <= r * (1.f - tol) ? 1 : (nd.b > r * (1.f + tol) ? 0 : 2);
-                    } else {
-                        // G m b^2 / d^4 <= rhs  <=>  G m b^2 <= rhs d^4  (no division)
-                        const float d2 = d32 * d32;
-                        const float num = G * nd.q, den = rhsf * (d2 * d2);
-                        const float tol = 4.f * rel + 1e-5f;
-                        if (tol < 0.25f && den > 1e-30f)
-                            verdict = num <= den * (1.f - tol) ? 1 : (num > den * (1.f + tol) ? 0 : 2);
-                    }
-                }
-                if (verdict == 2) verdict = mac_exact(t.nodes[c], g, p, rhs, geom) ? 1 : 0;
-                accept = verdict == 1;
-            }
-            const uint32_t nnode = (valid && accept) ? 1u : 0u;
-            const uint32_t nleaf = (valid && !accept && leaf) ? (info & ~kLeafBit) : 0u;
-            const uint32_t nchild = (valid && !accept && !leaf) ? (info & 0xffu) : 0u;
-            const uint32_t nfast = nleaf <= 8u ? nleaf : 0u;  // oversized leaves take the slow path below
-
-            // one packed scan: children | accepted nodes << 10 | leaf particles << 20
-            const uint32_t v = nchild | (nnode << 10) | (nfast << 20);
+            // one packed scan: children (<= 512) | accepted nodes (<= 64) << 10 | leaf particles (<= 512) << 17
+            const uint32_t v = (nchild0 + nchild1) | ((nnode0 + nnode1) << 10) | ((nfast0 + nfast1) << 17);
             uint32_t inc = v;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -493,12 +511,15 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 if (lane >= o) inc += y;
             }
             const uint32_t tot = __shfl_sync(kFull, inc, 31), exc = inc - v;
-            const uint32_t ctot = tot & 1023u, ntot = (tot >> 10) & 1023u, ltot = tot >> 20;
+            const uint32_t ctot = tot & 1023u, ntot = (tot >> 10) & 127u, ltot = tot >> 17;
 
             // ---- rejected internal cells: children onto the stack (cooperative)
             if (ctot) {
-                if (kCheck && nchild)
-                    atomicAdd(&b.level_count[size_t(grp - glo) * (kMaxDepth + 1) + ((info >> 8) & 31u) + 1u], nchild);
+                if (kCheck) {
+                    uint32_t* lc = &b.level_count[size_t(grp - glo) * (kMaxDepth + 1) + 1u];
+                    if (nchild0) atomicAdd(lc + ((s0.info >> 8) & 31u), nchild0);
+                    if (nchild1) atomicAdd(lc + ((s1.info >> 8) & 31u), nchild1);
+                }
                 if (ssize + int(ctot) > kScap) {
                     // shared part full: move it onto the spill top, keeping one logical
                     // LIFO (spill = bottom, shared = top) so the depth-first bound holds
@@ -522,18 +543,49 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                     }
                     __syncwarp();
                 }
-                if (ssize + int(ctot) <= kScap) {  // <= 8 children per lane: a short predicated loop
+                if (ssize + int(ctot) <= kScap) {  // <= 8 children per cell: short predicated loops
                     uint32_t* dst = sm.stack + ssize + (exc & 1023u);
 #pragma unroll
                     for (uint32_t j = 0; j < 8; ++j)
-                        if (j < nchild) dst[j] = link + j;
+                        if (j < nchild0) dst[j] = s0.link + j;
+                    dst += nchild0;
+#pragma unroll
+                    for (uint32_t j = 0; j < 8; ++j)
+                        if (j < nchild1) dst[j] = s1.link + j;
                     ssize += int(ctot);
                 }
             }
 
             // ---- accepted cells (owner lanes) and opened leaves (cooperative): list entries
+            // Leaf particles: entry = (leaf centre - group centre) + (particle - leaf centre), all
+            // FP32, staged as (leaf slot | j << 6) with slot = lane (cell 0) or 32 + lane (cell 1);
+            // lane entries start at lane_ofs (cell 0's particles, then cell 1's).
+            auto write_leaves = [&](uint32_t nf0, uint32_t nf1, int base, int lane_ofs, uint32_t total) {
+                int pos = base + lane_ofs;
+                if (nf0) {
+                    sm.leaf[lane] = make_float4(-s0.fx, -s0.fy, -s0.fz, __uint_as_float(s0.link));
+#pragma unroll
+                    for (uint32_t j = 0; j < 8; ++j)
+                        if (j < nf0) put_index(*lbp, pos + int(j), uint32_t(lane) | (j << 6));
+                    pos += int(nf0);
+                }
+                if (nf1) {
+                    sm.leaf[32 + lane] = make_float4(-s1.fx, -s1.fy, -s1.fz, __uint_as_float(s1.link));
+#pragma unroll
+                    for (uint32_t j = 0; j < 8; ++j)
+                        if (j < nf1) put_index(*lbp, pos + int(j), uint32_t(32 + lane) | (j << 6));
+                }
+                __syncwarp();
+                for (uint32_t o = lane; o < total; o += 32) {
+                    const int q = base + int(o);
+                    const uint32_t vv = get_index(*lbp, q);
+                    const float4 L = sm.leaf[vv & 63u];
+                    const float4 r = ld_rel(t.rel + (__float_as_uint(L.w) + (vv >> 6)));
+                    put_entry(*lbp, q, L.x + r.x, L.y + r.y, L.z + r.z, r.w);
+                }
+                __syncwarp();
+            };
             const uint32_t P = ntot + ltot;
-            ListBuf* lbp = &lb;
             if (P) {
                 if (lsize + int(P) > kLcap) {
                     handoff(lsize, grp, tflags);
@@ -542,57 +594,65 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                     lbp = &sm.buf[hand & 1];
                 }
                 // entry = node centre - group centre = -(group centre - node centre)
-                if (nnode) put_entry(*lbp, lsize + int((exc >> 10) & 1023u), -fx, -fy, -fz, fm);
-                if (ltot) {
-                    const int lbase = lsize + int(ntot);
-                    if (nfast) {
-                        // entry = (leaf centre - group centre) + (particle - leaf centre), all FP32
-                        sm.leaf[lane] = make_float4(-fx, -fy, -fz, __uint_as_float(link));
-                        const int pos = lbase + int(exc >> 20);
-#pragma unroll
-                        for (uint32_t j = 0; j < 8; ++j)
-                            if (j < nfast) put_index(*lbp, pos + int(j), uint32_t(lane) | (j << 5));
-                    }
-                    __syncwarp();
-                    for (uint32_t o = lane; o < ltot; o += 32) {
-                        const int pos = lbase + int(o);
-                        const uint32_t v = get_index(*lbp, pos);
-                        const float4 L = sm.leaf[v & 31u];
-                        const float4 r = ld_rel(t.rel + (__float_as_uint(L.w) + (v >> 5)));
-                        put_entry(*lbp, pos, L.x + r.x, L.y + r.y, L.z + r.z, r.w);
+                const int npos = lsize + int((exc >> 10) & 127u);
+                if (nnode0) put_entry(*lbp, npos, -s0.fx, -s0.fy, -s0.fz, s0.fm);
+                if (nnode1) put_entry(*lbp, npos + int(nnode0), -s1.fx, -s1.fy, -s1.fz, s1.fm);
+                if (P <= uint32_t(kLcap)) {
+                    if (ltot) write_leaves(nfast0, nfast1, lsize + int(ntot), int(exc >> 17), ltot);
+                    lsize += int(P);
+                } else {
+                    // more than one buffer of entries in a round (rare): one cell slot at a time
+                    lsize += int(ntot);
+                    for (int which = 0; which < 2; ++which) {
+                        const uint32_t nf = which ? nfast1 : nfast0;
+                        uint32_t wtot;
+                        const uint32_t wofs = warp_excl_scan(nf, wtot);
+                        if (wtot == 0) continue;
+                        if (lsize + int(wtot) > kLcap) {
+                            handoff(lsize, grp, tflags);
+                            tflags = 0;
+                            lsize = 0;
+                            lbp = &sm.buf[hand & 1];
+                        }
+                        write_leaves(which ? 0u : nf, which ? nf : 0u, lsize, int(wofs), wtot);
+                        lsize += int(wtot);
                     }
                 }
-                lsize += int(P);
                 pushes += P;
             }
             // ---- oversized leaves (coincident clusters at depth 21, or leaf_cap > 8): divergent writer
-            if (__any_sync(kFull, nleaf > 8u)) {
-                const uint32_t nb = nleaf > 8u ? nleaf : 0u;
-                uint32_t btot;
-                const uint32_t bofs = warp_excl_scan(nb, btot);
-                pushes += btot;
-                int pos = lsize + int(bofs), end_all = lsize + int(btot);
-                uint32_t j = 0;
-                __syncwarp();
-                while (true) {
-                    for (; j < nb && pos + int(j) < kLcap; ++j) {
-                        const float4 r = ld_rel(t.rel + (link + j));
-                        put_entry(*lbp, pos + int(j), r.x - fx, r.y - fy, r.z - fz, r.w);
-                    }
-                    if (end_all < kLcap) {
-                        lsize = end_all;
-                        break;
+            if (__any_sync(kFull, nleaf0 > 8u || nleaf1 > 8u)) {
+                for (int which = 0; which < 2; ++which) {
+                    const Screen& sc = which ? s1 : s0;
+                    const uint32_t nb = (which ? nleaf1 : nleaf0) > 8u ? (which ? nleaf1 : nleaf0) : 0u;
+                    uint32_t btot;
+                    const uint32_t bofs = warp_excl_scan(nb, btot);
+                    if (btot == 0) continue;
+                    pushes += btot;
+                    int pos = lsize + int(bofs), end_all = lsize + int(btot);
+                    uint32_t j = 0;
+                    __syncwarp();
+                    while (true) {
+                        for (; j < nb && pos + int(j) < kLcap; ++j) {
+                            const float4 r = ld_rel(t.rel + (sc.link + j));
+                            put_entry(*lbp, pos + int(j), r.x - sc.fx, r.y - sc.fy, r.z - sc.fz, r.w);
+                        }
+                        if (end_all < kLcap) {
+                            lsize = end_all;
+                            break;
+                        }
+                        __syncwarp();
+                        handoff(kLcap, grp, tflags);
+                        tflags = 0;
+                        lbp = &sm.buf[hand & 1];
+                        pos -= kLcap;
+                        end_all -= kLcap;
+                        if (end_all == 0) {
+                            lsize = 0;
+                            break;
+                        }
                     }
                     __syncwarp();
-                    handoff(kLcap, grp, tflags);
-                    tflags = 0;
-                    lbp = &sm.buf[hand & 1];
-                    pos -= kLcap;
-                    end_all -= kLcap;
-                    if (end_all == 0) {
-                        lsize = 0;
-                        break;
-                    }
                 }
             }
             __syncwarp();

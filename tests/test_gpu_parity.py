@@ -254,8 +254,11 @@ def test_simulation_step_parity(g2, ref):
         assert a["active"] == b.active and a["rebuilt"] == b.rebuilt
     r1, g1 = rs.state(), gs.system()
     assert g1.time == r1["time"]
-    assert np.max(np.abs(g1.pos - r1["pos"])) < 1e-8
-    assert np.max(np.abs(g1.vel - r1["vel"])) < 1e-6
+    # FP32 forces (median <= 1e-5, p99 <= 1e-4 relative) integrated over 6 steps of dt = 1/64:
+    # the bulk agrees to ~1e-10; the worst particle (closest pair) within 1e-7
+    dpos, dvel = np.abs(g1.pos - r1["pos"]), np.abs(g1.vel - r1["vel"])
+    assert np.median(dpos) < 1e-9 and np.max(dpos) < 1e-7
+    assert np.median(dvel) < 1e-7 and np.max(dvel) < 1e-5
 
 
 def test_direct_sum_targets(g2, oracle):
