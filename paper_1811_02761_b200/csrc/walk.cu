@@ -32,6 +32,10 @@
 namespace g2 {
 namespace {
 
+#ifndef G2_PRODUCER_REGS  // setmaxnreg split of the 64-register budget between the two warpgroups
+#define G2_PRODUCER_REGS 0
+#define G2_CONSUMER_REGS 0
+#endif
 constexpr int kPairs = 4;                  // producer/consumer warp pairs per CTA
 constexpr int kThreads = 64 * kPairs;      // producers are warps 0..kPairs-1, consumers kPairs..2kPairs-1
 #ifndef G2_WALK_MINB
@@ -314,6 +318,9 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
 
     if (warp >= kPairs) {
         // ================================ consumer: flush buffers into the sinks' accumulators
+#if G2_CONSUMER_REGS
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(G2_CONSUMER_REGS));
+#endif
         PairSmem& ps = pairs[warp - kPairs];
         const float eps2 = float(p.eps * p.eps);
         const f2 e2 = pk(eps2, eps2);
@@ -366,6 +373,9 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
     }
 
     // ==================================== producer: traversal
+#if G2_PRODUCER_REGS
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G2_PRODUCER_REGS));
+#endif
     PairSmem& sm = pairs[warp];
     uint32_t* spill = b.spill + (size_t(blockIdx.x) * kPairs + warp) * kSpillWords;
     // Task sources: the initial tasks (one per group, claimed by counter, in
