@@ -219,10 +219,11 @@ void Engine::split_and_nodes(bool with_nodes) {
         G2_CUDA(cudaMemsetAsync(level_start_.p, 0, (kMaxDepth + 3) * sizeof(uint32_t), s_));
         G2_CUDA(cudaMemsetAsync(tile_counters_.p, 0, (kMaxDepth + 1) * sizeof(uint32_t), s_));
         G2_CUDA(cudaMemsetAsync(split_status_.p, 0, (cell_cap_ / 32 + 64) * sizeof(uint64_t), s_));
+        split_tiles_.reserve(split_tile_words(n));
         SplitArgs a{keys_a_.p,  first_child_.p, child_count_.p, first_.p,
                     count_.p,   depth_.p,       level_start_.p, split_status_.p,
                     tile_counters_.p, uint32_t(cell_cap_), uint32_t(std::min<size_t>(c_.leaf_cap, 0xffffffffu)),
-                    flags_.p};
+                    flags_.p, split_tiles_.p};
         dbg_mark(3, s_);
         launch_split(a, uint32_t(n), s_);
         dbg_mark(4, s_);

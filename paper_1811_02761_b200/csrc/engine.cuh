@@ -112,6 +112,7 @@ private:
     DBuf<uint32_t> leaf_of_;
     DBuf<uint32_t> level_start_, tile_counters_;
     DBuf<uint64_t> split_status_;
+    DBuf<uint32_t> split_tiles_;
     DBuf<double> bbox_part_;
     DBuf<Cube> cube_;
     DBuf<uint32_t> sinks_, sinks_alt_, n_sinks_, n_groups_;

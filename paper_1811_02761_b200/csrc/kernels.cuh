@@ -48,7 +48,9 @@ struct SplitArgs {
     uint32_t cell_cap;
     uint32_t leaf_cap;
     DevFlags* flags;
+    uint32_t* tiles;          // split_tile_words(n) scratch for the non-recursive split (nullable)
 };
+size_t split_tile_words(size_t n);
 void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s);
 
 // calc_node over all levels, deepest first (octree.cpp:145-162)

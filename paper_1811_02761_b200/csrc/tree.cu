@@ -229,6 +229,265 @@ __global__ void __launch_bounds__(kBlock) split_level_kernel(SplitArgs a, int d)
     }
 }
 
+// ---- non-recursive split (leaf_cap <= kSplitMaxCap) --------------------------------
+// With L_i = number of leading Morton digits shared by sorted keys i-1 and i
+// (L_0 = L_n = -1), a depth-d cell exists at position i iff a depth-d digit run
+// starts there (i = 0 or L_i < d) and the enclosing depth-(d-1) run holds more
+// than leaf_cap particles (its parent is split; all ancestors are larger).  Per
+// position the existing depths form one interval [lo_i, hi_i], decided from L
+// in a window of +-leaf_cap around i.  BFS order (depth, first) then follows
+// from per-depth ranks, so the whole level-by-level recursion of
+// octree.cpp:74-102 becomes four launches: count, scan, write, child counts.
+constexpr int kSplitThreads = 256;
+constexpr int kSplitItems = 4;                              // particles per thread
+constexpr int kSplitTile = kSplitThreads * kSplitItems;     // particles per block
+constexpr int kSplitChunks = kSplitTile / 32;                // warp-sized chunks per tile, (item, warp) order
+constexpr uint32_t kSplitMaxCap = 32;
+
+__device__ __forceinline__ int lcp_digits(uint64_t a, uint64_t b) {
+    const uint64_t x = a ^ b;
+    if (!x) return kMortonBits;
+    return (62 - (63 - __clzll(static_cast<long long>(x)))) / 3;  // keys use bits 0..62
+}
+
+struct SplitWindow {
+    uint64_t key[kSplitTile + 2 * kSplitMaxCap + 2];
+    int8_t L[kSplitTile + 2 * kSplitMaxCap + 1];
+};
+
+// Loads the tile's key window and L values; then (lo, hi) of particle base + t (t = tile offset):
+// lo > hi means no cell starts there.
+__device__ __forceinline__ void split_window(const uint64_t* __restrict__ keys, uint32_t n, uint32_t lc,
+                                             uint32_t base, SplitWindow& w) {
+    const int64_t kb = int64_t(base) - int64_t(lc) - 1;  // key window [kb, base + T + lc]
+    const int nk = kSplitTile + 2 * int(lc) + 2;
+    for (int t = threadIdx.x; t < nk; t += kSplitThreads) {
+        const int64_t j = kb + t;
+        w.key[t] = (j >= 0 && j < int64_t(n)) ? keys[j] : 0ull;
+    }
+    __syncthreads();
+    const int64_t lb = int64_t(base) - int64_t(lc);  // L window [lb, base + T + lc]
+    for (int t = threadIdx.x; t < nk - 1; t += kSplitThreads) {
+        const int64_t j = lb + t;
+        w.L[t] = (j <= 0 || j >= int64_t(n)) ? int8_t(-1) : int8_t(lcp_digits(w.key[t], w.key[t + 1]));
+    }
+    __syncthreads();
+}
+
+// The window holds L = -1 outside [1, n), so runs end at the array ends without extra tests.
+__device__ __forceinline__ void split_range(uint32_t n, uint32_t lc, uint32_t base, int t, const SplitWindow& w,
+                                            int& lo, int& hi) {
+    const uint32_t i = base + uint32_t(t);
+    lo = kMaxDepth + 1, hi = kMaxDepth;
+    if (i >= n) return;
+    const int8_t* L = w.L + t + int(lc);  // L[0] = L_i
+    int M = 127;                          // min L over (i, i + lc]
+    for (int q = 1; q <= int(lc); ++q) M = min(M, int(L[q]));
+    if (i == 0) {
+        lo = 0, hi = min(kMaxDepth, M + 1);
+        return;
+    }
+    const int li = L[0];
+    if (li >= kMortonBits) return;  // identical keys: no cell starts here
+    // size of the depth-li run through i = back + fwd: back = i - (last j <= i with L_j < li),
+    // fwd = (first j > i with L_j < li) - i; only whether it exceeds lc matters
+    int back = int(lc) + 1, fwd = int(lc) + 1;
+    for (int q = 0; q <= int(lc); ++q)
+        if (L[-q] < li) {
+            back = q;
+            break;
+        }
+    if (back <= int(lc))
+        for (int q = 1; q <= int(lc) - back; ++q)
+            if (L[q] < li) {
+                fwd = q;
+                break;
+            }
+    lo = li + 1;
+    hi = back + fwd > int(lc) ? min(kMaxDepth, max(li + 1, M + 1)) : li;
+}
+
+// per-depth counts of the tile's (item, warp) chunks -> chunk-exclusive prefixes in wcnt, tile totals returned
+__device__ __forceinline__ void split_chunk_counts(const int* lo, const int* hi, uint32_t (*wcnt)[kSplitChunks]) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < kSplitItems; ++k) {
+        // only the depths some lane of this chunk has (warp-uniform bounds)
+        const int dmin = __reduce_min_sync(0xffffffffu, lo[k]);
+        const int dmax = __reduce_max_sync(0xffffffffu, hi[k]);
+        if (lane <= kMaxDepth && (lane < dmin || lane > dmax)) wcnt[lane][k * (kSplitThreads / 32) + wid] = 0;
+        for (int d = dmin; d <= dmax; ++d) {
+            const unsigned m = __ballot_sync(0xffffffffu, lo[k] <= d && d <= hi[k]);
+            if (lane == 0) wcnt[d][k * (kSplitThreads / 32) + wid] = __popc(m);
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSplitThreads) split_count_kernel(const uint64_t* __restrict__ keys, uint32_t n,
+                                                                    uint32_t lc, uint32_t* __restrict__ tile_counts,
+                                                                    uint32_t ntiles) {
+    __shared__ SplitWindow w;
+    __shared__ uint32_t wcnt[kMaxDepth + 1][kSplitChunks];
+    const uint32_t base = blockIdx.x * kSplitTile;
+    split_window(keys, n, lc, base, w);
+    int lo[kSplitItems], hi[kSplitItems];
+#pragma unroll
+    for (int k = 0; k < kSplitItems; ++k) split_range(n, lc, base, k * kSplitThreads + threadIdx.x, w, lo[k], hi[k]);
+    split_chunk_counts(lo, hi, wcnt);
+    if (threadIdx.x <= kMaxDepth) {
+        uint32_t c = 0;
+        for (int q = 0; q < kSplitChunks; ++q) c += wcnt[threadIdx.x][q];
+        tile_counts[size_t(threadIdx.x) * ntiles + blockIdx.x] = c;
+    }
+}
+
+// one block per depth: exclusive scan over the tiles in place, level size -> totals[d]
+__global__ void __launch_bounds__(1024) split_scan_kernel(uint32_t* __restrict__ tile_counts, uint32_t ntiles,
+                                                          uint32_t* __restrict__ totals) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t carry;
+    uint32_t* row = tile_counts + size_t(blockIdx.x) * ntiles;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (uint32_t b0 = 0; b0 < ntiles; b0 += 1024) {
+        const uint32_t k = b0 + threadIdx.x;
+        const uint32_t x = k < ntiles ? row[k] : 0u;
+        uint32_t inc = x;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[wid] = inc;
+        __syncthreads();
+        if (wid == 0) {
+            const uint32_t v = wsum[lane];
+            uint32_t vi = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, vi, o);
+                if (lane >= o) vi += y;
+            }
+            wsum[lane] = vi - v;
+        }
+        __syncthreads();
+        const uint32_t c0 = carry;
+        if (k < ntiles) row[k] = c0 + wsum[wid] + inc - x;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = c0 + wsum[wid] + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
+// cells in BFS order: first, depth, first_child (count and child_count follow in split_cells_kernel)
+__global__ void __launch_bounds__(kSplitThreads) split_write_kernel(SplitArgs a, uint32_t n,
+                                                                    const uint32_t* __restrict__ tile_offs,
+                                                                    uint32_t ntiles, const uint32_t* __restrict__ totals) {
+    __shared__ SplitWindow w;
+    __shared__ uint32_t wcnt[kMaxDepth + 1][kSplitChunks];
+    __shared__ uint32_t lstart[kMaxDepth + 2];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int d = 0; d <= kMaxDepth; ++d) lstart[d] = acc, acc += totals[d];
+        lstart[kMaxDepth + 1] = acc;
+    }
+    const uint32_t base = blockIdx.x * kSplitTile;
+    split_window(a.keys, n, a.leaf_cap, base, w);
+    int lo[kSplitItems], hi[kSplitItems];
+#pragma unroll
+    for (int k = 0; k < kSplitItems; ++k)
+        split_range(n, a.leaf_cap, base, k * kSplitThreads + threadIdx.x, w, lo[k], hi[k]);
+    split_chunk_counts(lo, hi, wcnt);
+    if (threadIdx.x <= kMaxDepth) {  // exclusive prefix over the tile's chunks, plus the tile offset
+        uint32_t acc = lstart[threadIdx.x] + tile_offs[size_t(threadIdx.x) * ntiles + blockIdx.x];
+        for (int q = 0; q < kSplitChunks; ++q) {
+            const uint32_t c = wcnt[threadIdx.x][q];
+            wcnt[threadIdx.x][q] = acc;
+            acc += c;
+        }
+    }
+    __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x <= kMaxDepth + 1) a.level_start[threadIdx.x] = lstart[threadIdx.x];
+    if (blockIdx.x == 0 && threadIdx.x == kMaxDepth + 2) a.level_start[kMaxDepth + 2] = lstart[kMaxDepth + 1];
+    const unsigned lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int k = 0; k < kSplitItems; ++k) {
+        const uint32_t i = base + k * kSplitThreads + threadIdx.x;
+        const int chunk = k * (kSplitThreads / 32) + wid;
+        uint32_t child_idx = 0;
+        const int dmin = __reduce_min_sync(0xffffffffu, lo[k]);
+        const int dmax = __reduce_max_sync(0xffffffffu, hi[k]);
+        for (int d = dmax; d >= dmin; --d) {  // deepest first: first_child is the previous index
+            const bool has = lo[k] <= d && d <= hi[k];
+            const unsigned m = __ballot_sync(0xffffffffu, has);
+            if (!has) continue;
+            const uint32_t idx = wcnt[d][chunk] + __popc(m & lt);
+            if (idx < a.cell_cap) {
+                a.first[idx] = i;
+                a.depth[idx] = uint8_t(d);
+                a.first_child[idx] = d < hi[k] ? child_idx : 0u;
+            } else {
+                a.flags->cell_overflow = 1;
+            }
+            child_idx = idx;
+        }
+    }
+}
+
+// first j > i whose depth-d prefix differs from key i's (upper_bound by galloping from `from`)
+__device__ __forceinline__ uint32_t run_end(const uint64_t* __restrict__ keys, uint32_t n, uint32_t from, uint64_t pre,
+                                            int sh) {
+    uint32_t ok = from - 1, step = 1, j = from;  // keys[ok] has the prefix
+    while (j < n && (keys[j] >> sh) == pre) {
+        ok = j;
+        j = ok + step;
+        step <<= 1;
+    }
+    uint32_t hi = min(j, n);  // first index known (or assumed at n) not to match
+    while (ok + 1 < hi) {
+        const uint32_t mid = ok + (hi - ok) / 2;
+        if ((keys[mid] >> sh) == pre)
+            ok = mid;
+        else
+            hi = mid;
+    }
+    return ok + 1;
+}
+
+// per cell: count = end of its digit run (8 keys probed at once, then galloping), and for split
+// cells the number of consecutive next-level cells starting inside it
+__global__ void __launch_bounds__(kBlock) split_cells_kernel(SplitArgs a, uint32_t n) {
+    const uint32_t total = min(a.level_start[kMaxDepth + 1], a.cell_cap);
+    for (uint32_t c = blockIdx.x * kBlock + threadIdx.x; c < total; c += gridDim.x * kBlock) {
+        const uint32_t i = a.first[c];
+        const int d = a.depth[c];
+        const int sh = 3 * (kMaxDepth - d);
+        const uint64_t pre = a.keys[i] >> sh;
+        uint64_t kk[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) kk[q] = i + 1 + q < n ? a.keys[i + 1 + q] : ~0ull;
+        uint32_t e = 0;
+#pragma unroll
+        for (int q = 7; q >= 0; --q)
+            if (i + 1 + q >= n || (kk[q] >> sh) != pre) e = i + 1 + q;
+        if (!e) e = run_end(a.keys, n, i + 9, pre, sh);
+        e = min(e, n);
+        a.count[c] = e - i;
+        const uint32_t fc = a.first_child[c];
+        uint32_t cc = 0;
+        if (fc) {
+            const uint32_t lend = min(a.level_start[d + 2], a.cell_cap);
+            cc = 1;
+            while (fc + cc < lend && a.first[fc + cc] < e) ++cc;
+        }
+        a.child_count[c] = cc;
+    }
+}
+
 __global__ void split_init_kernel(SplitArgs a, uint32_t n) {
     if (threadIdx.x == 0) {
         a.first_child[0] = 0;
@@ -364,7 +623,20 @@ void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const
     G2_CUDA(cudaGetLastError());
 }
 
+size_t split_tile_words(size_t n) { return (kMaxDepth + 1) * (ceil_div(n, kSplitTile) + 1) + 32; }
+
 void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
+    if (a.leaf_cap <= kSplitMaxCap && a.tiles) {
+        const uint32_t ntiles = ceil_div(n, kSplitTile);
+        uint32_t* totals = a.tiles + size_t(kMaxDepth + 1) * ntiles;
+        G2_COUNT(1), split_count_kernel<<<ntiles, kSplitThreads, 0, s>>>(a.keys, n, a.leaf_cap, a.tiles, ntiles);
+        G2_COUNT(1), split_scan_kernel<<<kMaxDepth + 1, 1024, 0, s>>>(a.tiles, ntiles, totals);
+        G2_COUNT(1), split_write_kernel<<<ntiles, kSplitThreads, 0, s>>>(a, n, a.tiles, ntiles, totals);
+        G2_COUNT(1), split_cells_kernel<<<grid_for(a.cell_cap), kBlock, 0, s>>>(a, n);
+        G2_CUDA(cudaGetLastError());
+        return;
+    }
+    // level-by-level path (leaf_cap > kSplitMaxCap)
     G2_COUNT(1), split_init_kernel<<<1, 32, 0, s>>>(a, n);
     // levels are sized on the device; a fixed persistent grid pulls tiles dynamically
     static const bool dbg = std::getenv("G2_SPLIT_DEBUG") != nullptr;  // development: per-level device times
