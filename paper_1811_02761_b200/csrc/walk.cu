@@ -27,6 +27,8 @@
 //     (group, cells) batches, which split the heavy-tailed "whole-system"
 //     groups across warps.  Partial accelerations are combined
 //     with FP32 atomics.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace g2 {
@@ -842,7 +844,9 @@ int walk_blocks_per_sm() {
 
 template <bool kPot, bool kEps0, bool kCheck>
 void walk_launch_t(const TreeView& t, const WalkParams& p, const WalkBuffers& b, DevFlags* flags, cudaStream_t s) {
-    const int per_sm = walk_blocks_per_sm<kPot, kEps0, kCheck>();
+    int per_sm = walk_blocks_per_sm<kPot, kEps0, kCheck>();
+    static const char* ov = std::getenv("G2_WALK_CTAS_PER_SM");  // development: occupancy experiments
+    if (ov) per_sm = std::max(1, std::min(per_sm, std::atoi(ov)));
     const unsigned grid = unsigned(per_sm * kNumSMs);
     G2_COUNT(1), walk_kernel<kPot, kEps0, kCheck><<<grid, kThreads, kWalkSmem, s>>>(t, p, b, flags);
 }
