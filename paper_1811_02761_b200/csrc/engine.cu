@@ -242,6 +242,7 @@ void Engine::split_and_nodes(bool with_nodes) {
         const size_t total = ls[kMaxDepth + 1];
         if (total <= cell_cap_) {
             ncells_ = total;
+            std::copy(ls, ls + kMaxDepth + 3, ls_host_);
             max_level_width_ = 0;
             for (int d = 0; d <= kMaxDepth; ++d) max_level_width_ = std::max(max_level_width_, ls[d + 1] - ls[d]);
             break;
@@ -253,7 +254,7 @@ void Engine::split_and_nodes(bool with_nodes) {
 
 void Engine::calc_nodes() {
     launch_calc_node(xyzm_s_.p, first_child_.p, child_count_.p, first_.p, count_.p, depth_.p, level_start_.p,
-                     nodes_.p, nodes32_.p, rel_.p, leaf_of_.p, s_);
+                     ls_host_, nodes_.p, nodes32_.p, rel_.p, leaf_of_.p, s_);
 }
 
 void Engine::refresh(size_t n, const double* mass, const double* pos) {

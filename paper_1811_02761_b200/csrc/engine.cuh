@@ -108,6 +108,7 @@ private:
     DBuf<uint8_t> depth_;
     DBuf<WNode> nodes_;
     DBuf<WNode32> nodes32_;
+    uint32_t ls_host_[kMaxDepth + 3] = {};  // host copy of level_start of the current topology
     DBuf<float4> rel_;
     DBuf<uint32_t> leaf_of_;
     DBuf<uint32_t> level_start_, tile_counters_;

@@ -53,11 +53,13 @@ struct SplitArgs {
 size_t split_tile_words(size_t n);
 void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s);
 
-// calc_node over all levels, deepest first (octree.cpp:145-162)
-// also writes the compact walk records and the leaf-relative particle offsets
+// calc_node over the whole tree (octree.cpp:145-162): all leaves in one launch, then the internal
+// levels deepest first; also writes the compact walk records and the leaf-relative particle offsets.
+// level_start_host: the host copy of level_start (launch sizes).
 void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const uint32_t* child_count,
                       const uint32_t* first, const uint32_t* count, const uint8_t* depth, const uint32_t* level_start,
-                      WNode* nodes, WNode32* nodes32, float4* rel, uint32_t* leaf_of, cudaStream_t s);
+                      const uint32_t* level_start_host, WNode* nodes, WNode32* nodes32, float4* rel,
+                      uint32_t* leaf_of, cudaStream_t s);
 // leaf-relative offsets of the CURRENT positions against the existing nodes (GravityEngine::evaluate
 // walks fresh positions with the node attributes of the last build/refresh, engine.cpp:31-81)
 void launch_leaf_rel(const double4* xyzm, const uint32_t* child_count, const uint32_t* first, const uint32_t* count,

@@ -500,63 +500,88 @@ __global__ void split_init_kernel(SplitArgs a, uint32_t n) {
     }
 }
 
-// ---- calc_node (octree.cpp:108-162), one launch per depth, deepest first ------
-__global__ void __launch_bounds__(kBlock) calc_node_level_kernel(
-    const double4* __restrict__ xyzm, const uint32_t* __restrict__ first_child,
-    const uint32_t* __restrict__ child_count, const uint32_t* __restrict__ first, const uint32_t* __restrict__ count,
-    const uint8_t* __restrict__ depth, const uint32_t* __restrict__ level_start, WNode* __restrict__ nodes,
-    WNode32* __restrict__ nodes32, float4* __restrict__ rel, uint32_t* __restrict__ leaf_of, int d) {
+// ---- calc_node (octree.cpp:108-162) --------------------------------------------
+// All leaves in one launch (the bulk: particle sums and the walk's leaf-relative
+// offsets), then the internal cells level by level, deepest first, each from its
+// children in order -- the reference's operation order, so the FP64 node
+// attributes are bit-identical.
+__device__ __forceinline__ void store_node(WNode* __restrict__ nodes, WNode32* __restrict__ nodes32, uint32_t c,
+                                           const WNode& nd) {
+    nodes[c] = nd;
+    const float fm = float(nd.mass), fb = float(nd.extent);
+    nodes32[c] = WNode32{float(nd.cx), float(nd.cy), float(nd.cz), fm, fb, fm * fb * fb, nd.link, nd.info};
+}
+
+__global__ void __launch_bounds__(kBlock) calc_leaf_kernel(const double4* __restrict__ xyzm,
+                                                           const uint32_t* __restrict__ child_count,
+                                                           const uint32_t* __restrict__ first,
+                                                           const uint32_t* __restrict__ count,
+                                                           const uint32_t* __restrict__ level_start,
+                                                           WNode* __restrict__ nodes, WNode32* __restrict__ nodes32,
+                                                           float4* __restrict__ rel, uint32_t* __restrict__ leaf_of) {
+    const uint32_t total = level_start[kMaxDepth + 1];
+    for (uint32_t c = blockIdx.x * kBlock + threadIdx.x; c < total; c += gridDim.x * kBlock) {
+        if (child_count[c]) continue;
+        WNode nd;
+        double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
+        const uint32_t f = first[c], k1 = f + count[c];
+        for (uint32_t k = f; k < k1; ++k) {
+            const double4 p = xyzm[k];
+            m = dadd(m, p.w);
+            wx = dadd(wx, dmul(p.w, p.x));
+            wy = dadd(wy, dmul(p.w, p.y));
+            wz = dadd(wz, dmul(p.w, p.z));
+        }
+        const double inv = ddiv(1.0, m);
+        nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+        const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
+        double e2 = 0.0;
+        for (uint32_t k = f; k < k1; ++k) {
+            const double4 p = xyzm[k];
+            e2 = smax(e2, norm2(dsub(p.x, nd.cx), dsub(p.y, nd.cy), dsub(p.z, nd.cz)));
+            rel[k] = make_float4(float(dsub(p.x, c32x)), float(dsub(p.y, c32y)), float(dsub(p.z, c32z)), float(p.w));
+            leaf_of[k] = c;
+        }
+        nd.extent = dsqrt(e2);
+        nd.link = f;
+        nd.info = (k1 - f) | kLeafBit;
+        nd.mass = m;
+        store_node(nodes, nodes32, c, nd);
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) calc_internal_kernel(const uint32_t* __restrict__ first_child,
+                                                               const uint32_t* __restrict__ child_count,
+                                                               const uint8_t* __restrict__ depth,
+                                                               const uint32_t* __restrict__ level_start,
+                                                               WNode* __restrict__ nodes,
+                                                               WNode32* __restrict__ nodes32, int d) {
     const uint32_t b = level_start[d], e = level_start[d + 1];
     for (uint32_t c = b + blockIdx.x * kBlock + threadIdx.x; c < e; c += gridDim.x * kBlock) {
         const uint32_t cc = child_count[c];
+        if (!cc) continue;
         WNode nd;
         double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
-        if (cc == 0) {
-            const uint32_t f = first[c], k1 = f + count[c];
-            for (uint32_t k = f; k < k1; ++k) {
-                const double4 p = xyzm[k];
-                m = dadd(m, p.w);
-                wx = dadd(wx, dmul(p.w, p.x));
-                wy = dadd(wy, dmul(p.w, p.y));
-                wz = dadd(wz, dmul(p.w, p.z));
-            }
-            const double inv = ddiv(1.0, m);
-            nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
-            const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
-            double e2 = 0.0;
-            for (uint32_t k = f; k < k1; ++k) {
-                const double4 p = xyzm[k];
-                e2 = smax(e2, norm2(dsub(p.x, nd.cx), dsub(p.y, nd.cy), dsub(p.z, nd.cz)));
-                rel[k] = make_float4(float(dsub(p.x, c32x)), float(dsub(p.y, c32y)), float(dsub(p.z, c32z)), float(p.w));
-                leaf_of[k] = c;
-            }
-            nd.extent = dsqrt(e2);
-            nd.link = f;
-            nd.info = (k1 - f) | kLeafBit;
-        } else {
-            const uint32_t f = first_child[c];
-            for (uint32_t ch = f; ch < f + cc; ++ch) {
-                const WNode q = nodes[ch];
-                m = dadd(m, q.mass);
-                wx = dadd(wx, dmul(q.mass, q.cx));
-                wy = dadd(wy, dmul(q.mass, q.cy));
-                wz = dadd(wz, dmul(q.mass, q.cz));
-            }
-            const double inv = ddiv(1.0, m);
-            nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
-            double ext = 0.0;
-            for (uint32_t ch = f; ch < f + cc; ++ch) {
-                const WNode q = nodes[ch];
-                ext = smax(ext, dadd(dsqrt(norm2(dsub(q.cx, nd.cx), dsub(q.cy, nd.cy), dsub(q.cz, nd.cz))), q.extent));
-            }
-            nd.extent = ext;
-            nd.link = f;
-            nd.info = cc | (uint32_t(depth[c]) << 8);  // depth feeds the frontier-cap check
+        const uint32_t f = first_child[c];
+        for (uint32_t ch = f; ch < f + cc; ++ch) {
+            const WNode q = nodes[ch];
+            m = dadd(m, q.mass);
+            wx = dadd(wx, dmul(q.mass, q.cx));
+            wy = dadd(wy, dmul(q.mass, q.cy));
+            wz = dadd(wz, dmul(q.mass, q.cz));
         }
+        const double inv = ddiv(1.0, m);
+        nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+        double ext = 0.0;
+        for (uint32_t ch = f; ch < f + cc; ++ch) {
+            const WNode q = nodes[ch];
+            ext = smax(ext, dadd(dsqrt(norm2(dsub(q.cx, nd.cx), dsub(q.cy, nd.cy), dsub(q.cz, nd.cz))), q.extent));
+        }
+        nd.extent = ext;
+        nd.link = f;
+        nd.info = cc | (uint32_t(depth[c]) << 8);  // depth feeds the frontier-cap check
         nd.mass = m;
-        nodes[c] = nd;
-        const float fm = float(m), fb = float(nd.extent);
-        nodes32[c] = WNode32{float(nd.cx), float(nd.cy), float(nd.cz), fm, fb, fm * fb * fb, nd.link, nd.info};
+        store_node(nodes, nodes32, c, nd);
     }
 }
 
@@ -663,10 +688,19 @@ void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
 
 void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const uint32_t* child_count,
                       const uint32_t* first, const uint32_t* count, const uint8_t* depth, const uint32_t* level_start,
-                      WNode* nodes, WNode32* nodes32, float4* rel, uint32_t* leaf_of, cudaStream_t s) {
-    for (int d = kMaxDepth; d >= 0; --d)
-        G2_COUNT(1), calc_node_level_kernel<<<kNumSMs * 8, kBlock, 0, s>>>(xyzm, first_child, child_count, first, count, depth,
-                                                              level_start, nodes, nodes32, rel, leaf_of, d);
+                      const uint32_t* level_start_host, WNode* nodes, WNode32* nodes32, float4* rel,
+                      uint32_t* leaf_of, cudaStream_t s) {
+    const size_t total = level_start_host[kMaxDepth + 1];
+    G2_COUNT(1), calc_leaf_kernel<<<grid_for(total), kBlock, 0, s>>>(xyzm, child_count, first, count, level_start,
+                                                                      nodes, nodes32, rel, leaf_of);
+    int deepest = 0;  // the deepest non-empty level holds leaves only
+    for (int d = 0; d <= kMaxDepth; ++d)
+        if (level_start_host[d + 1] > level_start_host[d]) deepest = d;
+    for (int d = deepest - 1; d >= 0; --d) {
+        const size_t w = level_start_host[d + 1] - level_start_host[d];
+        G2_COUNT(1), calc_internal_kernel<<<grid_for(w), kBlock, 0, s>>>(first_child, child_count, depth, level_start,
+                                                                          nodes, nodes32, d);
+    }
     G2_CUDA(cudaGetLastError());
 }
 
