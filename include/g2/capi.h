@@ -130,6 +130,12 @@ int g2_sim_get_state(g2_sim* s, double* pos, double* vel, double* acc, double* a
                      double* time);
 /* overwrite positions / velocities (original order) of the device-resident state */
 int g2_sim_set_state(g2_sim* s, const double* pos, const double* vel);
+/* engine().tree() of the simulation (integrator.hpp:62, engine.hpp:47): the tree of the last
+ * rebuild; node attributes are those of the last calc_node (refresh).  Same layout as
+ * g2_engine_get_tree. */
+int g2_sim_tree_size(g2_sim* s, size_t* n, size_t* ncells);
+int g2_sim_get_tree(g2_sim* s, double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* rank, uint32_t* cells4,
+                    uint8_t* depth, double* nodes5);
 /* extension: rebuild the tree every step (the all-active "full step" benchmark) */
 int g2_sim_set_rebuild_every_step(g2_sim* s, int on);
 int g2_sim_tuner_interval(g2_sim* s, size_t* interval);

@@ -253,6 +253,16 @@ int g2_engine_tree_size(const g2_engine* e, size_t* n, size_t* ncells) {
         if (ncells) *ncells = e->e->ncells();
     });
 }
+int g2_sim_tree_size(g2_sim* s, size_t* n, size_t* ncells) {
+    return guarded([&] {
+        if (n) *n = s->s->engine().n();
+        if (ncells) *ncells = s->s->engine().ncells();
+    });
+}
+int g2_sim_get_tree(g2_sim* s, double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* rank, uint32_t* cells4,
+                    uint8_t* depth, double* nodes5) {
+    return guarded([&] { s->s->engine().get_tree(bbox4, keys, perm, rank, cells4, depth, nodes5); });
+}
 int g2_engine_get_tree(g2_engine* e, double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* rank,
                        uint32_t* cells4, uint8_t* depth, double* nodes5) {
     return guarded([&] { e->e->get_tree(bbox4, keys, perm, rank, cells4, depth, nodes5); });

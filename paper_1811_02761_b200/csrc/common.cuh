@@ -35,7 +35,8 @@ struct DevFlags {
     int cell_overflow;    // cell buffer too small: host grows it and rebuilds
     int stack_overflow;   // walk stack spill area exhausted (internal, sized to never trigger)
     int queue_overflow;   // walk task queue exhausted (internal)
-    int pad[2];
+    int tie_run;          // a run of equal keys too long for the in-place tie repair (host re-sorts by id)
+    int pad;
 };
 
 constexpr int kMaxDepth = 21;        // octree.hpp:47

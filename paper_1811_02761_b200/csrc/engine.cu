@@ -167,6 +167,7 @@ void Engine::sort_keys_identity_payload(size_t n) {
     if (ks != keys_a_.p) G2_CUDA(cudaMemcpyAsync(keys_a_.p, ks, n * 8, cudaMemcpyDeviceToDevice, s_));
     G2_CUDA(cudaMemcpyAsync(perm_.p, vs, n * 4, cudaMemcpyDeviceToDevice, s_));
     launch_invert_perm(perm_.p, rank_.p, n, s_);
+    rank_valid_ = true;
 }
 
 void Engine::build(size_t n, const double* mass, const double* pos, bool with_nodes) {
@@ -203,14 +204,46 @@ const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank
     const size_t n = n_;
     dbg_mark(0, s_);
     launch_bbox(xyzm_s_.p, n, bbox_part_.p, cube_.p, flags_.p, s_);
-    launch_keys(xyzm_s_.p, ids, n, cube_.p, keys_a_.p, flags_.p, s_);  // keys by original id
-    dbg_mark(1, s_);
-    sort_keys_identity_payload(n);                                      // perm = original ids in Morton order
+    if (!rank_cur) {
+        // keys in storage order sorted with the storage position as payload (no scatter into id
+        // order, no rank gather); equal-key runs are then put in original-id order in place
+        launch_keys(xyzm_s_.p, nullptr, n, cube_.p, keys_a_.p, flags_.p, s_);
+        dbg_mark(1, s_);
+        const bool alt = radix_sort_pairs<uint64_t>(keys_a_.p, vals_a_.p, keys_b_.p, vals_b_.p, n, 63, true, sort_, s_);
+        if (alt) {
+            std::swap(keys_a_.p, keys_b_.p);
+            std::swap(keys_a_.cap, keys_b_.cap);
+        }
+        uint32_t* src = alt ? vals_b_.p : vals_a_.p;
+        launch_fix_ties(keys_a_.p, src, ids, n, flags_.p, s_);
+        G2_CUDA(cudaMemcpyAsync(src_.p, src, n * 4, cudaMemcpyDeviceToDevice, s_));
+        launch_gather_u32(ids, src_.p, perm_.p, n, s_);  // perm[k] = original id at new position k
+        rank_valid_ = false;
+    } else {
+        launch_keys(xyzm_s_.p, ids, n, cube_.p, keys_a_.p, flags_.p, s_);  // keys by original id
+        dbg_mark(1, s_);
+        sort_keys_identity_payload(n);                                      // perm = original ids in Morton order
+        launch_gather_u32(rank_cur, perm_.p, src_.p, n, s_);               // new k <- old position of perm[k]
+    }
     dbg_mark(2, s_);
-    launch_gather_u32(rank_cur, perm_.p, src_.p, n, s_);               // new k <- old position of perm[k]
     launch_gather_d4(xyzm_s_.p, src_.p, xyzm_alt_.p, n, s_);
     swap_xyzm();
     return src_.p;
+}
+
+void Engine::ensure_rank() {
+    if (rank_valid_) return;
+    launch_invert_perm(perm_.p, rank_.p, n_, s_);
+    rank_valid_ = true;
+}
+
+bool Engine::take_tie_overflow() {
+    DevFlags f;
+    G2_CUDA(cudaMemcpyAsync(&f, flags_.p, sizeof f, cudaMemcpyDeviceToHost, s_));
+    G2_CUDA(cudaStreamSynchronize(s_));
+    if (!f.tie_run) return false;
+    G2_CUDA(cudaMemsetAsync(&flags_.p->tie_run, 0, sizeof(int), s_));
+    return true;
 }
 
 void Engine::split_and_nodes(bool with_nodes) {
@@ -349,6 +382,7 @@ EventsH Engine::evaluate(size_t n, const double* mass, const double* pos, const 
     if (!has_tree_) throw Error(kDataError, "GravityEngine::evaluate: no tree built");
     if (n != n_) throw Error(kDataError, "GravityEngine::evaluate: particle count differs from the tree");
     if (targets && n_targets == 0) return {};
+    ensure_rank();
     const size_t nt = targets ? n_targets : n;
     if (targets)
         for (size_t j = 0; j < nt; ++j)
@@ -429,6 +463,7 @@ void Engine::get_tree(double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* r
                       uint8_t* depth, double* nodes5) {
     if (!has_tree_) throw Error(kDataError, "get_tree: no tree built");
     const size_t n = n_, nc = ncells_;
+    ensure_rank();
     if (bbox4) G2_CUDA(cudaMemcpyAsync(bbox4, cube_.p, 4 * sizeof(double), cudaMemcpyDeviceToHost, s_));
     if (keys) G2_CUDA(cudaMemcpyAsync(keys, keys_a_.p, n * 8, cudaMemcpyDeviceToHost, s_));
     if (perm) G2_CUDA(cudaMemcpyAsync(perm, perm_.p, n * 4, cudaMemcpyDeviceToHost, s_));
@@ -547,7 +582,28 @@ void Simulation::reorder(const uint32_t* src) {
     std::swap(active_.p, active2_.p);
     std::swap(last_.p, last2_.p);
     G2_CUDA(cudaMemcpyAsync(ids_.p, eng_.perm(), n * 4, cudaMemcpyDeviceToDevice, s));
-    G2_CUDA(cudaMemcpyAsync(rank_cur_.p, eng_.rank(), n * 4, cudaMemcpyDeviceToDevice, s));
+    rank_cur_valid_ = false;  // original id -> position: rebuilt on demand (API boundary only)
+}
+
+const uint32_t* Simulation::rank_cur() {
+    if (!rank_cur_valid_) {
+        launch_invert_perm(ids_.p, rank_cur_.p, n_, eng_.stream());
+        rank_cur_valid_ = true;
+    }
+    return rank_cur_.p;
+}
+
+void Simulation::rebuild_order() {
+    const uint32_t* src = eng_.rebuild_sorted(ids_.p, nullptr);
+    reorder(src);
+    eng_.split_and_nodes(false);  // syncs once to size the levels
+    if (eng_.take_tie_overflow()) {
+        // a long run of equal keys: redo the ordering with the (key, original id) sort
+        src = eng_.rebuild_sorted(ids_.p, rank_cur());
+        reorder(src);
+        eng_.split_and_nodes(false);
+    }
+    eng_.mark_tree(true);
 }
 
 double Simulation::elapsed(cudaEvent_t a, cudaEvent_t b) {
@@ -563,10 +619,8 @@ void Simulation::init() {
     if (n <= c.bootstrap_direct_limit) {  // engine.cpp:91-94: state is still in original order
         eng_.direct_sum_orig(eng_.xyzm_s(), n, ax_.p, ay_.p, az_.p);
     } else {
-        const uint32_t* src = eng_.rebuild_sorted(ids_.p, rank_cur_.p);
-        reorder(src);
-        eng_.split_and_nodes(true);
-        eng_.mark_tree(true);
+        rebuild_order();
+        eng_.calc_nodes();
         launch_iota(sinks_.p, n, s);
         const uint32_t n32 = uint32_t(n);
         G2_CUDA(cudaMemcpyAsync(n_active_.p, &n32, 4, cudaMemcpyHostToDevice, s));
@@ -605,10 +659,7 @@ StepResultH Simulation::step() {
             tuner_.on_rebuild();
         else
             tuner_.reset_cycle();
-        const uint32_t* src = eng_.rebuild_sorted(ids_.p, rank_cur_.p);
-        reorder(src);
-        eng_.split_and_nodes(false);  // syncs once to size the levels
-        eng_.mark_tree(true);
+        rebuild_order();
         G2_CUDA(cudaEventRecord(ev_[2], s));
         eng_.calc_nodes();
         G2_CUDA(cudaEventRecord(ev_[3], s));
@@ -676,7 +727,7 @@ void Simulation::get_state(double* pos, double* vel, double* acc, double* acc_ol
     cudaStream_t s = eng_.stream();
     const size_t n = n_;
     io_.reserve(3 * n);
-    const uint32_t* at = rank_cur_.p;  // original id -> current position
+    const uint32_t* at = rank_cur();  // original id -> current position
     if (pos) {
         G2_COUNT(1), xyzm_to_pos3_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), at, io_.p, n);
         G2_CUDA(cudaMemcpyAsync(pos, io_.p, 3 * n * 8, cudaMemcpyDeviceToHost, s));

@@ -54,7 +54,11 @@ public:
     void reserve(size_t n);
     // Morton-sort the particles currently in xyzm_s() (position k holds original
     // id ids[k]); reorders xyzm_s and returns src (new position k <- old src[k]).
+    // new Morton order of the resident state; returns src (new k <- old position).  rank_cur null:
+    // storage-order sort + tie repair (rank_ left stale); else the (key, id) sort via key_by_id.
     const uint32_t* rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur);
+    bool take_tie_overflow();  // syncs; true (and clears) if a tie run was too long for the repair
+    void ensure_rank();        // rank_ = inverse of perm_ if a storage-order rebuild left it stale
     void split_and_nodes(bool with_nodes);
     void calc_nodes();
     // walk sinks (sorted positions) with acc_old_mag (sorted); results into
@@ -97,6 +101,7 @@ private:
     cudaStream_t s_ = nullptr;
     size_t n_ = 0, cap_ = 0, ncells_ = 0, cell_cap_ = 0;
     bool has_tree_ = false;
+    bool rank_valid_ = true;  // rank_ matches perm_ (false after a storage-order rebuild)
     uint32_t max_level_width_ = 0;
 
     DBuf<double> pos3_, mass_, amag_o_;   // host-order staging
@@ -219,6 +224,8 @@ public:
 private:
     StepState state();
     void reorder(const uint32_t* src);
+    void rebuild_order();          // new Morton order + topology of the resident state
+    const uint32_t* rank_cur();    // original id -> current position (computed on demand)
     double elapsed(cudaEvent_t a, cudaEvent_t b);
 
     Engine eng_;
@@ -239,6 +246,7 @@ private:
     DBuf<uint8_t> level_, level2_, active_, active2_;
     DBuf<uint64_t> last_, last2_;
     DBuf<uint32_t> ids_, ids2_, rank_cur_, sinks_, n_active_, compact_ctr_;
+    bool rank_cur_valid_ = true;
     DBuf<uint64_t> compact_status_;
     DBuf<unsigned long long> t_next_;
     DBuf<double> io_, io2_;  // host-transfer staging (original particle order)

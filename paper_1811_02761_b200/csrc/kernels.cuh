@@ -71,6 +71,9 @@ void launch_gather_f64(const double* in, const uint32_t* src, double* out, size_
 void launch_gather_u64(const uint64_t* in, const uint32_t* src, uint64_t* out, size_t n, cudaStream_t s);
 void launch_gather_u8(const uint8_t* in, const uint32_t* src, uint8_t* out, size_t n, cudaStream_t s);
 void launch_gather_u32(const uint32_t* in, const uint32_t* src, uint32_t* out, size_t n, cudaStream_t s);
+// equal-key runs of a storage-order sort: src (storage positions) re-ordered by ids[src] within runs
+void launch_fix_ties(const uint64_t* keys, uint32_t* src, const uint32_t* ids, size_t n, DevFlags* flags,
+                     cudaStream_t s);
 // rank[perm[k]] = k
 void launch_invert_perm(const uint32_t* perm, uint32_t* rank, size_t n, cudaStream_t s);
 // xyzm[k] = (pos[3*id], ..., mass[id]) with id = perm[k] (host-order upload -> sorted)

@@ -603,6 +603,35 @@ __global__ void __launch_bounds__(kBlock) leaf_rel_kernel(const double4* __restr
     }
 }
 
+// ---- equal-key runs after a storage-order sort -----------------------------------------
+// The Simulation sorts (key, storage position) pairs: LSD radix sort is stable, so equal keys
+// come out in storage order, while the reference's (key, original index) pair sort wants them
+// by original id (octree.cpp:60-63).  Runs are rare (coincident quantised positions); each is
+// insertion-sorted by id in place.  Runs longer than kMaxTieRun set flags->tie_run.
+constexpr uint32_t kMaxTieRun = 64;
+__global__ void __launch_bounds__(kBlock) fix_ties_kernel(const uint64_t* __restrict__ keys, uint32_t* __restrict__ src,
+                                                          const uint32_t* __restrict__ ids, size_t n, DevFlags* flags) {
+    for (size_t k = blockIdx.x * size_t(kBlock) + threadIdx.x; k + 1 < n; k += size_t(gridDim.x) * kBlock) {
+        const uint64_t key = keys[k];
+        if (keys[k + 1] != key || (k > 0 && keys[k - 1] == key)) continue;  // not the start of a run
+        uint32_t len = 2;
+        while (k + len < n && keys[k + len] == key && len <= kMaxTieRun) ++len;
+        if (len > kMaxTieRun) {
+            flags->tie_run = 1;
+            continue;
+        }
+        for (uint32_t a = 1; a < len; ++a) {
+            const uint32_t v = src[k + a], iv = ids[v];
+            uint32_t b = a;
+            while (b > 0 && ids[src[k + b - 1]] > iv) {
+                src[k + b] = src[k + b - 1];
+                --b;
+            }
+            src[k + b] = v;
+        }
+    }
+}
+
 // ---- gathers / permutations ----------------------------------------------------------
 template <typename T>
 __global__ void __launch_bounds__(kBlock) gather_kernel(const T* __restrict__ in, const uint32_t* __restrict__ src,
@@ -724,6 +753,10 @@ void launch_gather_u8(const uint8_t* in, const uint32_t* src, uint8_t* out, size
 }
 void launch_gather_u32(const uint32_t* in, const uint32_t* src, uint32_t* out, size_t n, cudaStream_t s) {
     G2_COUNT(1), gather_kernel<uint32_t><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
+}
+void launch_fix_ties(const uint64_t* keys, uint32_t* src, const uint32_t* ids, size_t n, DevFlags* flags,
+                     cudaStream_t s) {
+    G2_COUNT(1), fix_ties_kernel<<<grid_for(n), kBlock, 0, s>>>(keys, src, ids, n, flags);
 }
 void launch_invert_perm(const uint32_t* perm, uint32_t* rank, size_t n, cudaStream_t s) {
     G2_COUNT(1), invert_perm_kernel<<<grid_for(n), kBlock, 0, s>>>(perm, rank, n);

@@ -362,6 +362,17 @@ class Simulation:
     def set_fixed_rebuild_interval(self, interval: int):
         _chk(_lib.g2_sim_set_fixed_rebuild_interval(self._h, C.c_size_t(interval)))
 
+    def tree(self) -> Tree:
+        """engine().tree() (integrator.hpp:62): the octree of the last rebuild."""
+        n, nc = C.c_size_t(), C.c_size_t()
+        _chk(_lib.g2_sim_tree_size(self._h, C.byref(n), C.byref(nc)))
+        n, nc = n.value, nc.value
+        t = Tree(np.empty(4), np.empty(n, np.uint64), np.empty(n, np.uint32), np.empty(n, np.uint32),
+                 np.empty((nc, 4), np.uint32), np.empty(nc, np.uint8), np.empty((nc, 5)))
+        _chk(_lib.g2_sim_get_tree(self._h, _ptr(t.bbox), _ptr(t.keys), _ptr(t.perm), _ptr(t.rank), _ptr(t.cells),
+                                  _ptr(t.depth), _ptr(t.nodes)))
+        return t
+
     def set_rebuild_every_step(self, on: bool = True):
         _chk(_lib.g2_sim_set_rebuild_every_step(self._h, C.c_int(int(on))))
 

@@ -302,3 +302,25 @@ def test_full_size_tree_bitexact_m31_2e23(g2, ref):
     rt = ref.build_tree(m, p)
     for k in ("bbox", "keys", "perm", "rank", "cells", "depth", "nodes"):
         assert np.array_equal(getattr(t, k), getattr(rt, k)), k
+
+
+@pytest.mark.parametrize("cluster", [10, 100])
+def test_simulation_rebuild_ties(g2, oracle, cluster):
+    """Simulation rebuilds sort keys in storage order and repair equal-key runs to the reference's
+    (key, original index) order in place (runs <= 64) or by the id-order sort (longer runs):
+    engine().tree() after a step equals build_tree on the step's positions, bit for bit."""
+    mass, pos, vel = plummer(20000, seed=5)
+    rng = np.random.default_rng(cluster)
+    at = rng.choice(len(mass), cluster, replace=False)
+    pos[at] = pos[at[0]]  # a run of identical positions (identical keys), scattered ids
+    vel[at] = vel[at[0]]
+    sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9),
+                        g2.StepScheme(dt_max=1 / 64))
+    sim.init()
+    sim.set_rebuild_every_step(True)
+    for _ in range(2):
+        sim.step()
+        t, st = sim.tree(), sim.system()
+        ref = oracle.build_tree(mass, st.pos)
+        for k in ("keys", "perm", "rank", "cells", "depth"):
+            assert np.array_equal(getattr(t, k), getattr(ref, k)), k
