@@ -188,6 +188,28 @@ void Engine::build(size_t n, const double* mass, const double* pos, bool with_no
     has_tree_ = true;
 }
 
+// development: descents / displacement of the storage-order keys (how sorted the input is)
+__global__ void disorder_kernel(const uint64_t* __restrict__ k, size_t n, unsigned long long* out) {
+    unsigned long long d = 0, big = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i + 1 < n; i += size_t(gridDim.x) * blockDim.x) {
+        d += k[i] > k[i + 1];
+        big += (k[i] >> 33) > (k[i + 1] >> 33);  // descent in the top 10 levels
+    }
+    atomicAdd(&out[0], d);
+    atomicAdd(&out[1], big);
+}
+static void debug_disorder(const uint64_t* k, size_t n, cudaStream_t s) {
+    static unsigned long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 16);
+    cudaMemsetAsync(buf, 0, 16, s);
+    disorder_kernel<<<148 * 4, 256, 0, s>>>(k, n, buf);
+    unsigned long long h[2];
+    cudaMemcpyAsync(h, buf, 16, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[g2 build] storage-order descents %llu (%.3f%%), top-10-level descents %llu\n", h[0],
+                 100.0 * h[0] / double(n), h[1]);
+}
+
 // development: G2_PHASE_DEBUG=1 prints device sub-phase times of each rebuild
 static bool phase_debug() {
     static const bool on = std::getenv("G2_PHASE_DEBUG") != nullptr;
@@ -208,6 +230,7 @@ const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank
         // keys in storage order sorted with the storage position as payload (no scatter into id
         // order, no rank gather); equal-key runs are then put in original-id order in place
         launch_keys(xyzm_s_.p, nullptr, n, cube_.p, keys_a_.p, flags_.p, s_);
+        if (phase_debug()) debug_disorder(keys_a_.p, n, s_);
         dbg_mark(1, s_);
         const bool alt = radix_sort_pairs<uint64_t>(keys_a_.p, vals_a_.p, keys_b_.p, vals_b_.p, n, 63, true, sort_, s_);
         if (alt) {
