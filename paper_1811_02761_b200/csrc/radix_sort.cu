@@ -6,8 +6,14 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 8;                       // keys per thread
-constexpr int kTile = kThreads * kItems;        // 2048 keys per tile
+#ifndef G2_SORT_ITEMS
+#define G2_SORT_ITEMS 8
+#endif
+#ifndef G2_SORT_MINB
+#define G2_SORT_MINB 4
+#endif
+constexpr int kItems = G2_SORT_ITEMS;           // keys per thread
+constexpr int kTile = kThreads * kItems;        // keys per tile
 constexpr int kWarpItems = 32 * kItems;         // 256 consecutive keys per warp
 
 
@@ -105,7 +111,7 @@ __global__ void __launch_bounds__(kThreads) scan_kernel(uint32_t* __restrict__ c
 }
 
 template <typename K, bool kIdentity>
-__global__ void __launch_bounds__(kThreads, 4) scatter_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
+__global__ void __launch_bounds__(kThreads, G2_SORT_MINB) scatter_kernel(const K* __restrict__ kin, const uint32_t* __restrict__ vin,
                                                            K* __restrict__ kout, uint32_t* __restrict__ vout,
                                                            size_t n, int shift, const uint32_t* __restrict__ offsets,
                                                            uint32_t tiles) {
