@@ -46,7 +46,13 @@ constexpr int kThreads = 64 * kPairs;      // producers are warps 0..kPairs-1, c
 constexpr int kLcap = 336;                 // interaction-list entries per buffer (4 CTAs x 4 pairs fit 228 KB)
 constexpr int kScap = 512;                 // shared stack entries per producer (>= 64 cells x 8 children)
 constexpr uint32_t kSpillWords = 16384;    // global stack entries per producer
-constexpr int kDonateEvery = 64;           // rounds between donations of a long-running task
+#ifndef G2_DONATE_EVERY
+#define G2_DONATE_EVERY 64
+#endif
+#ifndef G2_CHECK_EVERY
+#define G2_CHECK_EVERY 2
+#endif
+constexpr int kDonateEvery = G2_DONATE_EVERY;  // rounds between donations of a long-running task
 constexpr int kQueuedEnough = 4096;        // queued donated batches above which heavy tasks keep their work
 constexpr uint64_t kEmpty = ~0ull;
 constexpr int kRingBits = 20;              // donated-task ring: 2^20 slots, reused
@@ -672,7 +678,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             // ---- donate one batch from the logical bottom (shallowest cells = largest
             // subtrees) every kDonateEvery rounds of a long task, or when warps wait idle
             const int live = ssize + gtop - gbase;
-            if ((++iter & 3) == 0 && live >= 64) {
+            if ((++iter % G2_CHECK_EVERY) == 0 && live >= 64) {
                 int k = 0;
                 uint32_t ds = 0;
                 if (lane == 0) {

@@ -20,4 +20,5 @@ coef, *_ = np.linalg.lstsq(A, d * 1e3, rcond=None)
 print("dur_us ~ %.4f*pushes + %.4f*macs + %.2f" % tuple(coef))
 ini = root == 0
 print("last initial start %.3f; donated starts: min %.3f median %.3f" % (s[ini].max(), s[~ini].min() if (~ini).any() else -1, np.median(s[~ini]) if (~ini).any() else -1))
-print("sum task time / (span*warps) = %.3f" % (d.sum() / (e.max() * 4144)))
+W = int(sys.argv[2]) if len(sys.argv) > 2 else 2368  # producer warps of the walk grid
+print("sum task time / (span*warps) = %.3f" % (d.sum() / (e.max() * W)))

@@ -1,6 +1,7 @@
 """A/B timing of library builds (development only).
 
 usage: python tools/walk_ab.py N LIB1 [LIB2 ...]  -> mean phase times per build, M31 all-active steps
+       G2_AB_PAPER=1 python tools/walk_ab.py ...  -> paper protocol (dt_max 1, rebuild every 2), 32 steps
 Each build runs in its own subprocess (G2_LIB_PATH) on the same input."""
 import json, os, subprocess, sys
 
@@ -19,6 +20,20 @@ from paper_1811_02761_b200.gravitree import sample_model  # noqa: E402
 
 n = int(sys.argv[2])
 m, p, v = sample_model("m31", n, 1)
+if os.environ.get("G2_AB_PAPER"):
+    sim = g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9),
+                        g2.StepScheme(dt_max=1.0), g2.EngineConfig())
+    sim.init()
+    sim.set_fixed_rebuild_interval(2)
+    for _ in range(4):
+        sim.step()
+    rs = [sim.step() for _ in range(32)]
+    tot = [r.timings.total() for r in rs]
+    small = [r.timings.walk_tree for r in rs if r.active < 0.03 * n]
+    print(json.dumps({"paper_ms_per_step": round(1e3 * float(np.mean(tot)), 3),
+                      "walk_ms_per_step": round(1e3 * float(np.mean([r.timings.walk_tree for r in rs])), 3),
+                      "small_walk_ms": round(1e3 * float(np.mean(small)), 3) if small else None}))
+    sys.exit(0)
 sim = g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9),
                     g2.StepScheme(adaptive=False), g2.EngineConfig())
 sim.set_rebuild_every_step(True)
