@@ -54,6 +54,8 @@ __global__ void set_pos_kernel(double4* xyzm, const double* __restrict__ pos3, c
 }
 // the whole per-particle state gathered into the new Morton order in one pass
 struct ReorderArgs {
+    const double4* xin;
+    double4* xout;
     const double* in[7];
     double* out[7];
     const uint8_t *lin, *ain;
@@ -64,6 +66,7 @@ struct ReorderArgs {
 __global__ void __launch_bounds__(kB) reorder_kernel(ReorderArgs r, const uint32_t* __restrict__ src, size_t n) {
     for (size_t i = blockIdx.x * size_t(kB) + threadIdx.x; i < n; i += size_t(gridDim.x) * kB) {
         const uint32_t j = src[i];
+        r.xout[i] = r.xin[j];
 #pragma unroll
         for (int k = 0; k < 7; ++k) r.out[k][i] = r.in[k][j];
         r.lout[i] = r.lin[j];
@@ -249,9 +252,7 @@ const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank
         launch_gather_u32(rank_cur, perm_.p, src_.p, n, s_);               // new k <- old position of perm[k]
     }
     dbg_mark(2, s_);
-    launch_gather_d4(xyzm_s_.p, src_.p, xyzm_alt_.p, n, s_);
-    swap_xyzm();
-    return src_.p;
+    return src_.p;  // the caller gathers the state (positions included) into the new order
 }
 
 void Engine::ensure_rank() {
@@ -597,10 +598,12 @@ void Simulation::reorder(const uint32_t* src) {
     DBuf<double>* pairs[][2] = {{&vx_, &vx2_}, {&vy_, &vy2_}, {&vz_, &vz2_}, {&ax_, &ax2_},
                                 {&ay_, &ay2_}, {&az_, &az2_}, {&amag_, &amag2_}};
     ReorderArgs r;
+    r.xin = eng_.xyzm_s(), r.xout = eng_.xyzm_alt();
     for (int k = 0; k < 7; ++k) r.in[k] = pairs[k][0]->p, r.out[k] = pairs[k][1]->p;
     r.lin = level_.p, r.lout = level2_.p, r.ain = active_.p, r.aout = active2_.p, r.tin = last_.p, r.tout = last2_.p;
     G2_COUNT(1), reorder_kernel<<<gridn(n), kB, 0, s>>>(r, src, n);  // one pass over the index for all state
     for (auto& pr : pairs) std::swap(pr[0]->p, pr[1]->p);
+    eng_.swap_xyzm();
     std::swap(level_.p, level2_.p);
     std::swap(active_.p, active2_.p);
     std::swap(last_.p, last2_.p);
@@ -707,15 +710,11 @@ StepResultH Simulation::step() {
     }
     shard_lo_ = lo, shard_hi_ = hi;
     const bool sharded = world_ > 1 && exchange_;
-    eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false, lo, hi, !sharded);
+    eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false, lo, hi, false);
     G2_CUDA(cudaEventRecord(ev_[4], s));
-    if (sharded) {
-        exchange_->allgather_acc(*this);  // every rank receives every group's accelerations
-        eng_.finalize_walk(sinks_.p, n_active_.p, uint32_t(n), false);
-    }
+    if (sharded) exchange_->allgather_acc(*this);  // every rank receives every group's accelerations
     G2_CUDA(cudaEventRecord(ev_[5], s));
-    launch_correct(st, sinks_.p, n_active_.p, uint32_t(n), eng_.ax_s(), eng_.ay_s(), eng_.az_s(), t_next_.p, now_,
-                   tick_, sd, s);
+    launch_correct(st, sinks_.p, n_active_.p, uint32_t(n), eng_.accum(), t_next_.p, now_, tick_, sd, s);
     G2_CUDA(cudaEventRecord(ev_[6], s));
 
     unsigned long long tn = 0;

@@ -106,10 +106,11 @@ __device__ int block_level_dev(double acc_mag, const SchemeDev& s) {
 }
 
 // ---- correct loop over active sinks (integrator.cpp:148-156, apply_level :86-95)
+// new accelerations straight from the walk's FP32 accumulators (slot s = sink s): the same
+// double(float) values the finalize pass would store, without the FP64 round trip
 __global__ void __launch_bounds__(kBlock) correct_kernel(StepState st, const uint32_t* __restrict__ sinks,
                                                          const uint32_t* n_sinks, uint32_t cap,
-                                                         const double* __restrict__ nax, const double* __restrict__ nay,
-                                                         const double* __restrict__ naz,
+                                                         const float4* __restrict__ acc4,
                                                          const unsigned long long* t_next_p, uint64_t now, double tick,
                                                          SchemeDev sc) {
     const uint32_t na = min(*n_sinks, cap);
@@ -117,7 +118,8 @@ __global__ void __launch_bounds__(kBlock) correct_kernel(StepState st, const uin
     for (uint32_t s = blockIdx.x * kBlock + threadIdx.x; s < na; s += gridDim.x * kBlock) {
         const uint32_t i = sinks[s];
         const double h = dmul(0.5, dmul(double(t_next - st.last_update[i]), tick));
-        const double ax = nax[i], ay = nay[i], az = naz[i];
+        const float4 a4 = acc4[s];
+        const double ax = double(a4.x), ay = double(a4.y), az = double(a4.z);
         st.vx[i] = dadd(st.vx[i], dmul(dsub(ax, st.ax[i]), h));
         st.vy[i] = dadd(st.vy[i], dmul(dsub(ay, st.ay[i]), h));
         st.vz[i] = dadd(st.vz[i], dmul(dsub(az, st.az[i]), h));
@@ -287,10 +289,10 @@ void launch_compact(const uint8_t* flags, size_t n, uint32_t* out, uint32_t* n_o
 }
 
 void launch_correct(const StepState& st, const uint32_t* sinks, const uint32_t* n_sinks, uint32_t n_cap,
-                    const double* nax, const double* nay, const double* naz, const unsigned long long* t_next,
-                    uint64_t now, double tick, SchemeDev sc, cudaStream_t s) {
-    G2_COUNT(1), correct_kernel<<<grid_for(n_cap), kBlock, 0, s>>>(st, sinks, n_sinks, n_cap, nax, nay, naz, t_next, now, tick,
-                                                      sc);
+                    const float4* acc4, const unsigned long long* t_next, uint64_t now, double tick, SchemeDev sc,
+                    cudaStream_t s) {
+    G2_COUNT(1), correct_kernel<<<grid_for(n_cap), kBlock, 0, s>>>(st, sinks, n_sinks, n_cap, acc4, t_next, now, tick,
+                                                                   sc);
 }
 
 void launch_assign_levels(const StepState& st, size_t n, SchemeDev sc, cudaStream_t s) {

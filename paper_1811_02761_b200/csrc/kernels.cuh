@@ -141,9 +141,10 @@ struct SchemeDev {
     double eta, dt_max, eps;
     int adaptive, fixed_level;
 };
+// acc4: the walk's accumulator slots (sink order), FP32 -> FP64 exactly
 void launch_correct(const StepState& st, const uint32_t* sinks, const uint32_t* n_sinks, uint32_t n_cap,
-                    const double* nax, const double* nay, const double* naz, const unsigned long long* t_next,
-                    uint64_t now, double tick, SchemeDev sc, cudaStream_t s);
+                    const float4* acc4, const unsigned long long* t_next, uint64_t now, double tick, SchemeDev sc,
+                    cudaStream_t s);
 void launch_assign_levels(const StepState& st, size_t n, SchemeDev sc, cudaStream_t s);
 // free-function forms used by the C-ABI parity entry points
 void launch_block_levels(const double* acc_mag, size_t n, SchemeDev sc, int* levels, cudaStream_t s);
