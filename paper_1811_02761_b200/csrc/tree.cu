@@ -253,6 +253,7 @@ __device__ __forceinline__ int lcp_digits(uint64_t a, uint64_t b) {
 struct SplitWindow {
     uint64_t key[kSplitTile + 2 * kSplitMaxCap + 2];
     int8_t L[kSplitTile + 2 * kSplitMaxCap + 1];
+    int8_t M[kSplitTile + kSplitMaxCap];  // M_j = min L over (j, j + lc], positions base - lc .. base + T - 1
 };
 
 // Loads the tile's key window and L values; then (lo, hi) of particle base + t (t = tile offset):
@@ -272,39 +273,35 @@ __device__ __forceinline__ void split_window(const uint64_t* __restrict__ keys, 
         w.L[t] = (j <= 0 || j >= int64_t(n)) ? int8_t(-1) : int8_t(lcp_digits(w.key[t], w.key[t + 1]));
     }
     __syncthreads();
+    // sliding minimum: the run through position j has more than lc particles ahead of j iff M_j >= depth
+    for (int t = threadIdx.x; t < kSplitTile + int(lc); t += kSplitThreads) {
+        int m = 127;
+        for (int q = 1; q <= int(lc); ++q) m = min(m, int(w.L[t + q]));
+        w.M[t] = int8_t(m);
+    }
+    __syncthreads();
 }
 
 // The window holds L = -1 outside [1, n), so runs end at the array ends without extra tests.
+// The depth-L_i run through i holds more than lc particles iff some lc+1 consecutive positions
+// containing i lie in it, i.e. iff max_{j in [i-lc, i]} M_j >= L_i (fixed-length loops, no
+// divergence).
 __device__ __forceinline__ void split_range(uint32_t n, uint32_t lc, uint32_t base, int t, const SplitWindow& w,
                                             int& lo, int& hi) {
     const uint32_t i = base + uint32_t(t);
     lo = kMaxDepth + 1, hi = kMaxDepth;
     if (i >= n) return;
-    const int8_t* L = w.L + t + int(lc);  // L[0] = L_i
-    int M = 127;                          // min L over (i, i + lc]
-    for (int q = 1; q <= int(lc); ++q) M = min(M, int(L[q]));
+    const int M = w.M[t + int(lc)];  // M_i
     if (i == 0) {
         lo = 0, hi = min(kMaxDepth, M + 1);
         return;
     }
-    const int li = L[0];
+    const int li = w.L[t + int(lc)];
     if (li >= kMortonBits) return;  // identical keys: no cell starts here
-    // size of the depth-li run through i = back + fwd: back = i - (last j <= i with L_j < li),
-    // fwd = (first j > i with L_j < li) - i; only whether it exceeds lc matters
-    int back = int(lc) + 1, fwd = int(lc) + 1;
-    for (int q = 0; q <= int(lc); ++q)
-        if (L[-q] < li) {
-            back = q;
-            break;
-        }
-    if (back <= int(lc))
-        for (int q = 1; q <= int(lc) - back; ++q)
-            if (L[q] < li) {
-                fwd = q;
-                break;
-            }
+    int W = -1;
+    for (int q = 0; q <= int(lc); ++q) W = max(W, int(w.M[t + q]));
     lo = li + 1;
-    hi = back + fwd > int(lc) ? min(kMaxDepth, max(li + 1, M + 1)) : li;
+    hi = W >= li ? min(kMaxDepth, max(li + 1, M + 1)) : li;
 }
 
 // per-depth counts of the tile's (item, warp) chunks -> chunk-exclusive prefixes in wcnt, tile totals returned
