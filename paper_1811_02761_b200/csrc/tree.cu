@@ -323,14 +323,18 @@ __device__ __forceinline__ void split_chunk_counts(const int* lo, const int* hi,
 
 __global__ void __launch_bounds__(kSplitThreads) split_count_kernel(const uint64_t* __restrict__ keys, uint32_t n,
                                                                     uint32_t lc, uint32_t* __restrict__ tile_counts,
-                                                                    uint32_t ntiles) {
+                                                                    uint32_t ntiles, uint16_t* __restrict__ lohi) {
     __shared__ SplitWindow w;
     __shared__ uint32_t wcnt[kMaxDepth + 1][kSplitChunks];
     const uint32_t base = blockIdx.x * kSplitTile;
     split_window(keys, n, lc, base, w);
     int lo[kSplitItems], hi[kSplitItems];
 #pragma unroll
-    for (int k = 0; k < kSplitItems; ++k) split_range(n, lc, base, k * kSplitThreads + threadIdx.x, w, lo[k], hi[k]);
+    for (int k = 0; k < kSplitItems; ++k) {
+        split_range(n, lc, base, k * kSplitThreads + threadIdx.x, w, lo[k], hi[k]);
+        const uint32_t i = base + k * kSplitThreads + threadIdx.x;
+        if (i < n) lohi[i] = uint16_t(lo[k] | (hi[k] << 8));  // the write pass reuses the ranges
+    }
     split_chunk_counts(lo, hi, wcnt);
     if (threadIdx.x <= kMaxDepth) {
         uint32_t c = 0;
@@ -382,8 +386,8 @@ __global__ void __launch_bounds__(1024) split_scan_kernel(uint32_t* __restrict__
 // cells in BFS order: first, depth, first_child (count and child_count follow in split_cells_kernel)
 __global__ void __launch_bounds__(kSplitThreads) split_write_kernel(SplitArgs a, uint32_t n,
                                                                     const uint32_t* __restrict__ tile_offs,
-                                                                    uint32_t ntiles, const uint32_t* __restrict__ totals) {
-    __shared__ SplitWindow w;
+                                                                    uint32_t ntiles, const uint32_t* __restrict__ totals,
+                                                                    const uint16_t* __restrict__ lohi) {
     __shared__ uint32_t wcnt[kMaxDepth + 1][kSplitChunks];
     __shared__ uint32_t lstart[kMaxDepth + 2];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -393,11 +397,13 @@ __global__ void __launch_bounds__(kSplitThreads) split_write_kernel(SplitArgs a,
         lstart[kMaxDepth + 1] = acc;
     }
     const uint32_t base = blockIdx.x * kSplitTile;
-    split_window(a.keys, n, a.leaf_cap, base, w);
     int lo[kSplitItems], hi[kSplitItems];
 #pragma unroll
-    for (int k = 0; k < kSplitItems; ++k)
-        split_range(n, a.leaf_cap, base, k * kSplitThreads + threadIdx.x, w, lo[k], hi[k]);
+    for (int k = 0; k < kSplitItems; ++k) {
+        const uint32_t i = base + k * kSplitThreads + threadIdx.x;
+        const uint32_t v = i < n ? lohi[i] : uint32_t(kMaxDepth + 1) | (uint32_t(kMaxDepth) << 8);
+        lo[k] = int(v & 0xffu), hi[k] = int(v >> 8);
+    }
     split_chunk_counts(lo, hi, wcnt);
     if (threadIdx.x <= kMaxDepth) {  // exclusive prefix over the tile's chunks, plus the tile offset
         uint32_t acc = lstart[threadIdx.x] + tile_offs[size_t(threadIdx.x) * ntiles + blockIdx.x];
@@ -674,15 +680,17 @@ void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const
     G2_CUDA(cudaGetLastError());
 }
 
-size_t split_tile_words(size_t n) { return (kMaxDepth + 1) * (ceil_div(n, kSplitTile) + 1) + 32; }
+// per-depth tile counts + totals, then the per-particle (lo, hi) depth ranges (u16)
+size_t split_tile_words(size_t n) { return (kMaxDepth + 1) * (ceil_div(n, kSplitTile) + 1) + 32 + (n + 1) / 2 + 4; }
 
 void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
     if (a.leaf_cap <= kSplitMaxCap && a.tiles) {
         const uint32_t ntiles = ceil_div(n, kSplitTile);
         uint32_t* totals = a.tiles + size_t(kMaxDepth + 1) * ntiles;
-        G2_COUNT(1), split_count_kernel<<<ntiles, kSplitThreads, 0, s>>>(a.keys, n, a.leaf_cap, a.tiles, ntiles);
+        uint16_t* lohi = reinterpret_cast<uint16_t*>(a.tiles + (kMaxDepth + 1) * (size_t(ntiles) + 1) + 32);
+        G2_COUNT(1), split_count_kernel<<<ntiles, kSplitThreads, 0, s>>>(a.keys, n, a.leaf_cap, a.tiles, ntiles, lohi);
         G2_COUNT(1), split_scan_kernel<<<kMaxDepth + 1, 1024, 0, s>>>(a.tiles, ntiles, totals);
-        G2_COUNT(1), split_write_kernel<<<ntiles, kSplitThreads, 0, s>>>(a, n, a.tiles, ntiles, totals);
+        G2_COUNT(1), split_write_kernel<<<ntiles, kSplitThreads, 0, s>>>(a, n, a.tiles, ntiles, totals, lohi);
         G2_COUNT(1), split_cells_kernel<<<grid_for(a.cell_cap), kBlock, 0, s>>>(a, n);
         G2_CUDA(cudaGetLastError());
         return;
