@@ -369,7 +369,7 @@ def run_g2(args):
         try:
             from oracle.refpy import Ref
             amag = sim.system().acc_old_mag
-            sample = args.cpu_sample or max(1, args.n // (1 << 16))
+            sample = args.cpu_sample or max(1, args.n // (1 << 18))  # same sample as the --impl reference arm
             t, ph = cpu_reference_step(mass, pos, vel, amag, sample)
             cpu = {"value": t, "unit": "s/step", "cores": int(Ref().lib.gtref_resolve_threads(0)), "kind": "reference",
                    "sample": f"oracle/_ref (unmodified reference library) on the same M31 N={args.n} input: "
