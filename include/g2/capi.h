@@ -117,6 +117,19 @@ int g2_block_level(size_t n, const double* acc_mag, const g2_step_scheme* s, dou
 /* predict (integrator.cpp:40-45) on the device; pos/vel updated in place */
 int g2_predict(size_t n, double* pos, double* vel, const double* acc, double dt, int device);
 
+/* Diagnostics (diagnostics.hpp:9-15) and compute_diagnostics (diagnostics.cpp:10-38): kinetic
+ * energy and momentum, potential energy by FP64 direct summation up to 2^17 particles
+ * (kDirectPotentialLimit) and beyond by a dacc = 2^-20 tree walk with potentials that uses
+ * acc_old_mag as the system's (NULL: zeros => geometric MAC, as for a fresh ParticleSystem).
+ * Throws (G2_SINGULARITY) on coincident particles with eps == 0 on the direct path. */
+typedef struct {
+    double kinetic, potential, total;
+    double momentum[3];
+    double virial_ratio;
+} g2_diagnostics;
+int g2_compute_diagnostics(size_t n, const double* mass, const double* pos, const double* vel,
+                           const double* acc_old_mag, const g2_grav_params* p, int device, g2_diagnostics* out);
+
 /* ---- Simulation (integrator.hpp:54-91, integrator.cpp:56-164) ------------- */
 int g2_sim_create(size_t n, const double* mass, const double* pos, const double* vel, const g2_grav_params* p,
                   const g2_step_scheme* s, const g2_engine_config* c, const g2_tuner_config* t, int device,

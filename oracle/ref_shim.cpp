@@ -24,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "gravitree/diagnostics.hpp"
 #include "gravitree/engine.hpp"
 #include "gravitree/errors.hpp"
 #include "gravitree/gravity.hpp"
@@ -303,6 +304,28 @@ int gtref_direct_sum(std::size_t n, const double* mass, const double* pos, doubl
         load_system(s, n, mass, pos, nullptr, nullptr, nullptr);
         const DirectSumResult r = direct_sum(s, GravParams{G, eps, 0.001953125}, threads);
         store_vec(r.acc, acc_out);
+    });
+}
+
+// compute_diagnostics (diagnostics.cpp:10-38) on a ParticleSystem built from flat arrays
+int gtref_diagnostics(std::size_t n, const double* mass, const double* pos, const double* vel,
+                      const double* acc_old_mag, double G, double eps, double dacc, unsigned threads, double* out7) {
+    return guarded([&] {
+        ParticleSystem sys;
+        sys.mass.assign(mass, mass + n);
+        sys.pos.resize(n), sys.vel.resize(n), sys.acc.assign(n, Vec3{});
+        for (std::size_t i = 0; i < n; ++i) {
+            sys.pos[i] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+            sys.vel[i] = {vel[3 * i], vel[3 * i + 1], vel[3 * i + 2]};
+        }
+        sys.acc_old_mag.assign(n, 0.0);
+        if (acc_old_mag) sys.acc_old_mag.assign(acc_old_mag, acc_old_mag + n);
+        sys.level.assign(n, 0);
+        GravParams p;
+        p.G = G, p.eps = eps, p.dacc = dacc;
+        const Diagnostics d = compute_diagnostics(sys, p, threads);
+        out7[0] = d.kinetic, out7[1] = d.potential, out7[2] = d.total;
+        out7[3] = d.momentum.x, out7[4] = d.momentum.y, out7[5] = d.momentum.z, out7[6] = d.virial_ratio;
     });
 }
 

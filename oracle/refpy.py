@@ -148,6 +148,19 @@ class Ref:
                                             C.c_uint(threads), acc.ctypes.data_as(C.c_void_p)))
         return acc
 
+    def diagnostics(self, mass, pos, vel, acc_old_mag=None, G=1.0, eps=0.0, dacc=2.0 ** -9, threads=0):
+        """compute_diagnostics (diagnostics.cpp:10-38) of the reference library."""
+        mass, pos, vel = _f64(mass), _f64(pos), _f64(vel)
+        am = None if acc_old_mag is None else _f64(acc_old_mag)
+        out = np.empty(7)
+        self._chk(self.lib.gtref_diagnostics(_sz(len(mass)), mass.ctypes.data_as(C.c_void_p),
+                                             pos.ctypes.data_as(C.c_void_p), vel.ctypes.data_as(C.c_void_p),
+                                             None if am is None else am.ctypes.data_as(C.c_void_p),
+                                             C.c_double(G), C.c_double(eps), C.c_double(dacc), C.c_uint(threads),
+                                             out.ctypes.data_as(C.c_void_p)))
+        return {"kinetic": out[0], "potential": out[1], "total": out[2], "momentum": out[3:6].copy(),
+                "virial_ratio": out[6]}
+
     def force_error(self, acc, ref):
         acc, ref = _f64(acc), _f64(ref)
         out = np.empty(4)

@@ -4,12 +4,13 @@ Drop-in for the gravitree hot path (Morton keys + radix sort, makeTree,
 calcNode, walkTree, block-step predict/correct) behind the C-ABI in
 include/g2/capi.h; ``gravitree`` is the Python mirror of the reference API.
 """
-from .gravitree import (DataError, EngineConfig, GravityEngine, GravParams, InternalError, ParticleSystem,
+from .gravitree import (DataError, Diagnostics, EngineConfig, GravityEngine, GravParams, InternalError, ParticleSystem,
                         ResourceError, Simulation, SingularityError, StepResult, StepScheme, TraversalEvents,
-                        TunerConfig, block_level, count_walk_ops, direct_sum, flops_estimate, force_error,
+                        TunerConfig, block_level, compute_diagnostics, count_walk_ops, direct_sum, flops_estimate,
+                        force_error,
                         nccl_unique_id, predict, walk_flops)
 
-__all__ = ["DataError", "EngineConfig", "GravityEngine", "GravParams", "InternalError", "ParticleSystem",
+__all__ = ["DataError", "Diagnostics", "EngineConfig", "GravityEngine", "GravParams", "InternalError", "ParticleSystem",
            "ResourceError", "Simulation", "SingularityError", "StepResult", "StepScheme", "TraversalEvents",
-           "TunerConfig", "block_level", "count_walk_ops", "direct_sum", "flops_estimate", "force_error",
+           "TunerConfig", "block_level", "compute_diagnostics", "count_walk_ops", "direct_sum", "flops_estimate", "force_error",
            "nccl_unique_id", "predict", "walk_flops"]

@@ -322,6 +322,50 @@ int g2_block_level(size_t n, const double* acc_mag, const g2_step_scheme* s, dou
     });
 }
 
+int g2_compute_diagnostics(size_t n, const double* mass, const double* pos, const double* vel,
+                           const double* acc_old_mag, const g2_grav_params* p, int device, g2_diagnostics* out) {
+    return guarded([&] {
+        *out = g2_diagnostics{};
+        if (n == 0) return;
+        G2_CUDA(cudaSetDevice(device));
+        constexpr size_t kDirectPotentialLimit = size_t(1) << 17;  // diagnostics.hpp:26
+        const bool direct = n <= kDirectPotentialLimit;
+        g2::DBuf<double> p3, m, v3;
+        g2::DBuf<double4> xyzm;
+        g2::DBuf<g2::DevFlags> flags;
+        p3.reserve(3 * n), m.reserve(n), v3.reserve(3 * n), xyzm.reserve(n), flags.reserve(1);
+        G2_CUDA(cudaMemset(flags.p, 0, sizeof(g2::DevFlags)));
+        G2_CUDA(cudaMemcpy(p3.p, pos, 3 * n * 8, cudaMemcpyHostToDevice));
+        G2_CUDA(cudaMemcpy(m.p, mass, n * 8, cudaMemcpyHostToDevice));
+        G2_CUDA(cudaMemcpy(v3.p, vel, 3 * n * 8, cudaMemcpyHostToDevice));
+        g2::launch_pack_identity(p3.p, m.p, xyzm.p, n, nullptr);
+        double km[4], w = 0.0;
+        g2::diagnostics_device(m.p, v3.p, xyzm.p, n, p->G, p->eps, direct, km, &w, flags.p, nullptr);
+        g2::DevFlags f;
+        G2_CUDA(cudaMemcpy(&f, flags.p, sizeof f, cudaMemcpyDeviceToHost));
+        if (f.singularity) throw g2::Error(G2_SINGULARITY, "direct_potential_energy: coincident particles");
+        if (!direct) {
+            // the reference's high-accuracy tree potential (diagnostics.cpp:19-31)
+            g2::GravParamsH tp;
+            tp.G = p->G, tp.eps = p->eps, tp.dacc = 0x1.0p-20;
+            g2::EngineConfigH c;
+            c.count_ops = false;
+            g2::Engine eng(tp, c, device);
+            eng.build(n, mass, pos, true);
+            std::vector<double> am(acc_old_mag ? acc_old_mag : nullptr, acc_old_mag ? acc_old_mag + n : nullptr);
+            if (!acc_old_mag) am.assign(n, 0.0);
+            std::vector<double> acc(3 * n), pot(n, 0.0);
+            eng.evaluate(n, mass, pos, am.data(), 0, nullptr, acc.data(), pot.data());
+            for (size_t i = 0; i < n; ++i) w += 0.5 * mass[i] * pot[i];
+        }
+        out->kinetic = km[0];
+        out->momentum[0] = km[1], out->momentum[1] = km[2], out->momentum[2] = km[3];
+        out->potential = w;
+        out->total = out->kinetic + out->potential;
+        out->virial_ratio = out->potential != 0.0 ? -2.0 * out->kinetic / out->potential : 0.0;
+    });
+}
+
 int g2_predict(size_t n, double* pos, double* vel, const double* acc, double dt, int device) {
     return guarded([&] {
         G2_CUDA(cudaSetDevice(device));

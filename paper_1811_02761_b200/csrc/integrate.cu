@@ -2,6 +2,9 @@
 // (gravity.cpp:18-43) and active-set compaction on sm_100a.  FP64 state,
 // explicit round-to-nearest intrinsics: given identical accelerations the
 // predictor/corrector/level updates are bit-identical to the reference.
+#include <algorithm>
+#include <vector>
+
 #include "kernels.cuh"
 
 namespace g2 {
@@ -189,6 +192,71 @@ __global__ void __launch_bounds__(kBlock) compact_kernel(const uint8_t* __restri
     if (tile == ntiles - 1 && tid == 0) *n_out = uint32_t(s_excl) + tot;
 }
 
+// ---- compute_diagnostics (diagnostics.cpp:10-38) ---------------------------------
+// kinetic energy and momentum: per-block FP64 partial sums (fixed launch => reruns bit-identical)
+__global__ void __launch_bounds__(kBlock) kinetic_kernel(const double* __restrict__ mass, const double* __restrict__ vel3,
+                                                         size_t n, double* __restrict__ partial) {
+    double k = 0.0, px = 0.0, py = 0.0, pz = 0.0;
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock) {
+        const double m = mass[i], vx = vel3[3 * i], vy = vel3[3 * i + 1], vz = vel3[3 * i + 2];
+        k = dadd(k, dmul(dmul(0.5, m), norm2(vx, vy, vz)));
+        px = dadd(px, dmul(m, vx)), py = dadd(py, dmul(m, vy)), pz = dadd(pz, dmul(m, vz));
+    }
+    __shared__ double sh[4][kBlock / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        k += __shfl_xor_sync(0xffffffffu, k, o), px += __shfl_xor_sync(0xffffffffu, px, o);
+        py += __shfl_xor_sync(0xffffffffu, py, o), pz += __shfl_xor_sync(0xffffffffu, pz, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) sh[0][w] = k, sh[1][w] = px, sh[2][w] = py, sh[3][w] = pz;
+    __syncthreads();
+    if (threadIdx.x < 4) {
+        double v = 0.0;
+        for (int q = 0; q < kBlock / 32; ++q) v += sh[threadIdx.x][q];
+        partial[4 * blockIdx.x + threadIdx.x] = v;
+    }
+}
+
+// direct potential energy: phi_i = sum_{j != i} -G m_j / sqrt(r2 + eps2) (softened_potential,
+// gravity.hpp:22-26) in FP64, sources tiled through shared memory; W = 1/2 sum_i m_i phi_i
+__global__ void __launch_bounds__(kBlock) direct_potential_kernel(const double4* __restrict__ xyzm, uint32_t n,
+                                                                  double G, double eps2, double* __restrict__ wpart,
+                                                                  DevFlags* flags) {
+    __shared__ double4 tile[kBlock];
+    const uint32_t i = blockIdx.x * kBlock + threadIdx.x;
+    const double4 ri = i < n ? xyzm[i] : make_double4(0, 0, 0, 0);
+    double phi = 0.0;
+    for (uint32_t base = 0; base < n; base += kBlock) {
+        __syncthreads();
+        if (base + threadIdx.x < n) tile[threadIdx.x] = xyzm[base + threadIdx.x];
+        __syncthreads();
+        const uint32_t m = min(uint32_t(kBlock), n - base);
+        for (uint32_t q = 0; q < m; ++q) {
+            const double4 rj = tile[q];
+            if (base + q == i) continue;
+            const double d2 = norm2(dsub(rj.x, ri.x), dsub(rj.y, ri.y), dsub(rj.z, ri.z));
+            if (eps2 == 0.0 && d2 == 0.0) {
+                flags->singularity = 1;  // direct_potential_energy throws (gravity.cpp:55-56)
+                continue;
+            }
+            const double r2 = dadd(d2, eps2);
+            phi = dsub(phi, ddiv(dmul(G, rj.w), dsqrt(r2)));
+        }
+    }
+    double w = i < n ? dmul(dmul(0.5, ri.w), phi) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+    __shared__ double sw[kBlock / 32];
+    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = w;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double v = 0.0;
+        for (int q = 0; q < kBlock / 32; ++q) v += sw[q];
+        wpart[blockIdx.x] = v;
+    }
+}
+
 __global__ void __launch_bounds__(kBlock) block_levels_kernel(const double* amag, size_t n, SchemeDev sc, int* out) {
     for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
         out[i] = block_level_dev(amag[i], sc);
@@ -263,6 +331,36 @@ void launch_direct_sum(const double4* xyzm, size_t n, double G, double eps, doub
                        DevFlags* flags, cudaStream_t s) {
     G2_COUNT(1), direct_kernel<<<ceil_div(n, kBlock), kBlock, 0, s>>>(xyzm, uint32_t(n), G, eps * eps, ax, ay, az, flags);
     G2_CUDA(cudaGetLastError());
+}
+
+void diagnostics_device(const double* mass, const double* vel3, const double4* xyzm, size_t n, double G, double eps,
+                        bool direct_potential, double* kin_mom4, double* w_direct, DevFlags* flags, cudaStream_t s) {
+    const unsigned kb = std::max(1u, std::min<unsigned>(ceil_div(n, kBlock), kNumSMs * 4));
+    DBuf<double> part;
+    part.reserve(size_t(4) * kb + 4);
+    G2_COUNT(1), kinetic_kernel<<<kb, kBlock, 0, s>>>(mass, vel3, n, part.p);
+    std::vector<double> h(4 * size_t(kb));
+    G2_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+    DBuf<double> wp;
+    const unsigned pb = ceil_div(n, kBlock);
+    std::vector<double> hw;
+    if (direct_potential) {
+        wp.reserve(pb + 1);
+        G2_COUNT(1), direct_potential_kernel<<<pb, kBlock, 0, s>>>(xyzm, uint32_t(n), G, eps * eps, wp.p, flags);
+        hw.resize(pb);
+        G2_CUDA(cudaMemcpyAsync(hw.data(), wp.p, pb * 8, cudaMemcpyDeviceToHost, s));
+    }
+    G2_CUDA(cudaStreamSynchronize(s));
+    for (int q = 0; q < 4; ++q) {
+        double v = 0.0;
+        for (unsigned b = 0; b < kb; ++b) v += h[4 * b + q];  // fixed merge order
+        kin_mom4[q] = v;
+    }
+    if (direct_potential) {
+        double v = 0.0;
+        for (unsigned b = 0; b < pb; ++b) v += hw[b];
+        *w_direct = v;
+    }
 }
 
 void launch_norm3(const double* ax, const double* ay, const double* az, double* out, size_t n, cudaStream_t s) {

@@ -124,6 +124,10 @@ void launch_direct_sum(const double4* xyzm, size_t n, double G, double eps, doub
                        DevFlags* flags, cudaStream_t s);
 void launch_direct_targets(const double4* xyzm, size_t n, const uint32_t* targets, size_t nt, double G, double eps,
                            double* acc3, cudaStream_t s);
+// compute_diagnostics (diagnostics.cpp:10-38) on the device: kinetic energy + momentum (kin_mom4), and
+// when direct_potential the FP64 direct potential energy (n <= 2^17 path) into *w_direct; synchronises
+void diagnostics_device(const double* mass, const double* vel3, const double4* xyzm, size_t n, double G, double eps,
+                        bool direct_potential, double* kin_mom4, double* w_direct, DevFlags* flags, cudaStream_t s);
 void launch_norm3(const double* ax, const double* ay, const double* az, double* out, size_t n, cudaStream_t s);
 struct StepState {
     double4* xyzm;

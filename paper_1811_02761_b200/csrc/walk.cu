@@ -276,10 +276,11 @@ struct Screen {
     __device__ __forceinline__ uint32_t nleaf() const { return (!accept && leaf()) ? (info & ~kLeafBit) : 0u; }
 };
 
-__device__ __forceinline__ Screen screen(const TreeView& t, const GroupRec& g, const WalkParams& p, uint32_t c,
+// The FP64 group record is re-read only for undecided cells (rare), so the traversal loop does
+// not hold its 12 registers.
+__device__ __forceinline__ Screen screen(const TreeView& t, const GroupRec* gp, const WalkParams& p, uint32_t c,
                                          bool valid, float gxh, float gyh, float gzh, float gxl, float gyl, float gzl,
-                                         float tolc, float radf, float rhsf, double rhs, float G, float thetaf,
-                                         bool geom) {
+                                         float tolc, float radf, float rhsf, float G, float thetaf, bool geom) {
     Screen s{0.f, 0.f, 0.f, 0.f, 0u, 0u, false};
     if (!valid) return s;  // info 0: internal with no children, not accepted -> contributes nothing
     const WNode32 nd = ld_node32(t.nodes32 + c);
@@ -307,7 +308,10 @@ __device__ __forceinline__ Screen screen(const TreeView& t, const GroupRec& g, c
                 verdict = num <= den * (1.f - tol) ? 1 : (num > den * (1.f + tol) ? 0 : 2);
         }
     }
-    if (verdict == 2) verdict = mac_exact(t.nodes[c], g, p, rhs, geom) ? 1 : 0;
+    if (verdict == 2) {
+        const GroupRec g = *gp;
+        verdict = mac_exact(t.nodes[c], g, p, dmul(p.dacc, g.a_min), geom) ? 1 : 0;
+    }
     s.accept = verdict == 1;
     return s;
 }
@@ -462,10 +466,11 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         // ---------------- group
         uint64_t t_begin = 0;
         if (b.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_begin));
-        const GroupRec g = b.groups[grp];
+        const GroupRec* gp = b.groups + grp;
+        const GroupRec g = *gp;
         const bool geom = p.force_geometric || g.a_min <= 0.0;  // engine.cpp:66
-        const double rhs = dmul(p.dacc, g.a_min);
-        const float rhsf = float(rhs), radf = float(g.radius);
+        const float rhsf = float(dmul(p.dacc, g.a_min)), radf = float(g.radius);
+        const uint32_t gcount = g.count;
         // group centre as an unevaluated FP32 sum hi + lo: (hi - c) + lo is the FP32 difference to a
         // node's FP32 centre c with error <= 2^-24 (|c| + 2|d|) per axis (no FP64 in the screen)
         const float gxh = float(g.cx), gyh = float(g.cy), gzh = float(g.cz);
@@ -511,9 +516,9 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             __syncwarp();
             macs += take;
             const bool valid0 = lane < take, valid1 = lane + 32 < take;
-            const Screen s0 = screen(t, g, p, c0, valid0, gxh, gyh, gzh, gxl, gyl, gzl, tolc, radf, rhsf, rhs, G, thetaf,
+            const Screen s0 = screen(t, gp, p, c0, valid0, gxh, gyh, gzh, gxl, gyl, gzl, tolc, radf, rhsf, G, thetaf,
                                      geom);
-            const Screen s1 = screen(t, g, p, c1, valid1, gxh, gyh, gzh, gxl, gyl, gzl, tolc, radf, rhsf, rhs, G, thetaf,
+            const Screen s1 = screen(t, gp, p, c1, valid1, gxh, gyh, gzh, gxl, gyl, gzl, tolc, radf, rhsf, G, thetaf,
                                      geom);
             const uint32_t nchild0 = s0.nchild(), nchild1 = s1.nchild();
             const uint32_t nleaf0 = s0.nleaf(), nleaf1 = s1.nleaf();
@@ -732,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
 
         // ---------------- events
         if (lane == 0) {
-            const unsigned long long inter = (unsigned long long)pushes * g.count;
+            const unsigned long long inter = (unsigned long long)pushes * gcount;
             if (p.count_ops) {
                 atomicAdd(&b.events[0], inter);
                 atomicAdd(&b.events[1], (unsigned long long)macs);

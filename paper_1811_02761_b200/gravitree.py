@@ -437,6 +437,32 @@ def direct_sum_targets(system: ParticleSystem, targets, params: GravParams = Non
     return acc
 
 
+@dataclass
+class Diagnostics:
+    """Diagnostics (diagnostics.hpp:9-15)."""
+    kinetic: float = 0.0
+    potential: float = 0.0
+    total: float = 0.0
+    momentum: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    virial_ratio: float = 0.0
+
+
+class _CDiag(C.Structure):
+    _fields_ = [("kinetic", C.c_double), ("potential", C.c_double), ("total", C.c_double),
+                ("momentum", C.c_double * 3), ("virial_ratio", C.c_double)]
+
+
+def compute_diagnostics(system: ParticleSystem, params: GravParams = None, device: int = 0) -> Diagnostics:
+    """compute_diagnostics (diagnostics.cpp:10-38) on the device: energies, momentum and virial ratio.
+    The potential is an FP64 direct sum up to 2^17 particles, beyond that the reference's dacc = 2^-20
+    tree walk (FP32 forces/potentials) with the system's acc_old_mag."""
+    p = params or GravParams()
+    d = _CDiag()
+    _chk(_lib.g2_compute_diagnostics(C.c_size_t(system.n()), _ptr(system.mass), _ptr(system.pos), _ptr(system.vel),
+                                     _ptr(system.acc_old_mag), C.byref(p._c()), C.c_int(device), C.byref(d)))
+    return Diagnostics(d.kinetic, d.potential, d.total, np.array(list(d.momentum)), d.virial_ratio)
+
+
 def block_level(acc_mag, scheme: StepScheme = None, eps: float = 0.0, device: int = 0):
     """block_level (integrator.cpp:21-33), vectorised over acc_mag, on the device."""
     a = np.atleast_1d(np.ascontiguousarray(acc_mag, dtype=np.float64))
