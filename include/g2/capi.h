@@ -130,6 +130,18 @@ typedef struct {
 int g2_compute_diagnostics(size_t n, const double* mass, const double* pos, const double* vel,
                            const double* acc_old_mag, const g2_grav_params* p, int device, g2_diagnostics* out);
 
+/* ---- OCTF snapshots (snapshot.hpp:10-30, snapshot.cpp:65-121) ----------------
+ * Little-endian "OCTF", u32 version 1, u64 n, f64 time, G, eps, f64 mass[n], pos[3n], vel[3n]:
+ * the arrays ARE the C-ABI layout.  Failures are G2_DATA_ERROR with the reference's messages
+ * (bad magic / unsupported version / zero particle count / truncated <field> at byte <offset>).
+ * g2_read_snapshot fills caller buffers of capacity cap (g2_snapshot_info gives n first). */
+int g2_snapshot_info(const char* path, size_t* n, double* time, double* G, double* eps);
+int g2_read_snapshot(const char* path, size_t cap, double* mass, double* pos, double* vel, size_t* n, double* time,
+                     double* G, double* eps);
+/* atomic (temp file + rename), write_snapshot(path, system, params) */
+int g2_write_snapshot(const char* path, size_t n, const double* mass, const double* pos, const double* vel,
+                      double time, const g2_grav_params* p);
+
 /* ---- Simulation (integrator.hpp:54-91, integrator.cpp:56-164) ------------- */
 int g2_sim_create(size_t n, const double* mass, const double* pos, const double* vel, const g2_grav_params* p,
                   const g2_step_scheme* s, const g2_engine_config* c, const g2_tuner_config* t, int device,
@@ -149,6 +161,12 @@ int g2_sim_set_state(g2_sim* s, const double* pos, const double* vel);
 int g2_sim_tree_size(g2_sim* s, size_t* n, size_t* ncells);
 int g2_sim_get_tree(g2_sim* s, double* bbox4, uint64_t* keys, uint32_t* perm, uint32_t* rank, uint32_t* cells4,
                     uint8_t* depth, double* nodes5);
+/* Simulation from a snapshot file: read straight into pinned host memory and uploaded (no AoS
+ * conversion); GravParams = (snapshot G, snapshot eps, dacc), as the reference CLI builds them. */
+int g2_sim_create_from_snapshot(const char* path, double dacc, const g2_step_scheme* s, const g2_engine_config* c,
+                                const g2_tuner_config* t, int device, g2_sim** out);
+/* the device-resident state (original order) written as a snapshot with the simulation's time, G, eps */
+int g2_sim_write_snapshot(g2_sim* s, const char* path);
 /* extension: rebuild the tree every step (the all-active "full step" benchmark) */
 int g2_sim_set_rebuild_every_step(g2_sim* s, int on);
 int g2_sim_tuner_interval(g2_sim* s, size_t* interval);

@@ -26,6 +26,7 @@
 
 #include "gravitree/diagnostics.hpp"
 #include "gravitree/engine.hpp"
+#include "gravitree/snapshot.hpp"
 #include "gravitree/errors.hpp"
 #include "gravitree/gravity.hpp"
 #include "gravitree/integrator.hpp"
@@ -304,6 +305,36 @@ int gtref_direct_sum(std::size_t n, const double* mass, const double* pos, doubl
         load_system(s, n, mass, pos, nullptr, nullptr, nullptr);
         const DirectSumResult r = direct_sum(s, GravParams{G, eps, 0.001953125}, threads);
         store_vec(r.acc, acc_out);
+    });
+}
+
+// write_snapshot / read_snapshot (snapshot.cpp:65-121) on flat arrays
+int gtref_write_snapshot(const char* path, std::size_t n, const double* mass, const double* pos, const double* vel,
+                         double time, double G, double eps) {
+    return guarded([&] {
+        ParticleSystem sys(n);
+        sys.mass.assign(mass, mass + n);
+        for (std::size_t i = 0; i < n; ++i) {
+            sys.pos[i] = {pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]};
+            sys.vel[i] = {vel[3 * i], vel[3 * i + 1], vel[3 * i + 2]};
+        }
+        sys.time = time;
+        GravParams p;
+        p.G = G, p.eps = eps;
+        write_snapshot(path, sys, p);
+    });
+}
+int gtref_read_snapshot(const char* path, std::size_t cap, double* mass, double* pos, double* vel, double* hdr4) {
+    return guarded([&] {
+        const Snapshot s = read_snapshot(path);
+        const std::size_t n = s.system.n();
+        hdr4[0] = double(n), hdr4[1] = s.system.time, hdr4[2] = s.G, hdr4[3] = s.eps;
+        if (n > cap) return;
+        for (std::size_t i = 0; i < n; ++i) {
+            mass[i] = s.system.mass[i];
+            pos[3 * i] = s.system.pos[i].x, pos[3 * i + 1] = s.system.pos[i].y, pos[3 * i + 2] = s.system.pos[i].z;
+            vel[3 * i] = s.system.vel[i].x, vel[3 * i + 1] = s.system.vel[i].y, vel[3 * i + 2] = s.system.vel[i].z;
+        }
     });
 }
 

@@ -32,6 +32,7 @@ class RefError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"status {code}: {msg}")
         self.code = code
+        self.msg = msg
 
 
 def _f64(a):
@@ -147,6 +148,24 @@ class Ref:
                                             pos.ctypes.data_as(C.c_void_p), C.c_double(G), C.c_double(eps),
                                             C.c_uint(threads), acc.ctypes.data_as(C.c_void_p)))
         return acc
+
+    def write_snapshot(self, path, mass, pos, vel, time=0.0, G=1.0, eps=0.0):
+        mass, pos, vel = _f64(mass), _f64(pos), _f64(vel)
+        self._chk(self.lib.gtref_write_snapshot(str(path).encode(), _sz(len(mass)), mass.ctypes.data_as(C.c_void_p),
+                                                pos.ctypes.data_as(C.c_void_p), vel.ctypes.data_as(C.c_void_p),
+                                                C.c_double(time), C.c_double(G), C.c_double(eps)))
+
+    def read_snapshot(self, path):
+        """-> (mass, pos, vel, time, G, eps); raises DataError with the reference's message."""
+        hdr = np.zeros(4)
+        self._chk(self.lib.gtref_read_snapshot(str(path).encode(), _sz(0), None, None, None,
+                                               hdr.ctypes.data_as(C.c_void_p)))
+        n = int(hdr[0])
+        mass, pos, vel = np.empty(n), np.empty((n, 3)), np.empty((n, 3))
+        self._chk(self.lib.gtref_read_snapshot(str(path).encode(), _sz(n), mass.ctypes.data_as(C.c_void_p),
+                                               pos.ctypes.data_as(C.c_void_p), vel.ctypes.data_as(C.c_void_p),
+                                               hdr.ctypes.data_as(C.c_void_p)))
+        return mass, pos, vel, hdr[1], hdr[2], hdr[3]
 
     def diagnostics(self, mass, pos, vel, acc_old_mag=None, G=1.0, eps=0.0, dacc=2.0 ** -9, threads=0):
         """compute_diagnostics (diagnostics.cpp:10-38) of the reference library."""

@@ -12,6 +12,7 @@
 
 #include "../../include/g2/capi.h"
 #include "engine.cuh"
+#include "snapshot.hpp"
 
 struct g2_engine {
     std::unique_ptr<g2::Engine> e;
@@ -29,6 +30,9 @@ int guarded(F&& f) {
     } catch (const g2::Error& e) {
         g_err = e.what();
         return e.code;
+    } catch (const g2::SnapshotError& e) {  // the reference's data_error
+        g_err = e.what();
+        return G2_DATA_ERROR;
     } catch (const std::exception& e) {
         g_err = e.what();
         return G2_INTERNAL;
@@ -366,6 +370,30 @@ int g2_compute_diagnostics(size_t n, const double* mass, const double* pos, cons
     });
 }
 
+int g2_snapshot_info(const char* path, size_t* n, double* time, double* G, double* eps) {
+    return guarded([&] {
+        const g2::SnapshotHeader h = g2::read_snapshot_header(path);
+        if (n) *n = size_t(h.n);
+        if (time) *time = h.time;
+        if (G) *G = h.G;
+        if (eps) *eps = h.eps;
+    });
+}
+int g2_read_snapshot(const char* path, size_t cap, double* mass, double* pos, double* vel, size_t* n, double* time,
+                     double* G, double* eps) {
+    return guarded([&] {
+        const g2::SnapshotHeader h = g2::read_snapshot(path, mass, pos, vel, cap);
+        if (n) *n = size_t(h.n);
+        if (time) *time = h.time;
+        if (G) *G = h.G;
+        if (eps) *eps = h.eps;
+    });
+}
+int g2_write_snapshot(const char* path, size_t n, const double* mass, const double* pos, const double* vel,
+                      double time, const g2_grav_params* p) {
+    return guarded([&] { g2::write_snapshot(path, n, mass, pos, vel, time, p->G, p->eps); });
+}
+
 int g2_predict(size_t n, double* pos, double* vel, const double* acc, double dt, int device) {
     return guarded([&] {
         G2_CUDA(cudaSetDevice(device));
@@ -392,6 +420,39 @@ int g2_sim_create(size_t n, const double* mass, const double* pos, const double*
             throw;
         }
         *out = h;
+    });
+}
+int g2_sim_create_from_snapshot(const char* path, double dacc, const g2_step_scheme* s, const g2_engine_config* c,
+                                const g2_tuner_config* t, int device, g2_sim** out) {
+    return guarded([&] {
+        const g2::SnapshotHeader h = g2::read_snapshot_header(path);
+        const size_t n = size_t(h.n);
+        G2_CUDA(cudaSetDevice(device));
+        double* buf = nullptr;  // pinned: the reads land where the H2D copies stream from
+        G2_CUDA(cudaMallocHost(&buf, 7 * n * sizeof(double)));
+        std::unique_ptr<double, decltype(&cudaFreeHost)> hold(buf, &cudaFreeHost);
+        g2::read_snapshot(path, buf, buf + n, buf + 4 * n, n);
+        const g2_grav_params p{h.G, h.eps, dacc};
+        auto* sim = new g2_sim;
+        try {
+            sim->s = std::make_unique<g2::Simulation>(n, buf, buf + n, buf + 4 * n, to_h(&p), to_h(s), to_h(c), to_h(t),
+                                                      device);
+        } catch (...) {
+            delete sim;
+            throw;
+        }
+        *out = sim;
+    });
+}
+int g2_sim_write_snapshot(g2_sim* s, const char* path) {
+    return guarded([&] {
+        const size_t n = s->s->n();
+        std::vector<double> m(n), p(3 * n), v(3 * n);
+        double time = 0.0;
+        s->s->get_state(p.data(), v.data(), nullptr, nullptr, nullptr, &time);
+        s->s->get_mass(m.data());
+        const auto& gp = s->s->grav_params();
+        g2::write_snapshot(path, n, m.data(), p.data(), v.data(), time, gp.G, gp.eps);
     });
 }
 void g2_sim_destroy(g2_sim* s) { delete s; }

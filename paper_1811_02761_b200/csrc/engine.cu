@@ -776,6 +776,19 @@ void Simulation::get_state(double* pos, double* vel, double* acc, double* acc_ol
     if (time) *time = time_;
 }
 
+__global__ void xyzm_to_mass_kernel(const double4* __restrict__ xyzm, const uint32_t* __restrict__ idx, double* mass,
+                                    size_t n) {
+    for (size_t j = blockIdx.x * size_t(kB) + threadIdx.x; j < n; j += size_t(gridDim.x) * kB) mass[j] = xyzm[idx[j]].w;
+}
+
+void Simulation::get_mass(double* mass) {
+    cudaStream_t s = eng_.stream();
+    io_.reserve(3 * n_);
+    G2_COUNT(1), xyzm_to_mass_kernel<<<gridn(n_), kB, 0, s>>>(eng_.xyzm_s(), rank_cur(), io_.p, n_);
+    G2_CUDA(cudaMemcpyAsync(mass, io_.p, n_ * 8, cudaMemcpyDeviceToHost, s));
+    G2_CUDA(cudaStreamSynchronize(s));
+}
+
 void Simulation::set_state(const double* pos, const double* vel) {
     cudaStream_t s = eng_.stream();
     const size_t n = n_;

@@ -203,6 +203,8 @@ public:
     }
     // orig-order host copies
     void get_state(double* pos, double* vel, double* acc, double* acc_old_mag, uint8_t* level, double* time);
+    void get_mass(double* mass);  // original order
+    const GravParamsH& grav_params() const { return p_; }
     void set_state(const double* pos, const double* vel);  // overwrite pos/vel (orig order), keeps the rest
     Engine& engine() { return eng_; }
     RebuildTuner& tuner() { return tuner_; }

@@ -362,6 +362,31 @@ class Simulation:
     def set_fixed_rebuild_interval(self, interval: int):
         _chk(_lib.g2_sim_set_fixed_rebuild_interval(self._h, C.c_size_t(interval)))
 
+    @classmethod
+    def from_snapshot(cls, path, dacc: float = 2.0 ** -9, scheme: StepScheme = None,
+                      engine_config: EngineConfig = None, tuner_config: TunerConfig = None, device: int = 0):
+        """Simulation over a snapshot (read into pinned memory and uploaded in the library), with
+        GravParams(snapshot G, snapshot eps, dacc) as the reference CLI builds them."""
+        self = cls.__new__(cls)
+        info = [C.c_size_t(), C.c_double(), C.c_double(), C.c_double()]
+        _chk(_lib.g2_snapshot_info(str(path).encode(), *[C.byref(x) for x in info]))
+        self._params = GravParams(info[2].value, info[3].value, dacc)
+        self._scheme = scheme or StepScheme()
+        self._n = info[0].value
+        self._h = C.c_void_p()
+        _chk(_lib.g2_sim_create_from_snapshot(str(path).encode(), C.c_double(dacc), C.byref(self._scheme._c()),
+                                              C.byref((engine_config or EngineConfig())._c()),
+                                              C.byref((tuner_config or TunerConfig())._c()), C.c_int(device),
+                                              C.byref(self._h)))
+        snap = read_snapshot(path)  # masses for system() (the device holds them in Morton order)
+        self._mass = snap.system.mass
+        self._initialized = False
+        return self
+
+    def write_snapshot(self, path):
+        """The device-resident state as an OCTF snapshot (time, G, eps of this simulation)."""
+        _chk(_lib.g2_sim_write_snapshot(self._h, str(path).encode()))
+
     def tree(self) -> Tree:
         """engine().tree() (integrator.hpp:62): the octree of the last rebuild."""
         n, nc = C.c_size_t(), C.c_size_t()
@@ -435,6 +460,33 @@ def direct_sum_targets(system: ParticleSystem, targets, params: GravParams = Non
     _chk(_lib.g2_direct_sum_targets(C.c_size_t(system.n()), _ptr(system.mass), _ptr(system.pos), C.c_double(p.G),
                                     C.c_double(p.eps), C.c_size_t(len(tg)), _ptr(tg), C.c_int(device), _ptr(acc)))
     return acc
+
+
+@dataclass
+class Snapshot:
+    """Snapshot (snapshot.hpp:16-20): the system (with its time) and the G, eps stored with it."""
+    system: ParticleSystem
+    G: float = 1.0
+    eps: float = 0.0
+
+
+def read_snapshot(path) -> Snapshot:
+    """read_snapshot (snapshot.cpp:97-121): DataError with the reference's byte-offset messages."""
+    n, t, G, eps = C.c_size_t(), C.c_double(), C.c_double(), C.c_double()
+    _chk(_lib.g2_snapshot_info(str(path).encode(), C.byref(n), C.byref(t), C.byref(G), C.byref(eps)))
+    mass, pos, vel = np.empty(n.value), np.empty((n.value, 3)), np.empty((n.value, 3))
+    _chk(_lib.g2_read_snapshot(str(path).encode(), C.c_size_t(n.value), _ptr(mass), _ptr(pos), _ptr(vel), None,
+                               None, None, None))
+    sysm = ParticleSystem(mass, pos, vel)
+    sysm.time = t.value
+    return Snapshot(sysm, G.value, eps.value)
+
+
+def write_snapshot(path, system: ParticleSystem, params: GravParams = None):
+    """write_snapshot (snapshot.cpp:65-95): atomic temp file + rename."""
+    p = params or GravParams()
+    _chk(_lib.g2_write_snapshot(str(path).encode(), C.c_size_t(system.n()), _ptr(system.mass), _ptr(system.pos),
+                                _ptr(system.vel), C.c_double(system.time), C.byref(p._c())))
 
 
 @dataclass
