@@ -324,3 +324,42 @@ def test_simulation_rebuild_ties(g2, oracle, cluster):
         ref = oracle.build_tree(mass, st.pos)
         for k in ("keys", "perm", "rank", "cells", "depth"):
             assert np.array_equal(getattr(t, k), getattr(ref, k)), k
+
+
+@pytest.mark.slow
+def test_config2_plummer_2e20_block_steps(g2, ref):
+    """BASELINE config 2: Plummer 2^20, 16 block time steps of the GPU Simulation (reference driver
+    defaults, fixed rebuild interval 8); at each rebuild the tree equals the reference build_tree of
+    that step's positions bit for bit, and after 16 steps a fresh reference walk of the evolved state
+    (sampled sinks) matches the GPU walk within the FP32 tolerance, events exact."""
+    m, p, v = ref.sample_model("plummer", 1 << 20, 1)
+    params = g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9)
+    sim = g2.Simulation(g2.ParticleSystem(m, p, v), params, g2.StepScheme())
+    sim.init()  # n > 65536: builds the tree and bootstraps with the geometric walk (engine.cpp:95-100)
+    sim.set_fixed_rebuild_interval(8)
+    t, rt = sim.tree(), ref.build_tree(m, p)
+    for k in ("bbox", "keys", "perm", "rank", "cells", "depth"):
+        assert np.array_equal(getattr(t, k), getattr(rt, k)), k
+    rebuilds = 0
+    for _ in range(16):
+        r = sim.step()
+        if r.rebuilt:
+            rebuilds += 1
+            st = sim.system()
+            t, rt = sim.tree(), ref.build_tree(m, st.pos)
+            for k in ("bbox", "keys", "perm", "rank", "cells", "depth"):
+                assert np.array_equal(getattr(t, k), getattr(rt, k)), k
+    assert rebuilds >= 1
+    st = sim.system()
+    tg = np.sort(np.random.default_rng(5).choice(len(m), 8192, replace=False)).astype(np.uint32)
+    e = ref.engine(eps=params.eps, dacc=params.dacc, threads=0)
+    e.build(m, st.pos)
+    acc_r, _, ev_r = e.evaluate(m, st.pos, st.acc_old_mag, targets=tg)
+    s = g2.ParticleSystem(m, st.pos, acc_old_mag=st.acc_old_mag)
+    eng = g2.GravityEngine(params)
+    eng.build(s)
+    ev = eng.evaluate(s, targets=tg)
+    assert (ev.interactions, ev.mac_evals, ev.list_pushes) == (ev_r["interactions"], ev_r["mac_evals"],
+                                                               ev_r["list_pushes"])
+    err = g2.force_error(s.acc[tg], acc_r[tg])
+    assert err["median"] <= MED_TOL and err["p99"] <= P99_TOL, err
