@@ -330,13 +330,6 @@ void Engine::read_events(EventsH& ev) {
     ev.interactions = e[0], ev.mac_evals = e[1], ev.list_pushes = e[2];
 }
 
-void Engine::finalize_walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, bool with_pot) {
-    WalkBuffers b{};
-    b.sinks = sinks;
-    b.n_sinks = n_sinks_dev;
-    b.accum = accum_.p;
-    launch_walk_finalize(b, n_sinks_cap, ax_s_.p, ay_s_.p, az_s_.p, with_pot ? pot_s_.p : nullptr, s_);
-}
 
 EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, const double* amag_s,
                      bool with_pot, bool sync_events, uint32_t group_lo, uint32_t group_hi, bool finalize) {

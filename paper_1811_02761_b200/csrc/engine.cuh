@@ -67,7 +67,6 @@ public:
                  bool with_pot, bool sync_events, uint32_t group_lo = 0, uint32_t group_hi = ~0u,
                  bool finalize = true);
     // accum slots -> FP64 accelerations at the sinks' sorted positions
-    void finalize_walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, bool with_pot);
     float4* accum() { return accum_.p; }
     size_t accum_cap() const { return accum_.cap; }
     void reserve_accum(size_t slots) { accum_.reserve(slots); }

@@ -66,9 +66,7 @@ void launch_leaf_rel(const double4* xyzm, const uint32_t* child_count, const uin
                      const WNode32* nodes32, uint32_t ncells, float4* rel, cudaStream_t s);
 
 // out[k] = in[src[k]] gathers
-void launch_gather_d4(const double4* in, const uint32_t* src, double4* out, size_t n, cudaStream_t s);
 void launch_gather_f64(const double* in, const uint32_t* src, double* out, size_t n, cudaStream_t s);
-void launch_gather_u64(const uint64_t* in, const uint32_t* src, uint64_t* out, size_t n, cudaStream_t s);
 void launch_gather_u8(const uint8_t* in, const uint32_t* src, uint8_t* out, size_t n, cudaStream_t s);
 void launch_gather_u32(const uint32_t* in, const uint32_t* src, uint32_t* out, size_t n, cudaStream_t s);
 // equal-key runs of a storage-order sort: src (storage positions) re-ordered by ids[src] within runs

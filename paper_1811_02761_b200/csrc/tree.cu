@@ -744,14 +744,8 @@ void launch_leaf_rel(const double4* xyzm, const uint32_t* child_count, const uin
     G2_CUDA(cudaGetLastError());
 }
 
-void launch_gather_d4(const double4* in, const uint32_t* src, double4* out, size_t n, cudaStream_t s) {
-    G2_COUNT(1), gather_kernel<double4><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
-}
 void launch_gather_f64(const double* in, const uint32_t* src, double* out, size_t n, cudaStream_t s) {
     G2_COUNT(1), gather_kernel<double><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
-}
-void launch_gather_u64(const uint64_t* in, const uint32_t* src, uint64_t* out, size_t n, cudaStream_t s) {
-    G2_COUNT(1), gather_kernel<uint64_t><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
 }
 void launch_gather_u8(const uint8_t* in, const uint32_t* src, uint8_t* out, size_t n, cudaStream_t s) {
     G2_COUNT(1), gather_kernel<uint8_t><<<grid_for(n), kBlock, 0, s>>>(in, src, out, n);
