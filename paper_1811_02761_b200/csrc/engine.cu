@@ -112,6 +112,8 @@ Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), devic
     batch_.reserve(size_t(queue_cap_) * 32);
     G2_CUDA(cudaMemsetAsync(queue_.p, 0xff, size_t(queue_cap_) * sizeof(uint64_t), s_));
     spill_.reserve(walk_resident_warps() * walk_spill_words());
+    G2_CUDA(cudaMallocHost(&hs_, sizeof(HostSync)));
+    *hs_ = HostSync{};
 }
 
 Engine::~Engine() {
@@ -119,6 +121,7 @@ Engine::~Engine() {
         cudaStreamSynchronize(s_);
         cudaStreamDestroy(s_);
     }
+    if (hs_) cudaFreeHost(hs_);
 }
 
 void Engine::reserve(size_t n) {
@@ -143,10 +146,24 @@ void Engine::ensure_cells(size_t cap) {
     cell_cap_ = cap;
 }
 
+// Results read back at a step/build boundary share one pinned staging block and ONE
+// stream synchronisation (each extra host round trip idles the GPU between steps).
+void Engine::enqueue_flags() {
+    G2_CUDA(cudaMemcpyAsync(&hs_->flags, flags_.p, sizeof(DevFlags), cudaMemcpyDeviceToHost, s_));
+}
+void Engine::enqueue_events() {
+    G2_CUDA(cudaMemcpyAsync(hs_->events, events_.p, sizeof hs_->events, cudaMemcpyDeviceToHost, s_));
+}
+void Engine::sync() { G2_CUDA(cudaStreamSynchronize(s_)); }
+
 void Engine::check_flags() {
-    G2_CUDA(cudaStreamSynchronize(s_));
-    DevFlags f;
-    G2_CUDA(cudaMemcpy(&f, flags_.p, sizeof f, cudaMemcpyDeviceToHost));
+    enqueue_flags();
+    sync();
+    raise_flags();
+}
+
+void Engine::raise_flags() {
+    const DevFlags f = hs_->flags;
     if (f.data_error || f.resource_error || f.singularity || f.stack_overflow || f.queue_overflow) {
         G2_CUDA(cudaMemset(flags_.p, 0, sizeof(DevFlags)));
         if (f.singularity) throw Error(kSingularity, "direct_sum: coincident particles with zero softening");
@@ -262,10 +279,9 @@ void Engine::ensure_rank() {
 }
 
 bool Engine::take_tie_overflow() {
-    DevFlags f;
-    G2_CUDA(cudaMemcpyAsync(&f, flags_.p, sizeof f, cudaMemcpyDeviceToHost, s_));
-    G2_CUDA(cudaStreamSynchronize(s_));
-    if (!f.tie_run) return false;
+    // the flags were staged with the level sizes at split_and_nodes' synchronisation
+    if (!hs_->flags.tie_run) return false;
+    hs_->flags.tie_run = 0;
     G2_CUDA(cudaMemsetAsync(&flags_.p->tie_run, 0, sizeof(int), s_));
     return true;
 }
@@ -284,9 +300,10 @@ void Engine::split_and_nodes(bool with_nodes) {
         dbg_mark(3, s_);
         launch_split(a, uint32_t(n), s_);
         dbg_mark(4, s_);
-        uint32_t ls[kMaxDepth + 3];
-        G2_CUDA(cudaMemcpyAsync(ls, level_start_.p, sizeof ls, cudaMemcpyDeviceToHost, s_));
-        G2_CUDA(cudaStreamSynchronize(s_));
+        uint32_t* ls = hs_->ls;
+        G2_CUDA(cudaMemcpyAsync(ls, level_start_.p, sizeof hs_->ls, cudaMemcpyDeviceToHost, s_));
+        enqueue_flags();
+        sync();
         if (phase_debug() && dbg_ev[0]) {
             float t[4] = {0, 0, 0, 0};
             cudaEventElapsedTime(&t[0], dbg_ev[0], dbg_ev[1]);
@@ -324,10 +341,12 @@ void Engine::refresh(size_t n, const double* mass, const double* pos) {
 }
 
 void Engine::read_events(EventsH& ev) {
-    unsigned long long e[3];
-    G2_CUDA(cudaMemcpyAsync(e, events_.p, sizeof e, cudaMemcpyDeviceToHost, s_));
-    G2_CUDA(cudaStreamSynchronize(s_));
-    ev.interactions = e[0], ev.mac_evals = e[1], ev.list_pushes = e[2];
+    enqueue_events();
+    sync();
+    events_host(ev);
+}
+void Engine::events_host(EventsH& ev) const {
+    ev.interactions = hs_->events[0], ev.mac_evals = hs_->events[1], ev.list_pushes = hs_->events[2];
 }
 
 
@@ -710,12 +729,16 @@ StepResultH Simulation::step() {
     launch_correct(st, sinks_.p, n_active_.p, uint32_t(n), eng_.accum(), t_next_.p, now_, tick_, sd, s);
     G2_CUDA(cudaEventRecord(ev_[6], s));
 
-    unsigned long long tn = 0;
-    uint32_t na = 0;
-    G2_CUDA(cudaMemcpyAsync(&tn, t_next_.p, 8, cudaMemcpyDeviceToHost, s));
-    G2_CUDA(cudaMemcpyAsync(&na, n_active_.p, 4, cudaMemcpyDeviceToHost, s));
-    eng_.read_events(r.events);
-    eng_.check_flags();
+    HostSync* hs = eng_.host_sync();
+    G2_CUDA(cudaMemcpyAsync(&hs->tnext, t_next_.p, 8, cudaMemcpyDeviceToHost, s));
+    G2_CUDA(cudaMemcpyAsync(&hs->na, n_active_.p, 4, cudaMemcpyDeviceToHost, s));
+    eng_.enqueue_events();
+    eng_.enqueue_flags();
+    eng_.sync();
+    eng_.raise_flags();
+    eng_.events_host(r.events);
+    const unsigned long long tn = hs->tnext;
+    const uint32_t na = hs->na;
     r.timings.predict = elapsed(ev_[0], ev_[1]);
     if (rebuild) {
         r.timings.make_tree = elapsed(ev_[1], ev_[2]);

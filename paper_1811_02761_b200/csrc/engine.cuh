@@ -26,6 +26,15 @@ struct EventsH {
     uint64_t interactions = 0, mac_evals = 0, list_pushes = 0;
 };
 
+// pinned host block the step/build boundary read-backs land in (one synchronisation each)
+struct HostSync {
+    DevFlags flags;
+    unsigned long long events[3];
+    unsigned long long tnext;
+    uint32_t na;
+    uint32_t ls[kMaxDepth + 3];
+};
+
 class Engine {
 public:
     Engine(GravParamsH p, EngineConfigH c, int device);
@@ -57,7 +66,14 @@ public:
     // new Morton order of the resident state; returns src (new k <- old position).  rank_cur null:
     // storage-order sort + tie repair (rank_ left stale); else the (key, id) sort via key_by_id.
     const uint32_t* rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur);
-    bool take_tie_overflow();  // syncs; true (and clears) if a tie run was too long for the repair
+    bool take_tie_overflow();  // true (and clears) if a tie run was too long for the repair (staged by split)
+    // boundary read-backs: enqueue copies into the pinned staging block, one sync, then inspect
+    HostSync* host_sync() { return hs_; }
+    void enqueue_flags();
+    void enqueue_events();
+    void sync();
+    void raise_flags();  // throws for the staged device flags
+    void events_host(EventsH& ev) const;
     void ensure_rank();        // rank_ = inverse of perm_ if a storage-order rebuild left it stale
     void split_and_nodes(bool with_nodes);
     void calc_nodes();
@@ -99,6 +115,7 @@ private:
     int device_;
     cudaStream_t s_ = nullptr;
     size_t n_ = 0, cap_ = 0, ncells_ = 0, cell_cap_ = 0;
+    HostSync* hs_ = nullptr;  // pinned
     bool has_tree_ = false;
     bool rank_valid_ = true;  // rank_ matches perm_ (false after a storage-order rebuild)
     uint32_t max_level_width_ = 0;
