@@ -363,3 +363,35 @@ def test_config2_plummer_2e20_block_steps(g2, ref):
                                                                ev_r["list_pushes"])
     err = g2.force_error(s.acc[tg], acc_r[tg])
     assert err["median"] <= MED_TOL and err["p99"] <= P99_TOL, err
+
+
+@pytest.mark.parametrize("leaf_cap,group_size", [(1, 32), (16, 7), (3, 32)])
+def test_simulation_configs_tree_and_forces(g2, ref, leaf_cap, group_size):
+    """Non-default EngineConfig through the Simulation path (storage-order rebuild sort, tie repair,
+    non-recursive split, bottom-up calcNode, walk): after each rebuilding step the tree equals the
+    reference build_tree of that step's positions, and a fresh walk of the evolved state matches the
+    reference (events exact, FP32 tolerance)."""
+    m, p, v = ref.sample_model("m31", 40000, 2)
+    params = g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9)
+    cfg = g2.EngineConfig(leaf_cap=leaf_cap, group_size=group_size)
+    sim = g2.Simulation(g2.ParticleSystem(m, p, v), params, g2.StepScheme(dt_max=1 / 16), cfg)
+    sim.init()
+    sim.set_rebuild_every_step(True)
+    for _ in range(3):
+        sim.step()
+        st, t = sim.system(), sim.tree()
+        rt = ref.build_tree(m, st.pos, leaf_cap=leaf_cap)
+        for k in ("keys", "perm", "rank", "cells", "depth"):
+            assert np.array_equal(getattr(t, k), getattr(rt, k)), k
+    st = sim.system()
+    e = ref.engine(eps=params.eps, dacc=params.dacc, leaf_cap=leaf_cap, group_size=group_size, threads=0)
+    e.build(m, st.pos)
+    acc_r, _, ev_r = e.evaluate(m, st.pos, st.acc_old_mag)
+    s = g2.ParticleSystem(m, st.pos, acc_old_mag=st.acc_old_mag)
+    eng = g2.GravityEngine(params, cfg)
+    eng.build(s)
+    ev = eng.evaluate(s)
+    assert (ev.interactions, ev.mac_evals, ev.list_pushes) == (ev_r["interactions"], ev_r["mac_evals"],
+                                                               ev_r["list_pushes"])
+    err = g2.force_error(s.acc, acc_r)
+    assert err["median"] <= MED_TOL and err["p99"] <= P99_TOL, err
