@@ -9,6 +9,9 @@ constexpr int kWarps = kThreads / 32;
 #ifndef G2_SORT_ITEMS
 #define G2_SORT_ITEMS 8
 #endif
+#ifndef G2_ONESWEEP
+#define G2_ONESWEEP 1  // 1: one kernel per pass with decoupled look-back; 0: count/scan/scatter passes
+#endif
 #ifndef G2_SORT_MINB
 #define G2_SORT_MINB 4
 #endif
@@ -180,6 +183,145 @@ __global__ void __launch_bounds__(kThreads, G2_SORT_MINB) scatter_kernel(const K
     }
 }
 
+// ---- onesweep variant: one kernel per pass.  Global digit bases come from ONE histogram pass
+// over the keys for every digit (order-independent totals); tiles are claimed in order, rank and
+// stage themselves in shared memory (nothing held in registers across the look-back), publish
+// per-digit counts, and each thread (= digit) looks back over 8 predecessor tiles per step.
+constexpr uint32_t kOsAgg = 1u << 30, kOsInc = 2u << 30, kOsMask = (1u << 30) - 1;
+constexpr int kLookWindow = 8;
+
+__device__ __forceinline__ void os_store(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t os_load(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(kThreads) hist_all_kernel(const K* __restrict__ kin, size_t n, int passes,
+                                                            uint32_t* __restrict__ hist) {
+    __shared__ uint32_t h[8][256];
+    for (int i = threadIdx.x; i < 8 * 256; i += kThreads) (&h[0][0])[i] = 0;
+    __syncthreads();
+    for (size_t i = size_t(blockIdx.x) * kThreads + threadIdx.x; i < n; i += size_t(gridDim.x) * kThreads) {
+        const K k = kin[i];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (q < passes) atomicAdd(&h[q][uint32_t(k >> (8 * q)) & 0xffu], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * 256; i += kThreads)
+        if ((&h[0][0])[i]) atomicAdd(&hist[i], (&h[0][0])[i]);
+}
+
+__global__ void __launch_bounds__(kThreads) digit_base_kernel(uint32_t* __restrict__ hist) {
+    __shared__ uint32_t wt[kWarps];
+    uint32_t* row = hist + blockIdx.x * 256;
+    const uint32_t x = row[threadIdx.x];
+    const uint32_t e = block_excl_scan(x, wt, nullptr);
+    row[threadIdx.x] = e;
+}
+
+template <typename K, bool kIdentity>
+__global__ void __launch_bounds__(kThreads, G2_SORT_MINB) onesweep_kernel(const K* __restrict__ kin,
+                                                                          const uint32_t* __restrict__ vin,
+                                                                          K* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                                          size_t n, int shift,
+                                                                          const uint32_t* __restrict__ digit_base,
+                                                                          uint32_t* __restrict__ status,
+                                                                          uint32_t* __restrict__ tile_ctr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    K* skeys = reinterpret_cast<K*>(smem_raw);
+    uint32_t* svals = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K) * kTile);
+    __shared__ uint32_t whist[kWarps][256];
+    __shared__ uint32_t s_lofs[256], s_base[256];
+    __shared__ uint32_t s_wtot[kWarps];
+    __shared__ uint32_t s_tile;
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    for (int i = tid; i < kWarps * 256; i += kThreads) (&whist[0][0])[i] = 0;
+    if (tid == 0) s_tile = atomicAdd(tile_ctr, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const size_t tile_base = size_t(tile) * kTile;
+    const size_t wbase = tile_base + size_t(w) * kWarpItems;
+    uint32_t cnt = 0;
+    {
+        K k[kItems];
+        uint32_t v[kItems], d[kItems], r[kItems];
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const size_t idx = wbase + size_t(i) * 32 + lane;
+            const bool ok = idx < n;
+            k[i] = ok ? kin[idx] : K(0);
+            v[i] = kIdentity ? uint32_t(idx) : (ok ? vin[idx] : 0u);
+            d[i] = ok ? uint32_t((k[i] >> shift) & 0xff) : 256u;
+        }
+        const uint32_t lt_mask = (1u << lane) - 1u;
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            const uint32_t m = __match_any_sync(0xffffffffu, d[i]);
+            const uint32_t before = d[i] < 256u ? whist[w][d[i] & 0xff] : 0u;
+            r[i] = before + __popc(m & lt_mask);
+            __syncwarp();
+            if (d[i] < 256u && lane == __ffs(m) - 1) whist[w][d[i]] = before + __popc(m);
+            __syncwarp();
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ww = 0; ww < kWarps; ++ww) {
+            const uint32_t c = whist[ww][tid];
+            whist[ww][tid] = cnt;
+            cnt += c;
+        }
+        // publish this tile's count of digit tid right away: successors can look past it
+        os_store(status + size_t(tile) * 256 + tid, (tile == 0 ? kOsInc : kOsAgg) | cnt);
+        s_lofs[tid] = block_excl_scan(cnt, s_wtot, nullptr);
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kItems; ++i) {
+            if (d[i] < 256u) {
+                const uint32_t pos = s_lofs[d[i]] + whist[w][d[i]] + r[i];
+                skeys[pos] = k[i];
+                svals[pos] = v[i];
+            }
+        }
+    }
+    // look back for digit tid: kLookWindow predecessors per step, stop at the first inclusive prefix
+    uint32_t excl = 0;
+    if (tile > 0) {
+        int64_t t = int64_t(tile) - 1;
+        bool done = false;
+        while (!done) {
+            uint32_t x[kLookWindow];
+#pragma unroll
+            for (int q = 0; q < kLookWindow; ++q)
+                x[q] = t - q >= 0 ? os_load(status + size_t(t - q) * 256 + tid) : kOsInc;
+#pragma unroll
+            for (int q = 0; q < kLookWindow; ++q) {
+                if (done) break;
+                while ((x[q] >> 30) == 0) x[q] = os_load(status + size_t(t - q) * 256 + tid);
+                excl += x[q] & kOsMask;
+                done = (x[q] >> 30) == 2;
+            }
+            t -= kLookWindow;
+        }
+        os_store(status + size_t(tile) * 256 + tid, kOsInc | (excl + cnt));
+    }
+    s_base[tid] = digit_base[tid] + excl;
+    __syncthreads();
+    const uint32_t tile_n = uint32_t(min(size_t(kTile), n - tile_base));
+    for (uint32_t p = tid; p < tile_n; p += kThreads) {
+        const K kk = skeys[p];
+        const uint32_t dd = uint32_t((kk >> shift) & 0xff);
+        const uint32_t dst = s_base[dd] + (p - s_lofs[dd]);
+        kout[dst] = kk;
+        vout[dst] = svals[p];
+    }
+}
+
 template <typename K>
 void set_smem_attr() {
     static bool done = false;
@@ -187,16 +329,56 @@ void set_smem_attr() {
     const int bytes = int((sizeof(K) + 4) * kTile);
     G2_CUDA(cudaFuncSetAttribute(scatter_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     G2_CUDA(cudaFuncSetAttribute(scatter_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    G2_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    G2_CUDA(cudaFuncSetAttribute(onesweep_kernel<K, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     done = true;
 }
 
 }  // namespace
 
 template <typename K>
+bool radix_sort_onesweep(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, size_t n, int key_bits,
+                         bool identity, SortScratch& sc, cudaStream_t stream) {
+    const int passes = (key_bits + 7) / 8;
+    const uint32_t tiles = uint32_t((n + kTile - 1) / kTile);
+    // scratch: [digit bases: 8 x 256][tile counters: 32][status: passes x tiles x 256]
+    const size_t words = 8 * 256 + 32 + size_t(passes) * tiles * 256;
+    sc.hist.reserve(words);
+    uint32_t* hist = sc.hist.p;
+    uint32_t* ctr = hist + 8 * 256;
+    uint32_t* status = ctr + 32;
+    G2_CUDA(cudaMemsetAsync(hist, 0, words * sizeof(uint32_t), stream));
+    const unsigned hgrid = std::max(1u, std::min<unsigned>(unsigned((n + kThreads * 16 - 1) / (kThreads * 16)), 148u * 8u));
+    G2_COUNT(1), hist_all_kernel<K><<<hgrid, kThreads, 0, stream>>>(keys, n, passes, hist);
+    G2_COUNT(1), digit_base_kernel<<<passes, kThreads, 0, stream>>>(hist);
+    K *ki = keys, *ko = keys_alt;
+    uint32_t *vi = vals, *vo = vals_alt;
+    bool in_alt = false;
+    const int smem = int((sizeof(K) + 4) * kTile);
+    for (int p = 0; p < passes; ++p) {
+        uint32_t* st = status + size_t(p) * tiles * 256;
+        if (p == 0 && identity)
+            G2_COUNT(1), onesweep_kernel<K, true><<<tiles, kThreads, smem, stream>>>(ki, nullptr, ko, vo, n, 8 * p,
+                                                                                    hist + 256 * p, st, ctr + p);
+        else
+            G2_COUNT(1), onesweep_kernel<K, false><<<tiles, kThreads, smem, stream>>>(ki, vi, ko, vo, n, 8 * p,
+                                                                                     hist + 256 * p, st, ctr + p);
+        G2_CUDA(cudaGetLastError());
+        std::swap(ki, ko);
+        std::swap(vi, vo);
+        in_alt = !in_alt;
+    }
+    return in_alt;
+}
+
+template <typename K>
 bool radix_sort_pairs(K* keys, uint32_t* vals, K* keys_alt, uint32_t* vals_alt, size_t n, int key_bits,
                       bool identity, SortScratch& sc, cudaStream_t stream) {
     if (n == 0) return false;
     set_smem_attr<K>();
+#if G2_ONESWEEP
+    return radix_sort_onesweep<K>(keys, vals, keys_alt, vals_alt, n, key_bits, identity, sc, stream);
+#endif
     const int passes = (key_bits + 7) / 8;
     const uint32_t tiles = uint32_t((n + kTile - 1) / kTile);
     const size_t m = size_t(256) * tiles;                       // digit-major (digit, tile) matrix

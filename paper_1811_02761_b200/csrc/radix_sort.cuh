@@ -4,12 +4,15 @@
 // a stable LSD sort from the identity order equals the lexicographic
 // (key, index) pair sort, so keys/perm are bit-identical to the reference.
 //
-// Per 8-bit digit pass: a count kernel writes each 4096-key tile's digit
-// histogram into a digit-major matrix, one single-pass look-back scan turns
-// it into global offsets, and a scatter kernel ranks the tile in shared
-// memory (warp-striped loads, __match_any_sync ranking => stable) and writes
-// digit-contiguous runs.  Traffic per pass: read keys (8 B) for the count,
-// read key+value and write key+value (24 B) for the scatter.
+// Default (G2_ONESWEEP): one kernel reads the keys once for the global
+// histograms of every 8-bit digit; each pass is then ONE kernel: 2048-key
+// tiles claimed in order rank their keys in shared memory (warp-striped loads,
+// __match_any_sync ranking => stable), stage the ranked tile in shared memory,
+// publish per-digit tile counts and look back over 8 predecessor tiles per step
+// (decoupled look-back per digit) for their global offsets, then write
+// digit-contiguous runs.  The alternative is a count kernel, one look-back scan
+// over the (digit, tile) matrix and a scatter kernel per pass.  Traffic per
+// pass: read key+value and write key+value (24 B per pair for 64-bit keys).
 #pragma once
 
 #include "common.cuh"
