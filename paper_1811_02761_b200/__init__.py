@@ -8,9 +8,9 @@ from .gravitree import (DataError, Diagnostics, EngineConfig, GravityEngine, Gra
                         ResourceError, Simulation, SingularityError, StepResult, StepScheme, TraversalEvents,
                         TunerConfig, block_level, compute_diagnostics, count_walk_ops, direct_sum, flops_estimate,
                         force_error, read_snapshot, write_snapshot, Snapshot,
-                        nccl_unique_id, predict, walk_flops)
+                        nccl_unique_id, predict, predict_speedup, walk_flops)
 
 __all__ = ["DataError", "Diagnostics", "EngineConfig", "GravityEngine", "GravParams", "InternalError", "ParticleSystem",
            "ResourceError", "Simulation", "SingularityError", "StepResult", "StepScheme", "TraversalEvents",
            "TunerConfig", "block_level", "compute_diagnostics", "count_walk_ops", "direct_sum", "flops_estimate", "force_error",
-           "nccl_unique_id", "predict", "walk_flops", "read_snapshot", "write_snapshot", "Snapshot"]
+           "nccl_unique_id", "predict", "predict_speedup", "walk_flops", "read_snapshot", "write_snapshot", "Snapshot"]

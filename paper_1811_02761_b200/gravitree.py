@@ -556,6 +556,15 @@ def flops_estimate(ev: TraversalEvents, elapsed_seconds: float) -> float:
     return walk_flops(ev) / elapsed_seconds
 
 
+def predict_speedup(ops: dict, peak_ratio: float = 1.5) -> float:
+    """predict_speedup (op_counters.cpp:7-12): peak_ratio * (I + F) / max(I, F), F = fma + add + mul."""
+    f = float(ops["fp_fma"] + ops["fp_add"] + ops["fp_mul"])
+    i = float(ops["integer"])
+    if f == 0.0 and i == 0.0:
+        raise DataError("predict_speedup: no counted instructions")
+    return peak_ratio * (i + f) / max(i, f)
+
+
 def force_error(acc, ref) -> dict:
     """Nearest-rank relative-error statistics (gravity.cpp:67-90)."""
     acc, ref = np.asarray(acc, np.float64), np.asarray(ref, np.float64)
