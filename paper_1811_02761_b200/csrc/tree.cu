@@ -515,6 +515,78 @@ __device__ __forceinline__ void store_node(WNode* __restrict__ nodes, WNode32* _
     nodes32[c] = WNode32{float(nd.cx), float(nd.cy), float(nd.cz), fm, fb, fm * fb * fb, nd.link, nd.info};
 }
 
+// internal cell from its (at most 8) children in order (octree.cpp:145-162).  All children
+// are loaded up front: one memory round trip per cell instead of two dependent chains of cc.
+__device__ __forceinline__ WNode internal_node(const WNode* nodes, uint32_t f, uint32_t cc, uint8_t dep) {
+    double qx[8], qy[8], qz[8], qm[8], qe[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cc)) {
+            const double2* q = reinterpret_cast<const double2*>(nodes + f + j);
+            const double2 a = q[0], b = q[1], e = q[2];
+            qx[j] = a.x, qy[j] = a.y, qz[j] = b.x, qm[j] = b.y, qe[j] = e.x;
+        }
+    WNode nd;
+    double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cc)) {
+            m = dadd(m, qm[j]);
+            wx = dadd(wx, dmul(qm[j], qx[j]));
+            wy = dadd(wy, dmul(qm[j], qy[j]));
+            wz = dadd(wz, dmul(qm[j], qz[j]));
+        }
+    const double inv = ddiv(1.0, m);
+    nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+    double ext = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cc))
+            ext = smax(ext, dadd(dsqrt(norm2(dsub(qx[j], nd.cx), dsub(qy[j], nd.cy), dsub(qz[j], nd.cz))), qe[j]));
+    nd.extent = ext;
+    nd.link = f;
+    nd.info = cc | (uint32_t(dep) << 8);  // depth feeds the frontier-cap check
+    nd.mass = m;
+    return nd;
+}
+
+// a leaf of at most 8 particles, same operation order as the general loop below
+__device__ __forceinline__ void leaf_small(const double4* __restrict__ xyzm, uint32_t f, uint32_t cnt, uint32_t c,
+                                           WNode* __restrict__ nodes, WNode32* __restrict__ nodes32,
+                                           float4* __restrict__ rel, uint32_t* __restrict__ leaf_of) {
+    double4 p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cnt)) p[j] = xyzm[f + j];
+    WNode nd;
+    double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cnt)) {
+            m = dadd(m, p[j].w);
+            wx = dadd(wx, dmul(p[j].w, p[j].x));
+            wy = dadd(wy, dmul(p[j].w, p[j].y));
+            wz = dadd(wz, dmul(p[j].w, p[j].z));
+        }
+    const double inv = ddiv(1.0, m);
+    nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+    const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
+    double e2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cnt)) {
+            e2 = smax(e2, norm2(dsub(p[j].x, nd.cx), dsub(p[j].y, nd.cy), dsub(p[j].z, nd.cz)));
+            rel[f + j] = make_float4(float(dsub(p[j].x, c32x)), float(dsub(p[j].y, c32y)), float(dsub(p[j].z, c32z)),
+                                     float(p[j].w));
+            leaf_of[f + j] = c;
+        }
+    nd.extent = dsqrt(e2);
+    nd.link = f;
+    nd.info = cnt | kLeafBit;
+    nd.mass = m;
+    store_node(nodes, nodes32, c, nd);
+}
+
 __global__ void __launch_bounds__(kBlock) calc_leaf_kernel(const double4* __restrict__ xyzm,
                                                            const uint32_t* __restrict__ child_count,
                                                            const uint32_t* __restrict__ first,
@@ -525,9 +597,13 @@ __global__ void __launch_bounds__(kBlock) calc_leaf_kernel(const double4* __rest
     const uint32_t total = level_start[kMaxDepth + 1];
     for (uint32_t c = blockIdx.x * kBlock + threadIdx.x; c < total; c += gridDim.x * kBlock) {
         if (child_count[c]) continue;
+        const uint32_t f = first[c], k1 = f + count[c];
+        if (k1 - f <= 8) {  // the usual leaf: every particle loaded up front, one memory round trip
+            leaf_small(xyzm, f, k1 - f, c, nodes, nodes32, rel, leaf_of);
+            continue;
+        }
         WNode nd;
         double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
-        const uint32_t f = first[c], k1 = f + count[c];
         for (uint32_t k = f; k < k1; ++k) {
             const double4 p = xyzm[k];
             m = dadd(m, p.w);
@@ -563,28 +639,26 @@ __global__ void __launch_bounds__(kBlock) calc_internal_kernel(const uint32_t* _
     for (uint32_t c = b + blockIdx.x * kBlock + threadIdx.x; c < e; c += gridDim.x * kBlock) {
         const uint32_t cc = child_count[c];
         if (!cc) continue;
-        WNode nd;
-        double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
-        const uint32_t f = first_child[c];
-        for (uint32_t ch = f; ch < f + cc; ++ch) {
-            const WNode q = nodes[ch];
-            m = dadd(m, q.mass);
-            wx = dadd(wx, dmul(q.mass, q.cx));
-            wy = dadd(wy, dmul(q.mass, q.cy));
-            wz = dadd(wz, dmul(q.mass, q.cz));
+        store_node(nodes, nodes32, c, internal_node(nodes, first_child[c], cc, depth[c]));
+    }
+}
+
+// the narrow top levels (each at most kTopCells wide) in ONE block, levels separated by
+// __syncthreads instead of a launch each
+constexpr uint32_t kTopCells = 512;
+constexpr int kTopThreads = 512;
+__global__ void __launch_bounds__(kTopThreads, 1) calc_top_kernel(const uint32_t* __restrict__ first_child,
+                                                               const uint32_t* __restrict__ child_count,
+                                                               const uint8_t* __restrict__ depth,
+                                                               const uint32_t* __restrict__ level_start, WNode* nodes,
+                                                               WNode32* __restrict__ nodes32, int dtop) {
+    for (int d = dtop; d >= 0; --d) {
+        const uint32_t b = level_start[d], e = level_start[d + 1];
+        for (uint32_t c = b + threadIdx.x; c < e; c += kTopThreads) {
+            const uint32_t cc = child_count[c];
+            if (cc) store_node(nodes, nodes32, c, internal_node(nodes, first_child[c], cc, depth[c]));
         }
-        const double inv = ddiv(1.0, m);
-        nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
-        double ext = 0.0;
-        for (uint32_t ch = f; ch < f + cc; ++ch) {
-            const WNode q = nodes[ch];
-            ext = smax(ext, dadd(dsqrt(norm2(dsub(q.cx, nd.cx), dsub(q.cy, nd.cy), dsub(q.cz, nd.cz))), q.extent));
-        }
-        nd.extent = ext;
-        nd.link = f;
-        nd.info = cc | (uint32_t(depth[c]) << 8);  // depth feeds the frontier-cap check
-        nd.mass = m;
-        store_node(nodes, nodes32, c, nd);
+        __syncthreads();  // level d complete (and visible to the block) before level d - 1 reads it
     }
 }
 
@@ -726,12 +800,20 @@ void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const ui
                       uint32_t* leaf_of, cudaStream_t s) {
     const size_t total = level_start_host[kMaxDepth + 1];
     G2_COUNT(1), calc_leaf_kernel<<<grid_for(total), kBlock, 0, s>>>(xyzm, child_count, first, count, level_start,
-                                                                      nodes, nodes32, rel, leaf_of);
+                                                                          nodes, nodes32, rel, leaf_of);
     int deepest = 0;  // the deepest non-empty level holds leaves only
     for (int d = 0; d <= kMaxDepth; ++d)
         if (level_start_host[d + 1] > level_start_host[d]) deepest = d;
+    static const bool levels = std::getenv("G2_CALC_LEVELS") != nullptr;  // development: launch per level A/B
     for (int d = deepest - 1; d >= 0; --d) {
         const size_t w = level_start_host[d + 1] - level_start_host[d];
+        bool top = !levels;
+        for (int u = d; u >= 0 && top; --u) top = level_start_host[u + 1] - level_start_host[u] <= kTopCells;
+        if (top) {
+            G2_COUNT(1), calc_top_kernel<<<1, kTopThreads, 0, s>>>(first_child, child_count, depth, level_start, nodes,
+                                                                   nodes32, d);
+            break;
+        }
         G2_COUNT(1), calc_internal_kernel<<<grid_for(w), kBlock, 0, s>>>(first_child, child_count, depth, level_start,
                                                                           nodes, nodes32, d);
     }

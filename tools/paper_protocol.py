@@ -13,10 +13,13 @@ sim.init()
 if fixed:
     sim.set_fixed_rebuild_interval(fixed)
 tot = 0.0
+ph = dict(walk_tree=0.0, calc_node=0.0, make_tree=0.0, predict=0.0, correct=0.0)
 for k in range(steps):
     r = sim.step()
     t = r.timings
     tot += t.total()
+    for key in ph:
+        ph[key] += getattr(t, key)
     print(f"{k:3d} act {r.active/n:6.3f} rebuilt {int(r.rebuilt)} interval {r.rebuild_interval:3d} walk {t.walk_tree*1e3:8.2f} ms "
           f"build {(t.make_tree+t.calc_node)*1e3:6.2f} ms int/active {r.events.interactions/max(r.active,1):9.0f}", flush=True)
-print(f"mean device s/step {tot/steps:.4f}")
+print(f"mean device s/step {tot/steps:.5f}  " + " ".join(f"{k} {v/steps*1e3:.3f}ms" for k, v in ph.items()))
