@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--cpu-sample", type=int, default=0, help="walk 1 of every S groups on the CPU (0: auto)")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper-protocol block-step run")
     ap.add_argument("--paper-steps", type=int, default=32)
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-GPU acceleration exchange: fused walk-epilogue P2P stores, or ncclAllGather")
     return ap.parse_args()
 
 
@@ -204,10 +206,28 @@ def workload_config(args):
     return {"workload": f"{args.model} N={args.n} all-active full step (predict+makeTree+calcNode+walkTree+correct, "
                         f"rebuild every step)", "model": args.model, "n": args.n, "dacc": DACC, "eps": EPS,
             "leaf_cap": 8, "group_size": 32, "parallelism": f"groups sharded over {dist_env()[1]} GPU(s)",
+            "exchange": ("none" if dist_env()[1] == 1 else
+                         "fused: walk-epilogue P2P stores into peer accumulators (CUDA IPC)"
+                         if getattr(args, "exchange", "p2p") == "p2p" else "ncclAllGather"),
             "l2": "no flush: the resident state (~1 GB at 2^23) exceeds the 126 MB L2"}
 
 
 # ------------------------------------------------------------------------- g2 arm
+def join_mesh(args, g2, sim, rank, world):
+    """Shard the sink groups over the ranks.  p2p (default): the fused exchange -- the walk
+    kernel stores each finished group's accelerations into every peer's buffer over NVLink
+    (CUDA IPC handles all-gathered once at setup); nccl: one ncclAllGather per step."""
+    import torch.distributed as dist
+    if args.exchange == "p2p":
+        handles = [None] * world
+        dist.all_gather_object(handles, sim.p2p_export(rank, world))
+        sim.set_mesh_p2p(rank, world, handles)
+    else:
+        uid = [g2.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        sim.set_mesh(rank, world, uid[0])
+
+
 def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world):
     """The paper-comparable block-step protocol: reference defaults
     (eta 0.5, adaptive levels) with dt_max = 1, timed over `paper_steps` steps after init and
@@ -224,10 +244,7 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world):
         sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), params, g2.StepScheme(eta=0.5, dt_max=1.0),
                             g2.EngineConfig(), device=local)
         if world > 1:
-            import torch.distributed as dist
-            uid = [g2.nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(uid, src=0)
-            sim.set_mesh(rank, world, uid[0])
+            join_mesh(args, g2, sim, rank, world)
         sim.init()
         if fixed:
             sim.set_fixed_rebuild_interval(fixed)
@@ -279,10 +296,7 @@ def run_g2(args):
     sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), params, scheme, g2.EngineConfig(), device=local)
     sim.set_rebuild_every_step(True)
     if world > 1:
-        import torch.distributed as dist
-        uid = [g2.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        sim.set_mesh(rank, world, uid[0])
+        join_mesh(args, g2, sim, rank, world)
     t0 = time.perf_counter()
     sim.init()
     t_init = time.perf_counter() - t0

@@ -194,6 +194,16 @@ int g2_sim_set_mesh(g2_sim* s, int rank, int world, const unsigned char id[128])
 /* in-process mesh: sims[0..world) (one host thread per step call, any devices)
  * shard the sink groups and exchange accelerations by device copies */
 int g2_sim_set_mesh_local(g2_sim** sims, int world);
+/* fused peer exchange, no collective: the walk kernel stores each finished sink
+ * group's accelerations straight into every peer's accumulator (NVLink P2P stores
+ * through CUDA IPC mappings), then device flags order them before the correct.
+ * Every rank exports g2_p2p_handle_bytes() bytes, the handles of all ranks are
+ * exchanged out of band (rank order), then each rank opens its peers'. 2 <= world <= 8. */
+size_t g2_p2p_handle_bytes(void);
+int g2_sim_p2p_export(g2_sim* s, int rank, int world, void* handle);
+int g2_sim_set_mesh_p2p(g2_sim* s, int rank, int world, const void* handles);
+/* the same fused exchange between Simulations of one process (any devices with peer access) */
+int g2_sim_set_mesh_local_p2p(g2_sim** sims, int world);
 
 #ifdef __cplusplus
 }

@@ -186,11 +186,92 @@ struct LocalExchange final : ShardExchange {
     }
 };
 
+// ---- fused peer exchange (SURVEY §8e "fused-collective option") -----------------
+// No collective at all: the walk kernel itself stores every finished group's
+// accumulators into each peer rank's accumulator buffer (NVLink P2P stores through
+// IPC-mapped pointers, or plain device pointers for an in-process mesh), overlapped
+// with the rest of the walk.  Then one signal/wait pair on device flags (release /
+// acquire at system scope) orders those stores before the peers' correct.
+// Accumulators are double-buffered by step parity: a rank can only start pushing
+// step k + 2 after every rank finished walking step k + 1, hence after every rank's
+// correct of step k read the buffer; the zero pass touches only the own shard.
+struct PeerFlags {
+    uint64_t* f[g2::kMaxPeers];
+};
+
+__global__ void peer_signal_kernel(PeerFlags peers, int world, int self, uint64_t epoch) {
+    const int q = threadIdx.x;
+    __threadfence_system();
+    if (q < world)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peers.f[q] + self), "l"(epoch) : "memory");
+}
+
+__global__ void peer_wait_kernel(const uint64_t* flags, int world, uint64_t epoch) {
+    const int q = threadIdx.x;
+    if (q < world) {
+        uint64_t v;
+        do {
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
+            if (v < epoch) __nanosleep(200);
+        } while (v < epoch);
+    }
+    __syncwarp();
+    __threadfence_system();
+}
+
+struct PeerExchange final : g2::Exchange {
+    int world = 1, self = 0;
+    uint64_t epoch = 0;
+    float4* buf[2] = {};                        // own accumulators (exported)
+    uint64_t* flags = nullptr;                  // own arrival flags [kMaxPeers] (exported)
+    float4* pbuf[g2::kMaxPeers][2] = {};        // every rank's accumulators as seen from here
+    uint64_t* pflags[g2::kMaxPeers] = {};
+    std::vector<void*> opened;                  // IPC mappings to close
+    int device = 0;
+
+    void alloc(g2::Simulation& sim, int w, int r) {
+        world = w, self = r;
+        device = sim.engine().device();
+        G2_CUDA(cudaSetDevice(device));
+        const size_t slots = sim.n() + 64 * sim.group_size();
+        for (auto& b : buf) {
+            G2_CUDA(cudaMalloc(&b, slots * sizeof(float4)));
+            G2_CUDA(cudaMemset(b, 0, slots * sizeof(float4)));
+        }
+        G2_CUDA(cudaMalloc(&flags, g2::kMaxPeers * sizeof(uint64_t)));
+        G2_CUDA(cudaMemset(flags, 0, g2::kMaxPeers * sizeof(uint64_t)));
+        pbuf[self][0] = buf[0], pbuf[self][1] = buf[1], pflags[self] = flags;
+    }
+    ~PeerExchange() override {
+        for (void* p : opened) cudaIpcCloseMemHandle(p);
+        for (auto& b : buf)
+            if (b) cudaFree(b);
+        if (flags) cudaFree(flags);
+    }
+    void before_walk(g2::Simulation& sim) override {
+        const int par = int(epoch & 1);
+        float4* peers[g2::kMaxPeers] = {};
+        for (int q = 0; q < world; ++q) peers[q] = pbuf[q][par];
+        sim.engine().set_peer_push(world, self, buf[par], peers);
+    }
+    void allgather_acc(g2::Simulation& sim) override {
+        ++epoch;
+        cudaStream_t s = sim.engine().stream();
+        PeerFlags pf{};
+        for (int q = 0; q < world; ++q) pf.f[q] = pflags[q];
+        G2_COUNT(1), peer_signal_kernel<<<1, 32, 0, s>>>(pf, world, self, epoch);
+        G2_COUNT(1), peer_wait_kernel<<<1, 32, 0, s>>>(flags, world, epoch);
+        G2_CUDA(cudaGetLastError());
+    }
+};
+constexpr size_t kP2PHandleBytes = 3 * sizeof(cudaIpcMemHandle_t);
+
 }  // namespace
 
 struct g2_sim {
     std::unique_ptr<g2::Simulation> s;
-    std::unique_ptr<ShardExchange> ex;
+    std::unique_ptr<g2::Exchange> ex;
+    std::unique_ptr<PeerExchange> pending;  // exported, peers not opened yet
 };
 
 
@@ -527,6 +608,73 @@ int g2_sim_set_mesh(g2_sim* s, int rank, int world, const unsigned char id[128])
         ex->prepare(*s->s);
         s->s->set_shard(rank, world, ex.get());
         s->ex = std::move(ex);
+    });
+}
+
+size_t g2_p2p_handle_bytes(void) { return kP2PHandleBytes; }
+
+int g2_sim_p2p_export(g2_sim* s, int rank, int world, void* handle) {
+    return guarded([&] {
+        if (world < 2 || world > g2::kMaxPeers || rank < 0 || rank >= world)
+            throw g2::Error(G2_DATA_ERROR, "p2p_export: bad rank/world (2 <= world <= 8)");
+        auto ex = std::make_unique<PeerExchange>();
+        ex->alloc(*s->s, world, rank);
+        auto* h = static_cast<cudaIpcMemHandle_t*>(handle);
+        G2_CUDA(cudaIpcGetMemHandle(&h[0], ex->buf[0]));
+        G2_CUDA(cudaIpcGetMemHandle(&h[1], ex->buf[1]));
+        G2_CUDA(cudaIpcGetMemHandle(&h[2], ex->flags));
+        s->pending = std::move(ex);
+    });
+}
+
+int g2_sim_set_mesh_p2p(g2_sim* s, int rank, int world, const void* handles) {
+    return guarded([&] {
+        PeerExchange* ex = s->pending.get();
+        if (!ex || ex->world != world || ex->self != rank)
+            throw g2::Error(G2_DATA_ERROR, "set_mesh_p2p: call g2_sim_p2p_export with the same rank/world first");
+        const auto* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+        G2_CUDA(cudaSetDevice(ex->device));
+        for (int q = 0; q < world; ++q) {
+            if (q == rank) continue;
+            void* p[3];
+            for (int k = 0; k < 3; ++k) {
+                G2_CUDA(cudaIpcOpenMemHandle(&p[k], h[3 * q + k], cudaIpcMemLazyEnablePeerAccess));
+                ex->opened.push_back(p[k]);
+            }
+            ex->pbuf[q][0] = static_cast<float4*>(p[0]), ex->pbuf[q][1] = static_cast<float4*>(p[1]);
+            ex->pflags[q] = static_cast<uint64_t*>(p[2]);
+        }
+        s->s->set_shard(rank, world, ex);
+        s->ex = std::move(s->pending);
+    });
+}
+
+int g2_sim_set_mesh_local_p2p(g2_sim** sims, int world) {
+    return guarded([&] {
+        if (world < 2 || world > g2::kMaxPeers) throw g2::Error(G2_DATA_ERROR, "set_mesh_local_p2p: 2 <= world <= 8");
+        std::vector<PeerExchange*> ex(world);
+        for (int r = 0; r < world; ++r) {
+            auto e = std::make_unique<PeerExchange>();
+            e->alloc(*sims[r]->s, world, r);
+            ex[r] = e.get();
+            sims[r]->ex = std::move(e);
+        }
+        for (int r = 0; r < world; ++r) {
+            for (int q = 0; q < world; ++q) {
+                ex[r]->pbuf[q][0] = ex[q]->buf[0], ex[r]->pbuf[q][1] = ex[q]->buf[1];
+                ex[r]->pflags[q] = ex[q]->flags;
+                if (ex[q]->device != ex[r]->device) {
+                    int ok = 0;
+                    G2_CUDA(cudaDeviceCanAccessPeer(&ok, ex[r]->device, ex[q]->device));
+                    if (!ok) throw g2::Error(G2_INTERNAL, "set_mesh_local_p2p: devices without peer access");
+                    cudaSetDevice(ex[r]->device);
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(ex[q]->device, 0);
+                    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) G2_CUDA(e);
+                    cudaGetLastError();
+                }
+            }
+            sims[r]->s->set_shard(r, world, ex[r]);
+        }
     });
 }
 

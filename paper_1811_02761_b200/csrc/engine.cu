@@ -365,7 +365,13 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     b.n_sinks = n_sinks_dev;
     b.groups = groups_.p;
     b.n_groups = n_groups_.p;
-    b.accum = accum_.p;
+    b.accum = accum();
+    b.world = peer_world_, b.self = peer_self_;
+    if (peer_world_ > 1) {
+        gpend_.reserve(ng_cap + 1);
+        b.gpend = gpend_.p;
+        for (int q = 0; q < kMaxPeers; ++q) b.peer_accum[q] = peer_accum_[q];
+    }
     b.events = events_.p;
     b.queue = queue_.p;
     b.batch = batch_.p;
@@ -391,7 +397,7 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
     WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
                   c_.count_ops ? 1 : 0, 0};
-    launch_walk(tv, wp, b, with_pot, n_sinks_cap, flags_.p, s_);
+    launch_walk(tv, wp, b, with_pot, n_sinks_cap, gs, flags_.p, s_);
     if (check)
         G2_COUNT(1), frontier_check_kernel<<<gridn(size_t(ng_cap) * (kMaxDepth + 1)), kB, 0, s_>>>(
             level_count_.p, size_t(ng_cap) * (kMaxDepth + 1), uint32_t(std::min<size_t>(cap, 0xffffffffu)),
@@ -722,11 +728,13 @@ StepResultH Simulation::step() {
     }
     shard_lo_ = lo, shard_hi_ = hi;
     const bool sharded = world_ > 1 && exchange_;
+    if (sharded) exchange_->before_walk(*this);
     eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false, lo, hi, false);
     G2_CUDA(cudaEventRecord(ev_[4], s));
     if (sharded) exchange_->allgather_acc(*this);  // every rank receives every group's accelerations
     G2_CUDA(cudaEventRecord(ev_[5], s));
     launch_correct(st, sinks_.p, n_active_.p, uint32_t(n), eng_.accum(), t_next_.p, now_, tick_, sd, s);
+    if (sharded) eng_.set_peer_push(1, 0, nullptr, nullptr);  // other walks (init, evaluate) stay local
     G2_CUDA(cudaEventRecord(ev_[6], s));
 
     HostSync* hs = eng_.host_sync();

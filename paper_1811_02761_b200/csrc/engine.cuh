@@ -83,7 +83,14 @@ public:
                  bool with_pot, bool sync_events, uint32_t group_lo = 0, uint32_t group_hi = ~0u,
                  bool finalize = true);
     // accum slots -> FP64 accelerations at the sinks' sorted positions
-    float4* accum() { return accum_.p; }
+    int device() const { return device_; }
+    float4* accum() { return accum_ext_ ? accum_ext_ : accum_.p; }
+    // fused peer exchange for the next walks: accumulate into `accum` (an exported buffer) and
+    // push finished groups to `peers` (world entries, [self] unused); world <= 1 turns it off
+    void set_peer_push(int world, int self, float4* accum, float4* const* peers) {
+        peer_world_ = world, peer_self_ = self, accum_ext_ = world > 1 ? accum : nullptr;
+        for (int q = 0; q < kMaxPeers; ++q) peer_accum_[q] = world > 1 && q < world ? peers[q] : nullptr;
+    }
     size_t accum_cap() const { return accum_.cap; }
     void reserve_accum(size_t slots) { accum_.reserve(slots); }
     void direct_sum_orig(const double4* xyzm_orig, size_t n, double* ax, double* ay, double* az);
@@ -140,6 +147,10 @@ private:
     DBuf<uint32_t> sinks_, sinks_alt_, n_sinks_, n_groups_;
     DBuf<GroupRec> groups_;
     DBuf<float4> accum_;
+    DBuf<uint32_t> gpend_;
+    float4* accum_ext_ = nullptr;
+    float4* peer_accum_[kMaxPeers] = {};
+    int peer_world_ = 1, peer_self_ = 0;
     DBuf<unsigned long long> events_;
     DBuf<uint64_t> queue_;
     DBuf<uint32_t> batch_;
@@ -204,6 +215,7 @@ struct StepResultH {
 // groups; the exchange makes all ranks hold all of them (one all-gather).
 struct Exchange {
     virtual ~Exchange() = default;
+    virtual void before_walk(class Simulation&) {}  // e.g. point the walk at this step's exchange buffers
     virtual void allgather_acc(class Simulation& sim) = 0;
 };
 

@@ -87,6 +87,7 @@ struct WalkParams {
     int count_ops;
     int force_geometric;      // 1: geometric MAC for every group
 };
+constexpr int kMaxPeers = 8;
 struct WalkBuffers {
     const uint32_t* sinks;    // [n_sinks] sorted particle indices
     const uint32_t* n_sinks;  // device scalar
@@ -106,13 +107,18 @@ struct WalkBuffers {
     uint32_t* trace_n;
     uint32_t trace_cap;
     uint32_t group_lo, group_hi;  // shard of groups to walk (hi = ~0u: all)
+    // fused peer exchange (world > 1): the task that completes a group stores the group's final
+    // accumulators straight into every peer rank's accumulator (IPC-mapped, same slot layout)
+    uint32_t* gpend;                    // [n_groups] tasks of the group not yet written out
+    float4* peer_accum[kMaxPeers];      // peer accumulators, [self] unused
+    int world, self;
 };
 size_t walk_spill_words();
 size_t walk_resident_warps();
 void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffers& b, uint32_t group_size,
                    uint32_t n_sinks_cap, cudaStream_t s);
 void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
-                 DevFlags* flags, cudaStream_t s);
+                 uint32_t group_size, DevFlags* flags, cudaStream_t s);
 // acc_out/pot_out in sorted order for the sinks (FP64)
 void launch_walk_finalize(const WalkBuffers& b, uint32_t n_sinks_cap, double* ax, double* ay, double* az,
                           double* pot, cudaStream_t s);

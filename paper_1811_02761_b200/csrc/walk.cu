@@ -380,6 +380,23 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 atomicAdd(&out->z, G * ((z0 + z1) + (w0 + w1)));
                 if (kPot) atomicAdd(&out->w, G * (a0.ph + a1.ph));
             }
+            if ((fl & kLast) && b.world > 1) {
+                // the group's last task to finish pushes its final accumulators to every peer
+                // rank (NVLink stores, overlapped with the rest of the walk)
+                __threadfence();
+                __syncwarp();
+                uint32_t last = 0;
+                if (lane == 0) last = atomicSub(&b.gpend[grp], 1u) == 1u;
+                if (__shfl_sync(kFull, last, 0)) {
+                    __threadfence();
+                    if (has_sink) {
+                        const float4 v = __ldcg(&b.accum[gfirst + lane]);
+                        for (int q = 0; q < b.world; ++q)
+                            if (q != b.self) b.peer_accum[q][gfirst + lane] = v;
+                        __threadfence_system();
+                    }
+                }
+            }
         }
         return;
     }
@@ -700,6 +717,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                         k = min(live / 2, 32);
                         k = gtop == gbase ? min(k, ssize) : min(k, gtop - gbase);
                         atomicAdd(q_pending, 1u);
+                        if (b.world > 1) atomicAdd(&b.gpend[grp], 1u);  // before the batch is visible
                         // wait for the slot's previous occupant to be consumed (ring of 2^20)
                         while (ld_vol64(&b.queue[ds & (kRing - 1)]) != kEmpty) __nanosleep(64);
                     }
@@ -802,7 +820,10 @@ __global__ void __launch_bounds__(256) groups_kernel(TreeView t, const double* _
         double r2 = on ? norm2(dsub(q.x, cx), dsub(q.y, cy), dsub(q.z, cz)) : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r2 = smax(r2, __shfl_xor_sync(kFull, r2, o));
-        if (lane == 0) b.groups[g] = GroupRec{cx, cy, cz, dsqrt(r2), am, first, cnt};
+        if (lane == 0) {
+            b.groups[g] = GroupRec{cx, cy, cz, dsqrt(r2), am, first, cnt};
+            if (b.world > 1) b.gpend[g] = 1u;  // the initial task
+        }
     }
 }
 
@@ -819,9 +840,11 @@ __global__ void walk_init_kernel(WalkBuffers b) {
     }
 }
 
-__global__ void zero_accum_kernel(float4* accum, const uint32_t* n_sinks, uint32_t cap) {
-    const uint32_t n = min(*n_sinks, cap);
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+// zero the accumulator slots this launch accumulates into: all sinks, or with a peer exchange
+// only the own shard's slots (the other slots are written by the peers, possibly already)
+__global__ void zero_accum_kernel(float4* accum, const uint32_t* n_sinks, uint32_t cap, uint32_t lo, uint32_t hi) {
+    const uint32_t n = min(min(*n_sinks, cap), hi);
+    for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         accum[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
@@ -879,9 +902,14 @@ void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffe
 }
 
 void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
-                 DevFlags* flags, cudaStream_t s) {
+                 uint32_t gs, DevFlags* flags, cudaStream_t s) {
     const unsigned zb = std::max(1u, std::min<unsigned>(ceil_div(n_sinks_cap, 256), kNumSMs * 8));
-    G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap);
+    uint32_t zlo = 0, zhi = ~0u;
+    if (b.world > 1) {
+        zlo = uint32_t(std::min<uint64_t>(uint64_t(b.group_lo) * gs, ~0u));
+        zhi = uint32_t(std::min<uint64_t>(uint64_t(b.group_hi) * gs, ~0u));
+    }
+    G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi);
     G2_COUNT(1), walk_init_kernel<<<1, 32, 0, s>>>(b);
     const bool eps0 = p.eps == 0.0;
     const bool check = b.level_count != nullptr;

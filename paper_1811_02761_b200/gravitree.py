@@ -79,6 +79,7 @@ def _load():
     lib = C.CDLL(LIB_PATH)
     lib.g2_last_error.restype = C.c_char_p
     lib.g2_engine_has_tree.restype = C.c_int
+    lib.g2_p2p_handle_bytes.restype = C.c_size_t
     return lib
 
 
@@ -434,6 +435,27 @@ class Simulation:
         device copies; step the sims concurrently (one Python thread each)."""
         arr = (C.c_void_p * len(sims))(*[s._h.value for s in sims])
         _chk(_lib.g2_sim_set_mesh_local(arr, C.c_int(len(sims))))
+
+    def p2p_export(self, rank: int, world: int) -> bytes:
+        """Fused peer exchange, step 1: allocate this rank's exchange buffers and return their
+        CUDA IPC handles; gather every rank's handles (rank order) out of band."""
+        buf = (C.c_ubyte * _lib.g2_p2p_handle_bytes())()
+        _chk(_lib.g2_sim_p2p_export(self._h, C.c_int(rank), C.c_int(world), buf))
+        return bytes(buf)
+
+    def set_mesh_p2p(self, rank: int, world: int, handles):
+        """Fused peer exchange, step 2: map the peers' buffers.  The walk then stores each
+        finished group's accelerations straight into every peer (no collective)."""
+        blob = b"".join(handles)
+        buf = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _chk(_lib.g2_sim_set_mesh_p2p(self._h, C.c_int(rank), C.c_int(world), buf))
+
+    @staticmethod
+    def set_mesh_local_p2p(sims):
+        """In-process mesh with the fused peer exchange (the walk pushes into the other sims'
+        accumulators); step the sims concurrently (one Python thread each)."""
+        arr = (C.c_void_p * len(sims))(*[s._h.value for s in sims])
+        _chk(_lib.g2_sim_set_mesh_local_p2p(arr, C.c_int(len(sims))))
 
 
 def nccl_unique_id() -> bytes:

@@ -1,10 +1,15 @@
 """GPU: the sharded multi-rank step on one device.
 
-Ranks shard the sink groups and exchange accelerations through the same
-window/unpack path the NCCL mesh uses (LocalExchange transport).  The
+Ranks shard the sink groups and exchange accelerations either through the
+window/unpack path the NCCL mesh uses (LocalExchange transport) or through the
+fused peer exchange (the walk kernel stores finished groups into the peers'
+accumulators; in-process pointers, or CUDA IPC between two processes).  The
 sharded run must equal the single-rank run: identical trees (redundant,
 deterministic builds), summed events identical, accelerations equal to
 FP32 summation-order tolerance."""
+import os
+import subprocess
+import sys
 import threading
 
 import numpy as np
@@ -13,8 +18,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_steps_match_single_rank(world):
+@pytest.mark.parametrize("world,mesh", [(2, "copy"), (3, "copy"), (2, "p2p"), (3, "p2p")])
+def test_sharded_steps_match_single_rank(world, mesh):
     import paper_1811_02761_b200 as g2
     from paper_1811_02761_b200.gravitree import sample_model
     m, p, v = sample_model("m31", 100000, 5)
@@ -29,7 +34,7 @@ def test_sharded_steps_match_single_rank(world):
     ref = make()
     ref.init()
     sims = [make() for _ in range(world)]
-    g2.Simulation.set_mesh_local(sims)
+    (g2.Simulation.set_mesh_local if mesh == "copy" else g2.Simulation.set_mesh_local_p2p)(sims)
     for s in sims:
         s.init()
     for _ in range(3):
@@ -54,3 +59,30 @@ def test_sharded_steps_match_single_rank(world):
         err = g2.force_error(b.acc, a.acc)
         assert err["median"] <= 1e-6 and err["p99"] <= 1e-5, err
         assert np.max(np.abs(b.pos - a.pos)) < 1e-7  # FP32-order differences, integrated 3 steps
+
+
+def test_p2p_ipc_two_processes(tmp_path):
+    """Two processes (one rank each, both on cuda:0) map each other's exchange buffers
+    through CUDA IPC, exactly as one process per GPU would; handles travel over gloo."""
+    import paper_1811_02761_b200 as g2
+    from paper_1811_02761_b200.gravitree import sample_model
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29613", os.path.join(root, "tests", "p2p_ranks.py"),
+           str(tmp_path)]
+    subprocess.run(cmd, check=True, cwd=root, timeout=600)
+    m, p, v = sample_model("m31", 100000, 5)
+    ref = g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9),
+                        g2.StepScheme(dt_max=1.0 / 64, adaptive=False))
+    ref.set_rebuild_every_step(True)
+    ref.init()
+    inter = 0
+    for _ in range(3):
+        inter = ref.step().events.interactions
+    a = ref.system()
+    got = [np.load(tmp_path / f"rank{r}.npz") for r in range(2)]
+    assert sum(int(g["inter"]) for g in got) == inter
+    for g in got:
+        err = g2.force_error(g["acc"], a.acc)
+        assert err["median"] <= 1e-6 and err["p99"] <= 1e-5, err
+        assert np.max(np.abs(g["pos"] - a.pos)) < 1e-7
