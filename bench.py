@@ -212,6 +212,27 @@ def workload_config(args):
             "l2": "no flush: the resident state (~1 GB at 2^23) exceeds the 126 MB L2"}
 
 
+def hbm_phases(sim, r, n):
+    """HBM roofline of the non-walk phases of one all-active step: algorithmic
+    bytes per particle x N over the phase's CUDA-event time, against the measured copy peak.
+    makeTree = bbox+keys 60 B + radix sort 8 + 24 x 8 passes + split 8 B x mean particle depth
+    + 40 B x cells/N; calcNode 94 B; predict 120 B; correct 150 B per active particle."""
+    peak = measured_peaks().get("hbm_gbs")
+    t = sim.tree()
+    leaf = t.cells[:, 1] == 0
+    depth_mean = float((t.cells[leaf, 3].astype(np.float64) * t.depth[leaf]).sum() / n)
+    per = {"make_tree": 60 + 8 + 24 * 8 + 8 * depth_mean + 40 * len(t.depth) / n, "calc_node": 94.0,
+           "predict": 120.0, "correct": 150.0 * r.active / n}
+    out = {"peak_gbs": peak, "peak_note": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)",
+           "mean_particle_depth": depth_mean, "cells_per_particle": len(t.depth) / n}
+    for k, b in per.items():
+        sec = getattr(r.timings, k)
+        gbs = b * n / sec / 1e9 if sec > 0 else None
+        out[k] = {"bytes_per_particle": b, "seconds": sec, "achieved_gbs": gbs,
+                  "frac": gbs / peak if gbs and peak else None}
+    return out
+
+
 # ------------------------------------------------------------------------- g2 arm
 def join_mesh(args, g2, sim, rank, world):
     """Shard the sink groups over the ranks.  p2p (default): the fused exchange -- the walk
@@ -378,6 +399,8 @@ def run_g2(args):
     if not args.no_paper:
         paper = paper_protocol(args, g2, mass, pos, vel, params, local, rank, world)
 
+    hbm = hbm_phases(sim, r0, args.n) if rank == 0 else None
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -407,7 +430,7 @@ def run_g2(args):
             "phases_last_step": vars(r0.timings), "events_last_step": vars(r0.events), "active": r0.active,
             "init_seconds": t_init, "e2e": e2e, "gpu_launches": launches * args.steps,
             "gpu_launches_per_step": launches, "clocks": clocks, "cpu_baseline": cpu,
-            "paper_protocol": paper,
+            "paper_protocol": paper, "hbm_phases": hbm,
         }
         print(json.dumps(out))
     if world > 1:
