@@ -1,0 +1,127 @@
+"""GPU: the reference's integrator and walk-trend tests through the device-resident Simulation /
+GravityEngine (test_dynamics.cpp:125-268, acceptance.cpp:78-99 and 193-220), with the reference's
+parameters and thresholds."""
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+PERIOD = 6.283185307179586  # circular binary, r0 = 1, M = 1 (test_dynamics.cpp:18)
+
+
+@pytest.fixture(scope="module")
+def g2():
+    import paper_1811_02761_b200 as g2mod
+    return g2mod
+
+
+def circular_binary(g2, r0=1.0):
+    """test_support.hpp:51-60"""
+    v = 0.5 * math.sqrt(1.0 / r0)
+    return g2.ParticleSystem(np.array([0.5, 0.5]), np.array([[-0.5 * r0, 0, 0], [0.5 * r0, 0, 0]]),
+                             np.array([[0, -v, 0], [0, v, 0]]))
+
+
+def test_circular_orbit_holds_radius(g2):
+    sim = g2.Simulation(circular_binary(g2), g2.GravParams(1.0, 0.0, 2.0 ** -20),
+                        g2.StepScheme(adaptive=False, dt_max=PERIOD / 1000.0))
+    sim.init()
+    for _ in range(1000):
+        sim.step()
+        p = sim.system().pos
+        assert abs(np.linalg.norm(p[1] - p[0]) - 1.0) < 0.01
+
+
+def test_bound_pair_energy_drift(g2):
+    params = g2.GravParams(1.0, 0.0, 2.0 ** -20)
+    sim = g2.Simulation(circular_binary(g2), params, g2.StepScheme(adaptive=False, dt_max=PERIOD / 500.0))
+    sim.init()
+    e0 = g2.compute_diagnostics(sim.system(), params).total
+    for _ in range(100):
+        sim.step()
+    e1 = g2.compute_diagnostics(sim.system(), params).total
+    assert abs((e1 - e0) / e0) < 1e-4
+
+
+def test_symmetric_configuration_conserves_momentum(g2):
+    pos = np.array([[0.5 * x, 0.5 * y, 0.5 * z] for x in (-1, 1) for y in (-1, 1) for z in (-1, 1)])
+    sim = g2.Simulation(g2.ParticleSystem(np.ones(8), pos), g2.GravParams(1.0, 0.1, 2.0 ** -9),
+                        g2.StepScheme(dt_max=0.01))
+    sim.init()
+    sim.step()
+    s = sim.system()
+    assert np.linalg.norm((s.mass[:, None] * s.vel).sum(0)) < 1e-12
+
+
+def test_phase_timings_bounded_by_wall_time(g2):
+    from paper_1811_02761_b200.gravitree import sample_model
+    m, p, v = sample_model("plummer", 512, 4)
+    sim = g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 0.02, 2.0 ** -9), g2.StepScheme(dt_max=1 / 64))
+    sim.init()
+    for _ in range(5):
+        r = sim.step()
+        t = r.timings
+        assert min(t.walk_tree, t.calc_node, t.make_tree, t.predict, t.correct) >= 0.0
+        assert t.total() <= r.wall_seconds * (1 + 1e-9) + 1e-9
+
+
+@pytest.mark.parametrize("n", [1024, 1 << 17])
+def test_levels_bounded_and_move_by_one(g2, n):
+    from paper_1811_02761_b200.gravitree import sample_model
+    m, p, v = sample_model("plummer", n, 6)
+    sim = g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 0.02, 2.0 ** -6), g2.StepScheme(dt_max=1 / 16))
+    sim.init()
+    prev = sim.system().level.astype(int)
+    for _ in range(50 if n <= 1024 else 12):
+        sim.step()
+        lv = sim.system().level.astype(int)
+        assert lv.max() <= 24  # kMaxBlockLevel
+        assert np.abs(lv - prev).max() <= 1
+        prev = lv
+
+
+def test_block_steps_track_forced_minimum_step(g2):
+    from paper_1811_02761_b200.gravitree import sample_model
+    params = g2.GravParams(1.0, 0.05, 2.0 ** -12)
+
+    def drift(adaptive, fixed_level):
+        m, p, v = sample_model("plummer", 256, 15)
+        sim = g2.Simulation(g2.ParticleSystem(m, p, v), params,
+                            g2.StepScheme(dt_max=1 / 32, adaptive=adaptive, fixed_level=fixed_level))
+        sim.init()
+        max_level = 0
+        e0 = g2.compute_diagnostics(sim.system(), params).total
+        while sim.time() < 1.0:
+            sim.step()
+            max_level = max(max_level, int(sim.system().level.max()))
+        e1 = g2.compute_diagnostics(sim.system(), params).total
+        return abs((e1 - e0) / e0), max_level
+
+    block, max_level = drift(True, 0)
+    fine, _ = drift(False, max_level)
+    assert (max(block, fine) + 1e-12) / (min(block, fine) + 1e-12) < 3.0
+
+
+def test_counter_and_error_trend_over_dacc(g2):
+    """acceptance.cpp:78-99 and 193-220 on M31 2^17: tighter dacc -> more interactions and MAC
+    evaluations, smaller median error against direct summation."""
+    from paper_1811_02761_b200.gravitree import sample_model
+    m, p, _ = sample_model("m31", 1 << 17, 1)
+    sys0 = g2.ParticleSystem(m, p)
+    eng = g2.GravityEngine(g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9))
+    eng.build(sys0)
+    eng.bootstrap(sys0)  # acc_old_mag for the acceleration MAC
+    ref = g2.direct_sum(sys0, g2.GravParams(1.0, 2.0 ** -5))
+    inter, macs, med = [], [], []
+    for k in (3, 6, 9, 12, 15):
+        eng.set_params(g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -k))
+        s = sys0.copy()
+        ev = eng.evaluate(s)
+        inter.append(ev.interactions)
+        macs.append(ev.mac_evals)
+        med.append(g2.force_error(s.acc, ref)["median"])
+    assert all(a < b for a, b in zip(inter, inter[1:])), inter
+    assert all(a < b for a, b in zip(macs, macs[1:])), macs
+    assert all(a > b for a, b in zip(med, med[1:])), med
