@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="g2", choices=["g2", "reference"])
-    ap.add_argument("--n", type=int, default=1 << 23)
+    ap.add_argument("--n", "--particles", dest="n", type=int, default=1 << 23)
     ap.add_argument("--model", default="m31")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -60,6 +60,8 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("G2_BENCH_ONE_DEVICE"):  # testing only: every rank on cuda:0, gloo process group
+        local = 0
     return rank, world, local
 
 
@@ -241,12 +243,27 @@ def join_mesh(args, g2, sim, rank, world):
     import torch.distributed as dist
     if args.exchange == "p2p":
         handles = [None] * world
-        dist.all_gather_object(handles, sim.p2p_export(rank, world))
-        sim.set_mesh_p2p(rank, world, handles)
-    else:
-        uid = [g2.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        sim.set_mesh(rank, world, uid[0])
+        err = None
+        try:
+            h = sim.p2p_export(rank, world)
+        except Exception as e:  # noqa: BLE001
+            h, err = None, e
+        dist.all_gather_object(handles, h)
+        if all(x is not None for x in handles):
+            try:
+                sim.set_mesh_p2p(rank, world, handles)
+            except Exception as e:  # noqa: BLE001
+                err = e
+        ok = [None] * world
+        dist.all_gather_object(ok, err is None)
+        if all(ok):
+            return
+        # every rank falls back together (a mixed mesh would deadlock)
+        print(f"[bench] rank {rank}: fused P2P exchange unavailable ({err}); using ncclAllGather", file=sys.stderr)
+        args.exchange = "nccl"
+    uid = [g2.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    sim.set_mesh(rank, world, uid[0])
 
 
 def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world):
@@ -307,7 +324,10 @@ def run_g2(args):
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("G2_BENCH_ONE_DEVICE"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1811_02761_b200 as g2
     from paper_1811_02761_b200.gravitree import lib, sample_model
 
@@ -423,7 +443,7 @@ def run_g2(args):
             "dtype": "f32 walk / f64 tree+integrator", "data": "synthetic (reference sample_model m31, seed 1)",
             "config": workload_config(args),
             "roofline": {"bound": "fp32", "kernel": "walk_kernel", "achieved": achieved, "peak": fp32_peak,
-                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": walk_traffic_per_launch(),
+                         "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": walk_traffic_per_launch() if (args.n == 1 << 23 and world == 1) else None,
                          "peak_note": f"148 SM x 128 FP32 lanes x 2 x {f_max:.0f} MHz (sm_max_mhz of "
                                       "MEASURED_PEAKS.json); no FP32 peak is measured there",
                          "flop_per_launch": flops, "walk_seconds": walk_s},
