@@ -11,6 +11,9 @@ namespace g2 {
 namespace {
 
 constexpr int kBlock = 256;
+#ifndef G2_CALC_MINB
+#define G2_CALC_MINB 2  // 2 blocks of 256 per SM: 128 registers, no spills (1: more registers, 25 % slower)
+#endif
 
 // ---- bounding_cube (octree.cpp:24-49) ---------------------------------------
 __global__ void __launch_bounds__(kBlock) bbox_partial_kernel(const double4* __restrict__ xyzm, size_t n,
@@ -587,7 +590,7 @@ __device__ __forceinline__ void leaf_small(const double4* __restrict__ xyzm, uin
     store_node(nodes, nodes32, c, nd);
 }
 
-__global__ void __launch_bounds__(kBlock) calc_leaf_kernel(const double4* __restrict__ xyzm,
+__global__ void __launch_bounds__(kBlock, G2_CALC_MINB) calc_leaf_kernel(const double4* __restrict__ xyzm,
                                                            const uint32_t* __restrict__ child_count,
                                                            const uint32_t* __restrict__ first,
                                                            const uint32_t* __restrict__ count,
@@ -629,7 +632,7 @@ __global__ void __launch_bounds__(kBlock) calc_leaf_kernel(const double4* __rest
     }
 }
 
-__global__ void __launch_bounds__(kBlock) calc_internal_kernel(const uint32_t* __restrict__ first_child,
+__global__ void __launch_bounds__(kBlock, G2_CALC_MINB) calc_internal_kernel(const uint32_t* __restrict__ first_child,
                                                                const uint32_t* __restrict__ child_count,
                                                                const uint8_t* __restrict__ depth,
                                                                const uint32_t* __restrict__ level_start,
