@@ -782,32 +782,45 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
     mbar_arrive(&sm.full[hand & 1]);
 }
 
-// one warp per group: AABB centre, radius and a_min (make_group, traversal.cpp:16-38)
+// 8 lanes per group (4 groups per warp): AABB centre, radius and a_min of make_group
+// (traversal.cpp:16-38).  Each lane folds members lane, lane + 8, ... in order, then three
+// xor-shuffle levels combine the lanes: min / max are exact in any order, so the result is the
+// reference's.  (A warp per group spent its time in 5-level FP64 shuffle trees; a lane per group
+// gathered uncoalesced.)
+constexpr int kGroupLanes = 8;
 __global__ void __launch_bounds__(256) groups_kernel(TreeView t, const double* __restrict__ amag, WalkBuffers b,
                                                      uint32_t gs) {
     const uint32_t n_sinks = *b.n_sinks;
     const uint32_t n_groups = (n_sinks + gs - 1) / gs;
-    const int lane = threadIdx.x & 31;
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (gw == 0 && lane == 0) *b.n_groups = n_groups;
-    for (uint32_t g = gw; g < n_groups; g += (gridDim.x * blockDim.x) >> 5) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t sub = threadIdx.x & (kGroupLanes - 1);
+    if (tid == 0) *b.n_groups = n_groups;
+    const uint32_t stride = (gridDim.x * blockDim.x) / kGroupLanes;
+    // every lane of a warp runs the same number of iterations (shuffles need the full warp)
+    const uint32_t gw0 = tid / kGroupLanes;
+    const uint32_t iters = (n_groups + stride - 1) / stride;
+    for (uint32_t it = 0; it < iters; ++it) {
+        const uint32_t g = gw0 + it * stride;
+        const bool gon = g < n_groups;
         const uint32_t first = g * gs;
-        const uint32_t cnt = min(gs, n_sinks - first);
-        const bool on = uint32_t(lane) < cnt;
-        double4 q = make_double4(0, 0, 0, 0);
+        const uint32_t cnt = gon ? min(gs, n_sinks - first) : 0u;
+        const uint32_t* __restrict__ mk = b.sinks + first;
+        double lx = INFINITY, ly = INFINITY, lz = INFINITY, hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
         double am = INFINITY;
-        if (on) {
-            const uint32_t k = b.sinks[first + lane];
-            q = t.xyzm[k];
-            am = amag[k];
+        if (sub < cnt) {
+            const double4 q = t.xyzm[mk[sub]];
+            lx = hx = q.x, ly = hy = q.y, lz = hz = q.z;
+            am = amag[mk[sub]];
         }
-        // members[0] seeds lo/hi; min/max are exact in any order
-        const double q0x = __shfl_sync(kFull, q.x, 0), q0y = __shfl_sync(kFull, q.y, 0),
-                     q0z = __shfl_sync(kFull, q.z, 0);
-        double lx = on ? q.x : q0x, ly = on ? q.y : q0y, lz = on ? q.z : q0z;
-        double hx = lx, hy = ly, hz = lz;
+        for (uint32_t j = sub + kGroupLanes; j < cnt; j += kGroupLanes) {
+            const uint32_t k = mk[j];
+            const double4 q = t.xyzm[k];
+            lx = smin(lx, q.x), ly = smin(ly, q.y), lz = smin(lz, q.z);
+            hx = smax(hx, q.x), hy = smax(hy, q.y), hz = smax(hz, q.z);
+            am = smin(am, amag[k]);
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
+        for (int o = kGroupLanes / 2; o > 0; o >>= 1) {
             lx = smin(lx, __shfl_xor_sync(kFull, lx, o));
             ly = smin(ly, __shfl_xor_sync(kFull, ly, o));
             lz = smin(lz, __shfl_xor_sync(kFull, lz, o));
@@ -816,11 +829,15 @@ __global__ void __launch_bounds__(256) groups_kernel(TreeView t, const double* _
             hz = smax(hz, __shfl_xor_sync(kFull, hz, o));
             am = smin(am, __shfl_xor_sync(kFull, am, o));
         }
-        const double cx = dmul(dadd(lx, hx), 0.5), cy = dmul(dadd(ly, hy), 0.5), cz = dmul(dadd(lz, hz), 0.5);
-        double r2 = on ? norm2(dsub(q.x, cx), dsub(q.y, cy), dsub(q.z, cz)) : 0.0;
+        const double cx = dmul(0.5, dadd(lx, hx)), cy = dmul(0.5, dadd(ly, hy)), cz = dmul(0.5, dadd(lz, hz));
+        double r2 = 0.0;
+        for (uint32_t j = sub; j < cnt; j += kGroupLanes) {
+            const double4 q = t.xyzm[mk[j]];
+            r2 = smax(r2, norm2(dsub(q.x, cx), dsub(q.y, cy), dsub(q.z, cz)));
+        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) r2 = smax(r2, __shfl_xor_sync(kFull, r2, o));
-        if (lane == 0) {
+        for (int o = kGroupLanes / 2; o > 0; o >>= 1) r2 = smax(r2, __shfl_xor_sync(kFull, r2, o));
+        if (gon && sub == 0) {
             b.groups[g] = GroupRec{cx, cy, cz, dsqrt(r2), am, first, cnt};
             if (b.world > 1) b.gpend[g] = 1u;  // the initial task
         }
@@ -896,7 +913,7 @@ size_t walk_resident_warps() {
 void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffers& b, uint32_t group_size,
                    uint32_t n_sinks_cap, cudaStream_t s) {
     const uint32_t ng = (n_sinks_cap + group_size - 1) / group_size;
-    const unsigned blocks = std::max(1u, std::min<unsigned>(ceil_div(size_t(ng) * 32, 256), kNumSMs * 16));
+    const unsigned blocks = std::max(1u, std::min<unsigned>(ceil_div(size_t(ng) * kGroupLanes, 256), kNumSMs * 16));
     G2_COUNT(1), groups_kernel<<<blocks, 256, 0, s>>>(t, acc_old_mag, b, group_size);
     G2_CUDA(cudaGetLastError());
 }
