@@ -161,9 +161,18 @@ __global__ void __launch_bounds__(kBlock) compact_kernel(const uint8_t* __restri
     const uint32_t tile = s_tile;
     const size_t base = size_t(tile) * kCTile + size_t(tid) * kCItems;  // blocked: thread owns 16 consecutive
     uint32_t bits = 0;
+    if (base + kCItems <= n) {  // one 16-byte load of the thread's flags
+        static_assert(kCItems == 16, "flag vector load");
+        const uint4 v = *reinterpret_cast<const uint4*>(flags + base);
+        const uint32_t w4[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int k = 0; k < kCItems; ++k)
-        if (base + k < n && flags[base + k]) bits |= 1u << k;
+        for (int k = 0; k < kCItems; ++k)
+            if ((w4[k >> 2] >> (8 * (k & 3))) & 0xffu) bits |= 1u << k;
+    } else {
+#pragma unroll
+        for (int k = 0; k < kCItems; ++k)
+            if (base + k < n && flags[base + k]) bits |= 1u << k;
+    }
     const uint32_t x = __popc(bits);
     uint32_t inc = x;
 #pragma unroll
