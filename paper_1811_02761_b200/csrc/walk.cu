@@ -34,16 +34,29 @@
 namespace g2 {
 namespace {
 
-#ifndef G2_PRODUCER_REGS  // setmaxnreg split of the 64-register budget between the two warpgroups
-#define G2_PRODUCER_REGS 0
-#define G2_CONSUMER_REGS 0
+// Occupancy: 5 CTAs x 8 warps per SM.  The launch budget is 48 registers per thread; setmaxnreg
+// then moves 8 per thread from the consumer warpgroup (40: the flush is register-light) to the
+// producer warpgroup (56: the traversal is latency-bound and spills less).  Five CTAs fit the
+// 228 KB of shared memory with 256-entry list buffers.  Measured at 2^23 all-active: 14.13 ms vs
+// 14.50 ms for 4 CTAs x 64 registers with 336-entry buffers.
+#ifndef G2_PRODUCER_REGS  // setmaxnreg split of the register budget between the two warpgroups
+#define G2_PRODUCER_REGS 56
+#define G2_CONSUMER_REGS 40
 #endif
 constexpr int kPairs = 4;                  // producer/consumer warp pairs per CTA
 constexpr int kThreads = 64 * kPairs;      // producers are warps 0..kPairs-1, consumers kPairs..2kPairs-1
 #ifndef G2_WALK_MINB
-#define G2_WALK_MINB 4  // resident CTAs per SM the register budget is tuned for
+#define G2_WALK_MINB 5  // resident CTAs per SM the register budget is tuned for
 #endif
-constexpr int kLcap = 336;                 // interaction-list entries per buffer (4 CTAs x 4 pairs fit 228 KB)
+#ifndef G2_LCAP
+#define G2_LCAP 256     // >= 256: the per-slot overflow path writes one round's cell slot at a time
+#endif
+constexpr int kLcap = G2_LCAP;             // interaction-list entries per buffer
+// With few groups (small block-step active sets) the fifth CTA per SM only adds contention to the
+// draining tail: CTAs beyond 4 per SM then exit at once.
+#ifndef G2_DENSE_MIN_GROUPS
+#define G2_DENSE_MIN_GROUPS 12288
+#endif
 constexpr int kScap = 512;                 // shared stack entries per producer (>= 64 cells x 8 children)
 constexpr uint32_t kSpillWords = 16384;    // global stack entries per producer
 #ifndef G2_DONATE_EVERY
@@ -321,6 +334,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PairSmem* const pairs = reinterpret_cast<PairSmem*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (blockIdx.x >= 4u * kNumSMs && b.qstate[3] < uint32_t(G2_DENSE_MIN_GROUPS)) return;  // whole CTA
     if (threadIdx.x < kPairs) {
         PairSmem& ps = pairs[threadIdx.x];
         for (int i = 0; i < 2; ++i) mbar_init(&ps.full[i], 32), mbar_init(&ps.empty[i], 32);
