@@ -93,6 +93,50 @@ __global__ void __launch_bounds__(kBlock) predict_kernel(StepState st, size_t n,
     }
 }
 
+// the same, two particles per thread with 16-byte loads/stores of the SoA arrays (more bytes in
+// flight per thread; cudaMalloc'd arrays are 256-byte aligned, so pairs are 16-byte aligned)
+__device__ __forceinline__ void predict_one(double4& p, double& vx, double& vy, double& vz, double ax, double ay,
+                                            double az, double dt, double h) {
+    p.x = dadd(p.x, dadd(dmul(vx, dt), dmul(ax, h)));
+    p.y = dadd(p.y, dadd(dmul(vy, dt), dmul(ay, h)));
+    p.z = dadd(p.z, dadd(dmul(vz, dt), dmul(az, h)));
+    vx = dadd(vx, dmul(ax, dt));
+    vy = dadd(vy, dmul(ay, dt));
+    vz = dadd(vz, dmul(az, dt));
+}
+__global__ void __launch_bounds__(kBlock) predict2_kernel(StepState st, size_t n, const unsigned long long* t_next_p,
+                                                          uint64_t now, double tick, uint8_t* __restrict__ active) {
+    const uint64_t t_next = *t_next_p;
+    const double dt = dmul(double(t_next - now), tick);
+    const double h = dmul(dmul(0.5, dt), dt);
+    const size_t np = n / 2;
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < np; i += size_t(gridDim.x) * kBlock) {
+        double4 p0 = st.xyzm[2 * i], p1 = st.xyzm[2 * i + 1];
+        double2 vx = reinterpret_cast<const double2*>(st.vx)[i], vy = reinterpret_cast<const double2*>(st.vy)[i];
+        double2 vz = reinterpret_cast<const double2*>(st.vz)[i];
+        const double2 ax = reinterpret_cast<const double2*>(st.ax)[i], ay = reinterpret_cast<const double2*>(st.ay)[i];
+        const double2 az = reinterpret_cast<const double2*>(st.az)[i];
+        const ulonglong2 lu = reinterpret_cast<const ulonglong2*>(st.last_update)[i];
+        const uchar2 lv = reinterpret_cast<const uchar2*>(st.level)[i];
+        predict_one(p0, vx.x, vy.x, vz.x, ax.x, ay.x, az.x, dt, h);
+        predict_one(p1, vx.y, vy.y, vz.y, ax.y, ay.y, az.y, dt, h);
+        st.xyzm[2 * i] = p0, st.xyzm[2 * i + 1] = p1;
+        reinterpret_cast<double2*>(st.vx)[i] = vx, reinterpret_cast<double2*>(st.vy)[i] = vy;
+        reinterpret_cast<double2*>(st.vz)[i] = vz;
+        if (active)
+            reinterpret_cast<uchar2*>(active)[i] =
+                make_uchar2(lu.x + level_ticks(lv.x) == t_next ? 1 : 0, lu.y + level_ticks(lv.y) == t_next ? 1 : 0);
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) {  // odd tail
+        const size_t i = n - 1;
+        double4 p = st.xyzm[i];
+        double vx = st.vx[i], vy = st.vy[i], vz = st.vz[i];
+        predict_one(p, vx, vy, vz, st.ax[i], st.ay[i], st.az[i], dt, h);
+        st.xyzm[i] = p, st.vx[i] = vx, st.vy[i] = vy, st.vz[i] = vz;
+        if (active) active[i] = (st.last_update[i] + level_ticks(st.level[i]) == t_next) ? 1 : 0;
+    }
+}
+
 // ---- block_level (integrator.cpp:21-33) ------------------------------------------
 __device__ int block_level_dev(double acc_mag, const SchemeDev& s) {
     if (!s.adaptive) return max(0, min(s.fixed_level, kMaxBlockLevel));
@@ -383,7 +427,11 @@ void launch_tnext(const StepState& st, size_t n, unsigned long long* t_next, cud
 
 void launch_predict(const StepState& st, size_t n, const unsigned long long* t_next, uint64_t now, double tick,
                     uint8_t* active_flag, cudaStream_t s) {
-    G2_COUNT(1), predict_kernel<<<grid_for(n), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag);
+    static const bool one = std::getenv("G2_PREDICT_ONE") != nullptr;  // development A/B
+    if (one)
+        G2_COUNT(1), predict_kernel<<<grid_for(n), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag);
+    else
+        G2_COUNT(1), predict2_kernel<<<grid_for(n / 2 + 1), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag);
 }
 
 void launch_compact(const uint8_t* flags, size_t n, uint32_t* out, uint32_t* n_out, uint64_t* status,
