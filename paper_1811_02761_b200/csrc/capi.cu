@@ -224,10 +224,17 @@ struct PeerExchange final : g2::Exchange {
     uint64_t epoch = 0;
     float4* buf[2] = {};                        // own accumulators (exported)
     uint64_t* flags = nullptr;                  // own arrival flags [kMaxPeers] (exported)
+    uint32_t* cost[2] = {};                     // own per-group cost arrays (exported)
+    uint32_t* ngrec = nullptr;                  // [2] group counts behind cost[0], cost[1] (local)
     float4* pbuf[g2::kMaxPeers][2] = {};        // every rank's accumulators as seen from here
     uint64_t* pflags[g2::kMaxPeers] = {};
+    uint32_t* pcost[g2::kMaxPeers][2] = {};
     std::vector<void*> opened;                  // IPC mappings to close
     int device = 0;
+    // In-process mesh (all ranks in one context): the ranks meet at a host barrier after their walks
+    // instead of device flags -- a device-side spin would sit at the head of shared copy/launch
+    // queues and starve the ranks it waits for.
+    std::shared_ptr<LocalMesh> mesh;
 
     void alloc(g2::Simulation& sim, int w, int r) {
         world = w, self = r;
@@ -240,23 +247,40 @@ struct PeerExchange final : g2::Exchange {
         }
         G2_CUDA(cudaMalloc(&flags, g2::kMaxPeers * sizeof(uint64_t)));
         G2_CUDA(cudaMemset(flags, 0, g2::kMaxPeers * sizeof(uint64_t)));
+        const size_t groups = sim.n() / sim.group_size() + 64;
+        for (auto& c : cost) G2_CUDA(cudaMalloc(&c, groups * sizeof(uint32_t)));
+        G2_CUDA(cudaMalloc(&ngrec, 2 * sizeof(uint32_t)));
+        G2_CUDA(cudaMemset(ngrec, 0xff, 2 * sizeof(uint32_t)));  // no history: equal shards first
         pbuf[self][0] = buf[0], pbuf[self][1] = buf[1], pflags[self] = flags;
+        pcost[self][0] = cost[0], pcost[self][1] = cost[1];
     }
     ~PeerExchange() override {
         for (void* p : opened) cudaIpcCloseMemHandle(p);
         for (auto& b : buf)
             if (b) cudaFree(b);
+        for (auto& c : cost)
+            if (c) cudaFree(c);
         if (flags) cudaFree(flags);
+        if (ngrec) cudaFree(ngrec);
     }
+    bool device_shards() const override { return true; }
     void before_walk(g2::Simulation& sim) override {
         const int par = int(epoch & 1);
         float4* peers[g2::kMaxPeers] = {};
-        for (int q = 0; q < world; ++q) peers[q] = pbuf[q][par];
-        sim.engine().set_peer_push(world, self, buf[par], peers);
+        uint32_t* costs[g2::kMaxPeers] = {};
+        for (int q = 0; q < world; ++q) peers[q] = pbuf[q][par], costs[q] = pcost[q][par];
+        static const bool equal = std::getenv("G2_EQUAL_SHARDS") != nullptr;  // development A/B
+        sim.engine().set_peer_push(world, self, buf[par], peers, equal ? nullptr : costs, cost[par ^ 1],
+                                   ngrec + (par ^ 1), ngrec + par);
     }
     void allgather_acc(g2::Simulation& sim) override {
         ++epoch;
         cudaStream_t s = sim.engine().stream();
+        if (mesh) {
+            G2_CUDA(cudaStreamSynchronize(s));  // own walk (and its pushes) complete
+            mesh->barrier();                    // every rank's walk complete
+            return;
+        }
         PeerFlags pf{};
         for (int q = 0; q < world; ++q) pf.f[q] = pflags[q];
         G2_COUNT(1), peer_signal_kernel<<<1, 32, 0, s>>>(pf, world, self, epoch);
@@ -264,7 +288,7 @@ struct PeerExchange final : g2::Exchange {
         G2_CUDA(cudaGetLastError());
     }
 };
-constexpr size_t kP2PHandleBytes = 3 * sizeof(cudaIpcMemHandle_t);
+constexpr size_t kP2PHandleBytes = 5 * sizeof(cudaIpcMemHandle_t);
 
 }  // namespace
 
@@ -623,6 +647,8 @@ int g2_sim_p2p_export(g2_sim* s, int rank, int world, void* handle) {
         G2_CUDA(cudaIpcGetMemHandle(&h[0], ex->buf[0]));
         G2_CUDA(cudaIpcGetMemHandle(&h[1], ex->buf[1]));
         G2_CUDA(cudaIpcGetMemHandle(&h[2], ex->flags));
+        G2_CUDA(cudaIpcGetMemHandle(&h[3], ex->cost[0]));
+        G2_CUDA(cudaIpcGetMemHandle(&h[4], ex->cost[1]));
         s->pending = std::move(ex);
     });
 }
@@ -636,13 +662,14 @@ int g2_sim_set_mesh_p2p(g2_sim* s, int rank, int world, const void* handles) {
         G2_CUDA(cudaSetDevice(ex->device));
         for (int q = 0; q < world; ++q) {
             if (q == rank) continue;
-            void* p[3];
-            for (int k = 0; k < 3; ++k) {
-                G2_CUDA(cudaIpcOpenMemHandle(&p[k], h[3 * q + k], cudaIpcMemLazyEnablePeerAccess));
+            void* p[5];
+            for (int k = 0; k < 5; ++k) {
+                G2_CUDA(cudaIpcOpenMemHandle(&p[k], h[5 * q + k], cudaIpcMemLazyEnablePeerAccess));
                 ex->opened.push_back(p[k]);
             }
             ex->pbuf[q][0] = static_cast<float4*>(p[0]), ex->pbuf[q][1] = static_cast<float4*>(p[1]);
             ex->pflags[q] = static_cast<uint64_t*>(p[2]);
+            ex->pcost[q][0] = static_cast<uint32_t*>(p[3]), ex->pcost[q][1] = static_cast<uint32_t*>(p[4]);
         }
         s->s->set_shard(rank, world, ex);
         s->ex = std::move(s->pending);
@@ -653,9 +680,12 @@ int g2_sim_set_mesh_local_p2p(g2_sim** sims, int world) {
     return guarded([&] {
         if (world < 2 || world > g2::kMaxPeers) throw g2::Error(G2_DATA_ERROR, "set_mesh_local_p2p: 2 <= world <= 8");
         std::vector<PeerExchange*> ex(world);
+        auto mesh = std::make_shared<LocalMesh>();
+        for (int r = 0; r < world; ++r) mesh->sims.push_back(sims[r]->s.get());
         for (int r = 0; r < world; ++r) {
             auto e = std::make_unique<PeerExchange>();
             e->alloc(*sims[r]->s, world, r);
+            e->mesh = mesh;
             ex[r] = e.get();
             sims[r]->ex = std::move(e);
         }
@@ -663,6 +693,7 @@ int g2_sim_set_mesh_local_p2p(g2_sim** sims, int world) {
             for (int q = 0; q < world; ++q) {
                 ex[r]->pbuf[q][0] = ex[q]->buf[0], ex[r]->pbuf[q][1] = ex[q]->buf[1];
                 ex[r]->pflags[q] = ex[q]->flags;
+                ex[r]->pcost[q][0] = ex[q]->cost[0], ex[r]->pcost[q][1] = ex[q]->cost[1];
                 if (ex[q]->device != ex[r]->device) {
                     int ok = 0;
                     G2_CUDA(cudaDeviceCanAccessPeer(&ok, ex[r]->device, ex[q]->device));

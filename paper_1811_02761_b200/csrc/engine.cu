@@ -369,8 +369,15 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     b.world = peer_world_, b.self = peer_self_;
     if (peer_world_ > 1) {
         gpend_.reserve(ng_cap + 1);
+        gcost_.reserve(ng_cap + 1);
         b.gpend = gpend_.p;
-        for (int q = 0; q < kMaxPeers; ++q) b.peer_accum[q] = peer_accum_[q];
+        b.gcost = gcost_.p;
+        for (int q = 0; q < kMaxPeers; ++q) b.peer_accum[q] = peer_accum_[q], b.peer_cost[q] = peer_cost_[q];
+        // shards computed on the device (no host round trip): cost-balanced when a cost history is
+        // given, else equal group counts
+        shard_.reserve(2);
+        b.shard = shard_.p;
+        if (peer_cost_[peer_self_] && ng_cur_) b.cost_prev = cost_prev_, b.ng_prev = ng_prev_, b.ng_cur = ng_cur_;
     }
     b.events = events_.p;
     b.queue = queue_.p;
@@ -719,8 +726,12 @@ StepResultH Simulation::step() {
     if (world_ > 1) {
         // contiguous equal shard of the groups (cost-balanced sharding: see DESIGN.md)
         uint32_t na = 0;
-        G2_CUDA(cudaMemcpyAsync(&na, n_active_.p, 4, cudaMemcpyDeviceToHost, s));
-        G2_CUDA(cudaStreamSynchronize(s));
+        if (!exchange_ || !exchange_->device_shards()) {  // host-side equal shards (copy / NCCL meshes)
+            HostSync* hs = eng_.host_sync();
+            G2_CUDA(cudaMemcpyAsync(&hs->na, n_active_.p, 4, cudaMemcpyDeviceToHost, s));
+            G2_CUDA(cudaStreamSynchronize(s));
+            na = hs->na;
+        }
         const uint32_t gs = uint32_t(eng_.config().group_size);
         const uint32_t ng = (na + gs - 1) / gs;
         lo = uint32_t(uint64_t(ng) * rank_ / world_);

@@ -87,9 +87,17 @@ public:
     float4* accum() { return accum_ext_ ? accum_ext_ : accum_.p; }
     // fused peer exchange for the next walks: accumulate into `accum` (an exported buffer) and
     // push finished groups to `peers` (world entries, [self] unused); world <= 1 turns it off
-    void set_peer_push(int world, int self, float4* accum, float4* const* peers) {
+    // peer_cost: every rank's cost array of this step ([self] = own); cost_prev / ng_prev: the own copy
+    // of the previous step's costs and their group count, ng_cur: where this step records its count
+    void set_peer_push(int world, int self, float4* accum, float4* const* peers, uint32_t* const* peer_cost = nullptr,
+                       const uint32_t* cost_prev = nullptr, const uint32_t* ng_prev = nullptr,
+                       uint32_t* ng_cur = nullptr) {
         peer_world_ = world, peer_self_ = self, accum_ext_ = world > 1 ? accum : nullptr;
-        for (int q = 0; q < kMaxPeers; ++q) peer_accum_[q] = world > 1 && q < world ? peers[q] : nullptr;
+        for (int q = 0; q < kMaxPeers; ++q) {
+            peer_accum_[q] = world > 1 && q < world ? peers[q] : nullptr;
+            peer_cost_[q] = world > 1 && q < world && peer_cost ? peer_cost[q] : nullptr;
+        }
+        cost_prev_ = cost_prev, ng_prev_ = ng_prev, ng_cur_ = ng_cur;
     }
     size_t accum_cap() const { return accum_.cap; }
     void reserve_accum(size_t slots) { accum_.reserve(slots); }
@@ -147,7 +155,11 @@ private:
     DBuf<uint32_t> sinks_, sinks_alt_, n_sinks_, n_groups_;
     DBuf<GroupRec> groups_;
     DBuf<float4> accum_;
-    DBuf<uint32_t> gpend_;
+    DBuf<uint32_t> gpend_, gcost_, shard_;
+    uint32_t* peer_cost_[kMaxPeers] = {};
+    const uint32_t* cost_prev_ = nullptr;
+    const uint32_t* ng_prev_ = nullptr;
+    uint32_t* ng_cur_ = nullptr;
     float4* accum_ext_ = nullptr;
     float4* peer_accum_[kMaxPeers] = {};
     int peer_world_ = 1, peer_self_ = 0;
@@ -216,6 +228,7 @@ struct StepResultH {
 struct Exchange {
     virtual ~Exchange() = default;
     virtual void before_walk(class Simulation&) {}  // e.g. point the walk at this step's exchange buffers
+    virtual bool device_shards() const { return false; }  // the walk splits the groups on the device
     virtual void allgather_acc(class Simulation& sim) = 0;
 };
 

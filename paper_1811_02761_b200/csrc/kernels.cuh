@@ -112,6 +112,14 @@ struct WalkBuffers {
     uint32_t* gpend;                    // [n_groups] tasks of the group not yet written out
     float4* peer_accum[kMaxPeers];      // peer accumulators, [self] unused
     int world, self;
+    // cost-balanced shards (peer exchange): every group's list-entry count of this step goes to every
+    // rank's cost_out; the next step splits the groups by the previous step's costs on the device
+    uint32_t* gcost;                    // [n_groups] entry counts accumulated over a group's tasks
+    uint32_t* peer_cost[kMaxPeers];     // this step's cost arrays of every rank ([self] = own)
+    const uint32_t* cost_prev;          // own copy of the previous step's costs (nullable: equal shards)
+    const uint32_t* ng_prev;            // groups behind cost_prev
+    uint32_t* ng_cur;                   // groups of this step (written by the shard kernel)
+    uint32_t* shard;                    // [2] device lo, hi (group indices) when cost-balanced
 };
 size_t walk_spill_words();
 size_t walk_resident_warps();

@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         const f2 e2 = pk(eps2, eps2);
         f2 sx2 = 0, sy2 = 0, sz2 = 0;
         Acc2 a0{0ull, 0ull, 0ull, 0.f}, a1{0ull, 0ull, 0ull, 0.f};
-        uint32_t gfirst = 0;
+        uint32_t gfirst = 0, tentries = 0;
         bool has_sink = false;
         for (uint32_t it = 0;; ++it) {
             const int bi = int(it & 1);
@@ -369,6 +369,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                             gzl = float(dsub(g.cz, double(gzh)));
                 has_sink = uint32_t(lane) < g.count;
                 gfirst = g.first;
+                tentries = 0;
                 float sx = 0.f, sy = 0.f, sz = 0.f;
                 if (has_sink) {
                     const uint32_t k = b.sinks[g.first + lane];
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 a0 = Acc2{0ull, 0ull, 0ull, 0.f}, a1 = a0;
             }
             flush_list<kPot, kEps0>(ps.buf[bi], int(cnt), sx2, sy2, sz2, e2, a0, a1);
+            tentries += cnt;
             __syncwarp();
             mbar_arrive(&ps.empty[bi]);
             if ((fl & kLast) && has_sink) {
@@ -397,6 +399,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             if ((fl & kLast) && b.world > 1) {
                 // the group's last task to finish pushes its final accumulators to every peer
                 // rank (NVLink stores, overlapped with the rest of the walk)
+                if (lane == 0) atomicAdd(&b.gcost[grp], tentries);
                 __threadfence();
                 __syncwarp();
                 uint32_t last = 0;
@@ -407,8 +410,10 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                         const float4 v = __ldcg(&b.accum[gfirst + lane]);
                         for (int q = 0; q < b.world; ++q)
                             if (q != b.self) b.peer_accum[q][gfirst + lane] = v;
-                        __threadfence_system();
                     }
+                    // the group's cost: the same value into every rank's array (identical shards next step)
+                    if (b.peer_cost[0] && lane < b.world) b.peer_cost[lane][grp] = __ldcg(&b.gcost[grp]);
+                    __threadfence_system();
                 }
             }
         }
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
     uint32_t* q_pending = b.qstate + 2;
     uint32_t* q_dhead = b.qstate + 4;  // donated slots claimed
     const uint32_t ng = b.qstate[3];   // initial tasks (written by walk_init)
-    const uint32_t glo = b.group_lo;
+    const uint32_t glo = b.qstate[5];  // first group of this launch's shard (walk_init)
     const float thetaf = float(p.theta);
     uint32_t hand = 0;  // buffers handed to the consumer so far: buffer = hand & 1
 
@@ -853,16 +858,67 @@ __global__ void __launch_bounds__(256) groups_kernel(TreeView t, const double* _
         for (int o = kGroupLanes / 2; o > 0; o >>= 1) r2 = smax(r2, __shfl_xor_sync(kFull, r2, o));
         if (gon && sub == 0) {
             b.groups[g] = GroupRec{cx, cy, cz, dsqrt(r2), am, first, cnt};
-            if (b.world > 1) b.gpend[g] = 1u;  // the initial task
+            if (b.world > 1) b.gpend[g] = 1u, b.gcost[g] = 0u;  // the initial task
         }
+    }
+}
+
+// Cost-balanced contiguous shards of the groups: rank r walks groups
+// [b_r, b_{r+1}) with b_r the first group whose cost prefix reaches r/world of the total, the
+// costs being the previous step's per-group list-entry counts (every rank holds the same array, so
+// every rank computes the same boundaries).  With no usable history (first step, or a different
+// group count: the active set changed) the shards are equal group counts.
+constexpr int kShardThreads = 1024;
+__global__ void __launch_bounds__(kShardThreads) shard_kernel(const uint32_t* __restrict__ cost,
+                                                              const uint32_t* ng_prev, uint32_t* ng_cur,
+                                                              const uint32_t* n_groups_p, int world, int rank,
+                                                              uint32_t* shard) {
+    __shared__ unsigned long long part[kShardThreads];
+    __shared__ uint32_t bnd[kMaxPeers + 1];
+    const uint32_t ng = *n_groups_p;
+    const bool hist = cost && ng_prev && *ng_prev == ng && ng > 0;
+    const uint32_t per = (ng + kShardThreads - 1) / kShardThreads;
+    const uint32_t g0 = min(ng, threadIdx.x * per), g1 = min(ng, g0 + per);
+    unsigned long long sum = 0;
+    if (hist)
+        for (uint32_t g = g0; g < g1; ++g) sum += cost[g];
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    for (int o = 1; o < kShardThreads; o <<= 1) {  // inclusive Hillis-Steele scan of the partial sums
+        const unsigned long long y = threadIdx.x >= unsigned(o) ? part[threadIdx.x - o] : 0ull;
+        __syncthreads();
+        part[threadIdx.x] += y;
+        __syncthreads();
+    }
+    const unsigned long long total = part[kShardThreads - 1];
+    if (threadIdx.x <= unsigned(world)) bnd[threadIdx.x] = uint32_t(uint64_t(ng) * threadIdx.x / world);  // equal
+    __syncthreads();
+    if (hist && total > 0) {
+        const unsigned long long before = part[threadIdx.x] - sum;
+        for (int r = 1; r < world; ++r) {
+            const unsigned long long t = total * unsigned(r) / unsigned(world);
+            if (before <= t && t < part[threadIdx.x]) {  // boundary r falls inside this thread's segment
+                unsigned long long acc = before;
+                uint32_t g = g0;
+                while (g < g1 && acc + cost[g] <= t) acc += cost[g++];
+                bnd[r] = g;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        shard[0] = bnd[rank], shard[1] = bnd[rank + 1];
+        if (ng_cur) *ng_cur = ng;  // the groups whose costs this step records
     }
 }
 
 __global__ void walk_init_kernel(WalkBuffers b) {
     if (threadIdx.x == 0) {
         const uint32_t n_groups = *b.n_groups;
-        const uint32_t hi = min(b.group_hi, n_groups);
-        const uint32_t ng = hi > b.group_lo ? hi - b.group_lo : 0u;
+        const uint32_t lo = b.shard ? b.shard[0] : b.group_lo;
+        const uint32_t hi = min(b.shard ? b.shard[1] : b.group_hi, n_groups);
+        const uint32_t ng = hi > lo ? hi - lo : 0u;
+        b.qstate[5] = lo;
         b.qstate[0] = 0;   // initial tasks claimed
         b.qstate[1] = 0;   // donated slots reserved
         b.qstate[2] = ng;  // tasks pending
@@ -873,7 +929,12 @@ __global__ void walk_init_kernel(WalkBuffers b) {
 
 // zero the accumulator slots this launch accumulates into: all sinks, or with a peer exchange
 // only the own shard's slots (the other slots are written by the peers, possibly already)
-__global__ void zero_accum_kernel(float4* accum, const uint32_t* n_sinks, uint32_t cap, uint32_t lo, uint32_t hi) {
+__global__ void zero_accum_kernel(float4* accum, const uint32_t* n_sinks, uint32_t cap, uint32_t lo, uint32_t hi,
+                                  const uint32_t* shard, uint32_t gs) {
+    if (shard) {
+        lo = uint32_t(min(uint64_t(shard[0]) * gs, uint64_t(~0u)));
+        hi = uint32_t(min(uint64_t(shard[1]) * gs, uint64_t(~0u)));
+    }
     const uint32_t n = min(min(*n_sinks, cap), hi);
     for (uint32_t i = lo + blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         accum[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -940,7 +1001,12 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
         zlo = uint32_t(std::min<uint64_t>(uint64_t(b.group_lo) * gs, ~0u));
         zhi = uint32_t(std::min<uint64_t>(uint64_t(b.group_hi) * gs, ~0u));
     }
-    G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi);
+    if (b.shard) {
+        G2_COUNT(1), shard_kernel<<<1, kShardThreads, 0, s>>>(b.cost_prev, b.ng_prev, b.ng_cur, b.n_groups, b.world,
+                                                              b.self, b.shard);
+        G2_CUDA(cudaGetLastError());
+    }
+    G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi, b.shard, gs);
     G2_COUNT(1), walk_init_kernel<<<1, 32, 0, s>>>(b);
     const bool eps0 = p.eps == 0.0;
     const bool check = b.level_count != nullptr;
