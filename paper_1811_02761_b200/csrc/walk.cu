@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         const f2 e2 = pk(eps2, eps2);
         f2 sx2 = 0, sy2 = 0, sz2 = 0;
         Acc2 a0{0ull, 0ull, 0ull, 0.f}, a1{0ull, 0ull, 0ull, 0.f};
-        uint32_t gfirst = 0, tentries = 0;
+        uint32_t gfirst = 0;
         bool has_sink = false;
         for (uint32_t it = 0;; ++it) {
             const int bi = int(it & 1);
@@ -369,7 +369,6 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                             gzl = float(dsub(g.cz, double(gzh)));
                 has_sink = uint32_t(lane) < g.count;
                 gfirst = g.first;
-                tentries = 0;
                 float sx = 0.f, sy = 0.f, sz = 0.f;
                 if (has_sink) {
                     const uint32_t k = b.sinks[g.first + lane];
@@ -383,7 +382,6 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 a0 = Acc2{0ull, 0ull, 0ull, 0.f}, a1 = a0;
             }
             flush_list<kPot, kEps0>(ps.buf[bi], int(cnt), sx2, sy2, sz2, e2, a0, a1);
-            tentries += cnt;
             __syncwarp();
             mbar_arrive(&ps.empty[bi]);
             if ((fl & kLast) && has_sink) {
@@ -399,7 +397,6 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             if ((fl & kLast) && b.world > 1) {
                 // the group's last task to finish pushes its final accumulators to every peer
                 // rank (NVLink stores, overlapped with the rest of the walk)
-                if (lane == 0) atomicAdd(&b.gcost[grp], tentries);
                 __threadfence();
                 __syncwarp();
                 uint32_t last = 0;
@@ -769,6 +766,9 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 }
             }
         }
+        // the task's list entries into the group's cost (read by the consumer retiring the group's last
+        // task, which is ordered after this through the buffer hand-over and the pending counter)
+        if (b.world > 1 && lane == 0) atomicAdd(&b.gcost[grp], pushes);
         // the last buffer of the task (possibly empty) tells the consumer to write out
         handoff(lsize, grp, tflags | kLast);
 
