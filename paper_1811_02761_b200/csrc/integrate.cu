@@ -72,29 +72,9 @@ __global__ void __launch_bounds__(kBlock) tnext_kernel(const uint8_t* __restrict
     if ((threadIdx.x & 31) == 0 && m != ~0ull) atomicMin(t_next, m);
 }
 
-// ---- predict (integrator.cpp:40-45) on ALL particles + active flags (:107-110)
-__global__ void __launch_bounds__(kBlock) predict_kernel(StepState st, size_t n, const unsigned long long* t_next_p,
-                                                         uint64_t now, double tick, uint8_t* __restrict__ active) {
-    const uint64_t t_next = *t_next_p;
-    const double dt = dmul(double(t_next - now), tick);
-    const double h = dmul(dmul(0.5, dt), dt);
-    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock) {
-        double4 p = st.xyzm[i];
-        const double vx = st.vx[i], vy = st.vy[i], vz = st.vz[i];
-        const double ax = st.ax[i], ay = st.ay[i], az = st.az[i];
-        p.x = dadd(p.x, dadd(dmul(vx, dt), dmul(ax, h)));
-        p.y = dadd(p.y, dadd(dmul(vy, dt), dmul(ay, h)));
-        p.z = dadd(p.z, dadd(dmul(vz, dt), dmul(az, h)));
-        st.xyzm[i] = p;
-        st.vx[i] = dadd(vx, dmul(ax, dt));
-        st.vy[i] = dadd(vy, dmul(ay, dt));
-        st.vz[i] = dadd(vz, dmul(az, dt));
-        if (active) active[i] = (st.last_update[i] + level_ticks(st.level[i]) == t_next) ? 1 : 0;
-    }
-}
-
-// the same, two particles per thread with 16-byte loads/stores of the SoA arrays (more bytes in
-// flight per thread; cudaMalloc'd arrays are 256-byte aligned, so pairs are 16-byte aligned)
+// ---- predict (integrator.cpp:40-45) on ALL particles + active flags (:107-110), two particles per
+// thread with 16-byte loads/stores of the SoA arrays (more bytes in flight per thread; cudaMalloc'd
+// arrays are 256-byte aligned, so pairs are 16-byte aligned)
 __device__ __forceinline__ void predict_one(double4& p, double& vx, double& vy, double& vz, double ax, double ay,
                                             double az, double dt, double h) {
     p.x = dadd(p.x, dadd(dmul(vx, dt), dmul(ax, h)));
@@ -104,7 +84,7 @@ __device__ __forceinline__ void predict_one(double4& p, double& vx, double& vy, 
     vy = dadd(vy, dmul(ay, dt));
     vz = dadd(vz, dmul(az, dt));
 }
-__global__ void __launch_bounds__(kBlock) predict2_kernel(StepState st, size_t n, const unsigned long long* t_next_p,
+__global__ void __launch_bounds__(kBlock) predict_kernel(StepState st, size_t n, const unsigned long long* t_next_p,
                                                           uint64_t now, double tick, uint8_t* __restrict__ active) {
     const uint64_t t_next = *t_next_p;
     const double dt = dmul(double(t_next - now), tick);
@@ -427,11 +407,7 @@ void launch_tnext(const StepState& st, size_t n, unsigned long long* t_next, cud
 
 void launch_predict(const StepState& st, size_t n, const unsigned long long* t_next, uint64_t now, double tick,
                     uint8_t* active_flag, cudaStream_t s) {
-    static const bool one = std::getenv("G2_PREDICT_ONE") != nullptr;  // development A/B
-    if (one)
-        G2_COUNT(1), predict_kernel<<<grid_for(n), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag);
-    else
-        G2_COUNT(1), predict2_kernel<<<grid_for(n / 2 + 1), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag);
+    G2_COUNT(1), predict_kernel<<<grid_for(n / 2 + 1), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag);
 }
 
 void launch_compact(const uint8_t* flags, size_t n, uint32_t* out, uint32_t* n_out, uint64_t* status,
