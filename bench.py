@@ -271,15 +271,17 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world):
     (eta 0.5, adaptive levels) with dt_max = 1, timed over `paper_steps` steps after init and
     4 warm-up steps, once with the reference's own rebuild auto-tuner (fed CUDA-event times)
     and once with a fixed rebuild interval of 2 (the shortest the reference's tuner allows:
-    GPU rebuilds are cheap).  Reports mean device s/step next to the paper's V100
-    3.3e-2 s/step, the mean active fraction and s per 1e11 walk Flop."""
+    GPU rebuilds are cheap); plus the reference's default scheme (dt_max = 1/16, auto-tuner), the
+    other block-step scheme SURVEY §8d config 3 names.  Reports mean device s/step next to the paper's
+    V100 3.3e-2 s/step, the mean active fraction and s per 1e11 walk Flop."""
     import ctypes
     import torch
     from paper_1811_02761_b200.gravitree import lib
     out = {"what": "block steps, reference driver defaults with dt_max=1 (eta 0.5, adaptive levels)",
            "paper_v100_s_per_step": PAPER_V100_S_PER_STEP}
-    for label, fixed in (("auto_tuned_rebuild", 0), ("rebuild_every_2", 2)):
-        sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), params, g2.StepScheme(eta=0.5, dt_max=1.0),
+    for label, fixed, dt_max in (("auto_tuned_rebuild", 0, 1.0), ("rebuild_every_2", 2, 1.0),
+                                 ("default_scheme_dt_max_1_16_auto_tuned", 0, 1.0 / 16)):
+        sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), params, g2.StepScheme(eta=0.5, dt_max=dt_max),
                             g2.EngineConfig(), device=local)
         if world > 1:
             join_mesh(args, g2, sim, rank, world)
@@ -309,7 +311,7 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world):
             t = torch.tensor([flops], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.SUM)
             flops = float(t[0])
-        out[label] = {"steps": args.paper_steps, "s_per_step": s_per_step,
+        out[label] = {"steps": args.paper_steps, "dt_max": dt_max, "s_per_step": s_per_step,
                       "mean_active_fraction": float(np.mean([r.active for r in rs])) / args.n,
                       "rebuilds": int(sum(r.rebuilt for r in rs)), "walk_flop_per_step": flops,
                       "speedup_vs_paper_v100": PAPER_V100_S_PER_STEP / s_per_step if s_per_step > 0 else None,
