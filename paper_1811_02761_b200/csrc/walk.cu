@@ -257,7 +257,7 @@ __device__ __forceinline__ void flush_list(const ListBuf& lb, int cnt, f2 sx, f2
     const ulonglong2* pa = reinterpret_cast<const ulonglong2*>(lb.la);
     const ulonglong2* pb = reinterpret_cast<const ulonglong2*>(lb.lb);
     int p = 0;
-#pragma unroll 2
+#pragma unroll 4  // 8 entry pairs in flight per iteration group: 13.93 vs 14.10 ms (unroll 2) at 2^23
     for (; p + 1 < np; p += 2) {
         const ulonglong2 A0 = pa[p], B0 = pb[p], A1 = pa[p + 1], B1 = pb[p + 1];
         pair_force<kPot, kEps0>(A0, B0, sx, sy, sz, eps2, a);
