@@ -632,6 +632,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                         if (j < nf1) put_index(*lbp, pos + int(j), uint32_t(32 + lane) | (j << 6));
                 }
                 __syncwarp();
+#pragma unroll 2
                 for (uint32_t o = lane; o < total; o += 32) {
                     const int q = base + int(o);
                     const uint32_t vv = get_index(*lbp, q);
