@@ -1,5 +1,9 @@
-import os, sys, threading, time
-sys.path.insert(0, "/root/repo")
+"""In-process fused-exchange mesh probe (development): world Simulations on one device, M31 N,
+three sharded all-active steps; prints each rank's walk events per step.
+
+usage: python tools/p2p_local_probe.py N WORLD"""
+import os, sys, threading
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import paper_1811_02761_b200 as g2
 from paper_1811_02761_b200.gravitree import sample_model
