@@ -902,6 +902,8 @@ __global__ void __launch_bounds__(kShardThreads) shard_kernel(const uint32_t* __
                 unsigned long long acc = before;
                 uint32_t g = g0;
                 while (g < g1 && acc + cost[g] <= t) acc += cost[g++];
+                // group g straddles the target: it goes to the side it overshoots least
+                if (g < g1 && acc + cost[g] - t < t - acc) ++g;
                 bnd[r] = g;
             }
         }
