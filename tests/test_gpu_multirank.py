@@ -91,3 +91,21 @@ def test_p2p_ipc_two_processes(tmp_path):
         err = g2.force_error(g["acc"], a.acc)
         assert err["median"] <= 1e-6 and err["p99"] <= 1e-5, err
         assert np.max(np.abs(g["pos"] - a.pos)) < 1e-7
+
+
+def test_bench_two_ranks_one_device(tmp_path):
+    """bench.py's N > 1 path (torchrun, fused peer exchange, max over ranks) end to end, both ranks on
+    cuda:0 through the bench's one-device test mode (gloo process group)."""
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, G2_BENCH_ONE_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29617", os.path.join(root, "bench.py"), "--gpus", "2",
+           "--particles", "262144", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-paper"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(line) == 1, r.stdout
+    d = json.loads(line[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    assert d["config"]["exchange"].startswith("fused")
