@@ -1,5 +1,5 @@
 """GPU: the reference's integrator and walk-trend tests through the device-resident Simulation /
-GravityEngine (test_dynamics.cpp:125-268, acceptance.cpp:78-99 and 193-220), with the reference's
+GravityEngine (test_dynamics.cpp:125-268, acceptance.cpp:78-99 and 193-297), with the reference's
 parameters and thresholds."""
 import math
 
@@ -125,3 +125,49 @@ def test_counter_and_error_trend_over_dacc(g2):
     assert all(a < b for a, b in zip(inter, inter[1:])), inter
     assert all(a < b for a, b in zip(macs, macs[1:])), macs
     assert all(a > b for a, b in zip(med, med[1:])), med
+
+
+def _steady_state_interval(g2, m, p, v, dacc):
+    """acceptance.cpp:222-250: median retuned interval over the second half of 192 steps."""
+    sim = g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 0.02, dacc),
+                        g2.StepScheme(adaptive=False, dt_max=2.0 ** -7), g2.EngineConfig(leaf_cap=1),
+                        g2.TunerConfig(min_interval=1, max_interval=32, initial_interval=8))
+    sim.init()
+    for _ in range(16):
+        sim.step()
+    retunes, last = [], None
+    for _ in range(192):
+        r = sim.step()
+        if r.rebuilt:
+            retunes.append(r.rebuild_interval)
+        last = r.rebuild_interval
+    if not retunes:
+        return last
+    tail = sorted(retunes[len(retunes) // 2:])
+    return tail[len(tail) // 2]
+
+
+def test_acceptance_autotuner_direction(g2):
+    """acceptance.cpp:252-258: the tuner (fed CUDA-event times) rebuilds less often at loose accuracy."""
+    from paper_1811_02761_b200.gravitree import sample_model
+    m, p, v = sample_model("plummer", 8192, 3)
+    assert _steady_state_interval(g2, m, p, v, 2.0 ** -1) > _steady_state_interval(g2, m, p, v, 2.0 ** -12)
+
+
+def test_acceptance_phase_dominance(g2):
+    """acceptance.cpp:260-297: walkTree is the largest phase at 2^17 and 2^20; the calcNode share
+    falls with N."""
+    from paper_1811_02761_b200.gravitree import sample_model
+    share, dominant = {}, {}
+    for n in (1 << 10, 1 << 17, 1 << 20):
+        m, p, v = sample_model("m31", n, 1)
+        sim = g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 0.05, 2.0 ** -9),
+                            g2.StepScheme(adaptive=False, dt_max=2.0 ** -8))
+        sim.set_fixed_rebuild_interval(8)
+        sim.init()
+        t = [sim.step().timings for _ in range(3)]
+        s = {k: sum(getattr(x, k) for x in t) for k in ("walk_tree", "calc_node", "make_tree", "predict", "correct")}
+        share[n] = s["calc_node"] / sum(s.values())
+        dominant[n] = s["walk_tree"] >= max(s.values())
+    assert dominant[1 << 17] and dominant[1 << 20]
+    assert share[1 << 10] > share[1 << 20]
