@@ -90,3 +90,25 @@ def test_sampler_bit_identical_to_reference(ref, model, n):
     b = sample_model(model, n, 1, threads=4)
     for x, y in zip(a, b):
         assert np.array_equal(x, y)
+
+
+def test_product_autotune_matches_reference(ref):
+    """g2_autotune (the Simulation's RebuildTuner logic in libg2, host code: callable without a GPU)
+    against the reference library's autotune_rebuild (rebuild_tuner.cpp:28-61)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from paper_1811_02761_b200.gravitree import lib
+    f = lib().g2_autotune
+    f.restype = C.c_size_t
+    rng = np.random.default_rng(11)
+    hists = [[1.0] * 8, [1.0 + k for k in range(16)], [5.0], list(rng.uniform(0, 3, 11)),
+             list(np.cumsum(rng.uniform(0, 0.2, 40)) + 1.0), [2.0] * 8]
+    for hist in hists:
+        h = np.ascontiguousarray(hist, dtype=np.float64)
+        for bt in (0.0, 1e-4, 10.0, 1e6):
+            for lo, hi, cur in ((1, 128, 8), (1, 32, 8), (2, 64, 13)):
+                got = f(C.c_double(bt), C.c_size_t(len(h)), h.ctypes.data_as(C.c_void_p), C.c_size_t(lo),
+                        C.c_size_t(hi), C.c_size_t(cur))
+                assert got == ref.autotune(bt, hist, lo, hi, cur), (hist, bt, lo, hi, cur)
