@@ -17,8 +17,9 @@ predict -> makeTree (bbox, keys, radix sort, split) -> calcNode -> walkTree
           FP32 CUDA-core peak (148 SM x 128 lanes x 2 x f_max).
 
 `--impl reference` times the reference's CPU implementation (oracle/_ref) of
-the same step on this host's cores, on a bounded sample (all of makeTree and
-calcNode, a 1/S sample of the sink groups for the walk, scaled by S).
+the same step on this host's cores: full, unsampled all-active steps of the
+reference's own stepping loop (integrator.cpp:97-164 with a rebuild every
+step), same metric string, unit and config as this arm.
 """
 import argparse
 import json
@@ -39,6 +40,10 @@ PAPER_V100_S_PER_STEP = 3.3e-2  # PAPER.md:18,191 (block-step average, not all-a
 
 
 def parse():
+    return parse_args_list(None)
+
+
+def parse_args_list(argv):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -48,12 +53,11 @@ def parse():
     ap.add_argument("--model", default="m31")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=0, help="walk 1 of every S groups on the CPU (0: auto)")
     ap.add_argument("--no-paper", action="store_true", help="skip the paper-protocol block-step run")
     ap.add_argument("--paper-steps", type=int, default=32)
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="multi-GPU acceleration exchange: fused walk-epilogue P2P stores, or ncclAllGather")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -135,38 +139,21 @@ def walk_traffic_per_launch():
 
 
 # ------------------------------------------------------------------------- CPU reference
-def cpu_reference_step(mass, pos, vel, amag, sample, threads=0):
-    """One all-active step of the reference (oracle/_ref) on a bounded sample:
-    predict (all), build_structure + refresh (all), evaluate on every S-th sink
-    group (exact reference groups: whole 32-particle chunks of the Morton order),
-    correct (all).  Returns (estimated s/step, phase dict)."""
-    from oracle.refpy import Ref
+DT_STEP = 1.0 / 16  # level-0 step of the bench scheme (StepScheme dt_max = 1/16, fixed_level 0)
+
+
+def metric_name(args):
+    """One metric string for both arms (the driver divides the two only when they match)."""
+    return f"sec/step ({args.model} N={args.n} all-active full step)"
+
+
+def cpu_reference_loop(mass, pos, vel, acc=None, amag=None, threads=0):
+    """The reference's stepping loop on this host (oracle/refpy.RefLoop): every step is one full,
+    UNSAMPLED all-active step through the reference's public API -- predict, build_structure +
+    refresh, evaluate on all N, corrector (integrator.cpp:97-164 with a rebuild every step)."""
+    from oracle.refpy import Ref, RefLoop
     ref = Ref()
-    n = len(mass)
-    t0 = time.perf_counter()
-    p2, v2 = ref.predict(pos, vel, np.zeros_like(pos), 0.0)
-    t_pred = time.perf_counter() - t0
-    eng = ref.engine(eps=EPS, dacc=DACC, threads=threads)
-    t0 = time.perf_counter()
-    eng.build(mass, pos, with_nodes=False)
-    t_make = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    eng.refresh(mass, pos)
-    t_calc = time.perf_counter() - t0
-    tree = eng.tree()
-    groups = np.arange(0, (n + 31) // 32, sample)
-    idx = (groups[:, None] * 32 + np.arange(32)[None, :]).ravel()
-    idx = idx[idx < n]
-    targets = tree.perm[idx].astype(np.uint32)
-    t0 = time.perf_counter()
-    _, _, ev = eng.evaluate(mass, pos, amag, targets=targets)
-    t_walk = (time.perf_counter() - t0) * sample
-    t0 = time.perf_counter()
-    ref.correct(vel, np.zeros_like(pos), amag, np.zeros_like(pos), 0.0)
-    t_corr = time.perf_counter() - t0
-    total = t_pred + t_make + t_calc + t_walk + t_corr
-    return total, {"predict": t_pred, "make_tree": t_make, "calc_node": t_calc, "walk_tree_scaled": t_walk,
-                   "correct": t_corr, "walk_sample_events": ev, "groups_walked": int(len(groups))}
+    return ref, RefLoop(ref, mass, pos, vel, G=1.0, eps=EPS, dacc=DACC, threads=threads, acc=acc, acc_old_mag=amag)
 
 
 def run_reference(args):
@@ -174,34 +161,36 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle.refpy import Ref
-    ref = Ref()
-    threads = ref.lib.gtref_resolve_threads(0)
+    threads = int(Ref().lib.gtref_resolve_threads(0))
     t0 = time.perf_counter()
-    mass, pos, vel = ref.sample_model(args.model, args.n, 1)
+    mass, pos, vel = Ref().sample_model(args.model, args.n, 1)
     t_ic = time.perf_counter() - t0
-    eng = ref.engine(eps=EPS, dacc=DACC, threads=0)
     t0 = time.perf_counter()
-    _, amag, _ = eng.bootstrap(mass, pos)
+    _, loop = cpu_reference_loop(mass, pos, vel, threads=0)  # the reference's bootstrap (Simulation::init)
     t_boot = time.perf_counter() - t0
-    del eng
-    sample = args.cpu_sample or max(1, args.n // (1 << 18))
     for _ in range(args.warmup):
-        cpu_reference_step(mass, pos, vel, amag, sample)
-    times, phases = [], None
+        loop.step(DT_STEP)
+    times, last = [], None
+    t_wall = time.perf_counter()
     for _ in range(args.steps):
-        t, phases = cpu_reference_step(mass, pos, vel, amag, sample)
-        times.append(t)
+        t0 = time.perf_counter()
+        last = loop.step(DT_STEP)
+        times.append(time.perf_counter() - t0)
+    t_wall = time.perf_counter() - t_wall
     v = float(np.mean(times))
-    desc = (f"reference (oracle/_ref) all-active step on {args.model} N={args.n}: predict, makeTree, calcNode "
-            f"and correct on all N; walkTree on 1 of every {sample} sink groups x{sample}; {threads} threads")
+    desc = (f"reference (oracle/_ref, unmodified gravitree) stepping loop on {args.model} N={args.n}: "
+            f"{args.steps} full all-active steps (predict, build_structure, refresh, evaluate on all N, "
+            f"correct), no sampling; {threads} threads")
     print(json.dumps({
-        "impl": "reference", "metric": "sec/step (all-active full step)", "value": v, "unit": "s/step",
+        "impl": "reference", "metric": metric_name(args), "value": v, "unit": "s/step",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args),
-        "cpu_baseline": {"value": v, "unit": "s/step", "cores": int(threads), "kind": "reference", "sample": desc},
+        "cpu_baseline": {"value": v, "unit": "s/step", "cores": threads, "kind": "reference", "sample": desc},
         "e2e": {"value": v, "unit": "s/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "setup_seconds": {"ic": t_ic, "bootstrap": t_boot}, "phases_last_step": phases}))
+        "timed_wall_seconds": t_wall, "setup_seconds": {"ic": t_ic, "bootstrap": t_boot},
+        "phases_last_step": {k: last[k] for k in ("predict", "make_tree", "calc_node", "walk_tree", "correct")},
+        "events_last_step": last["events"]}))
 
 
 def workload_config(args):
@@ -432,20 +421,25 @@ def run_g2(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            from oracle.refpy import Ref
-            amag = sim.system().acc_old_mag
-            sample = args.cpu_sample or max(1, args.n // (1 << 18))  # same sample as the --impl reference arm
-            t, ph = cpu_reference_step(mass, pos, vel, amag, sample)
-            cpu = {"value": t, "unit": "s/step", "cores": int(Ref().lib.gtref_resolve_threads(0)), "kind": "reference",
-                   "sample": f"oracle/_ref (unmodified reference library) on the same M31 N={args.n} input: "
-                             f"predict/makeTree/calcNode/correct on all N, walkTree on every {sample}-th sink group "
-                             f"scaled x{sample}", "phases": ph}
+            # one full, unsampled all-active step of the reference on the same input (~20 s on the
+            # box's 16 cores); the held accelerations come from the g2 state so no bootstrap runs
+            st = sim.system()
+            ref, loop = cpu_reference_loop(mass, pos, vel, acc=st.acc, amag=st.acc_old_mag)
+            ph = loop.step(DT_STEP)
+            cpu = {"value": ph["total"], "unit": "s/step", "cores": int(ref.lib.gtref_resolve_threads(0)),
+                   "kind": "reference",
+                   "sample": f"oracle/_ref (unmodified reference library): ONE full all-active step (predict, "
+                             f"build_structure, refresh, evaluate on all N={args.n}, correct) on the same "
+                             f"{args.model} input, no sampling",
+                   "phases": {k: ph[k] for k in ("predict", "make_tree", "calc_node", "walk_tree", "correct")},
+                   "events": ph["events"]}
+            del loop
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "s/step", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
     if rank == 0:
         out = {
-            "metric": "sec/step (M31 N=2^23 all-active full step), walkTree TFlop/s", "value": per_step,
+            "metric": metric_name(args), "value": per_step,
             "unit": "s/step", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": per_step * 1e3, "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32 walk / f64 tree+integrator", "data": "synthetic (reference sample_model m31, seed 1)",

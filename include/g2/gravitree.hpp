@@ -227,6 +227,12 @@ public:
     const EngineConfig& config() const { return config_; }
 
     TraversalEvents evaluate(ParticleSystem& s, std::span<const std::uint32_t> targets, std::span<double> pot = {}) {
+        // engine.cpp:32-35: an empty target span walks nothing (a null data() would mean "all
+        // particles" at the C ABI), and pot must cover the system (the library writes pot[target])
+        if (!has_tree()) throw data_error("GravityEngine::evaluate: no tree built");
+        if (!pot.empty() && pot.size() != s.n())
+            throw data_error("GravityEngine::evaluate: potential span must cover the system");
+        if (targets.empty()) return {};
         sync_params();
         g2_events e{};
         check(g2_engine_evaluate(h_, s.n(), s.mass.data(), detail::d(s.pos), s.acc_old_mag.data(), targets.size(),
@@ -234,6 +240,9 @@ public:
         return detail::ev(e);
     }
     TraversalEvents evaluate(ParticleSystem& s, std::span<double> pot = {}) {
+        if (!has_tree()) throw data_error("GravityEngine::evaluate: no tree built");
+        if (!pot.empty() && pot.size() != s.n())
+            throw data_error("GravityEngine::evaluate: potential span must cover the system");
         sync_params();
         g2_events e{};
         check(g2_engine_evaluate(h_, s.n(), s.mass.data(), detail::d(s.pos), s.acc_old_mag.data(), 0, nullptr,

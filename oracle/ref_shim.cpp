@@ -17,6 +17,7 @@
 // Status codes: 0 ok, 3 data_error, 4 resource_error, 5 singularity_error.
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -467,6 +468,85 @@ int gtref_sim_step(void* h, double* out8, int* rebuilt, std::uint64_t* events3) 
         events3[1] = r.events.mac_evals;
         events3[2] = r.events.list_pushes;
     });
+}
+
+// ---- all-active stepping loop (bench.py --impl reference / cpu_baseline) ----------------
+// Simulation::step (integrator.cpp:97-164) with every particle at level 0 (StepScheme
+// adaptive=false, fixed_level=0: all particles active every step, dt_block = dt_max) and the
+// rebuild decision forced to "rebuild" -- the reference's own Simulation cannot rebuild every step
+// (rebuild_tuner.hpp:26 requires >= 2 steps), and bench.py's workload rebuilds every step.  Every
+// phase is the reference's public API on a resident ParticleSystem: predict (integrator.cpp:40-45),
+// GravityEngine::build_structure + refresh (engine.cpp), evaluate on all active particles
+// (engine.cpp:31-81) and the corrector loop of integrator.cpp:148-156.  Setup runs the reference's
+// bootstrap (engine.cpp:89-103), as Simulation::init does.
+struct LoopHandle {
+    ParticleSystem system;
+    GravityEngine engine;
+    std::vector<std::uint32_t> active;
+    LoopHandle(GravParams p, EngineConfig c) : engine(p, c) {}
+};
+
+int gtref_loop_create(std::size_t n, const double* mass, const double* pos, const double* vel, const double* acc,
+                      const double* acc_old_mag, double G, double eps, double dacc, unsigned threads, void** out) {
+    return guarded([&] {
+        EngineConfig c;
+        c.threads = threads;
+        auto h = std::make_unique<LoopHandle>(GravParams{G, eps, dacc}, c);
+        load_system(h->system, n, mass, pos, vel, acc, acc_old_mag);
+        h->system.validate();
+        if (!acc) h->engine.bootstrap(h->system);  // Simulation::init (integrator.cpp:69-79)
+        h->active.resize(n);
+        for (std::size_t i = 0; i < n; ++i) h->active[i] = static_cast<std::uint32_t>(i);
+        *out = h.release();
+    });
+}
+
+void gtref_loop_destroy(void* h) { delete static_cast<LoopHandle*>(h); }
+
+// out6: predict, make_tree, calc_node, walk_tree, correct, total seconds; events3
+int gtref_loop_step(void* hv, double dt, double* out6, std::uint64_t* events3) {
+    return guarded([&] {
+        using Clock = std::chrono::steady_clock;
+        auto secs = [](Clock::time_point a) { return std::chrono::duration<double>(Clock::now() - a).count(); };
+        auto* h = static_cast<LoopHandle*>(hv);
+        ParticleSystem& s = h->system;
+        const auto start = Clock::now();
+        auto t0 = Clock::now();
+        predict(s, dt);
+        out6[0] = secs(t0);
+        t0 = Clock::now();
+        h->engine.build_structure(s);
+        out6[1] = secs(t0);
+        t0 = Clock::now();
+        h->engine.refresh(s);
+        out6[2] = secs(t0);
+        std::vector<Vec3> acc_old(s.acc);  // every particle is active
+        t0 = Clock::now();
+        const TraversalEvents ev = h->engine.evaluate(s, h->active);
+        out6[3] = secs(t0);
+        t0 = Clock::now();
+        for (std::size_t i = 0; i < s.n(); ++i) {
+            s.vel[i] += (0.5 * dt) * (s.acc[i] - acc_old[i]);
+            s.acc_old_mag[i] = s.acc[i].norm();
+        }
+        s.time += dt;
+        out6[4] = secs(t0);
+        out6[5] = secs(start);
+        if (events3) {
+            events3[0] = ev.interactions;
+            events3[1] = ev.mac_evals;
+            events3[2] = ev.list_pushes;
+        }
+    });
+}
+
+void gtref_loop_get_state(void* hv, double* pos, double* vel, double* acc, double* acc_old_mag) {
+    const ParticleSystem& s = static_cast<LoopHandle*>(hv)->system;
+    if (pos) store_vec(s.pos, pos);
+    if (vel) store_vec(s.vel, vel);
+    if (acc) store_vec(s.acc, acc);
+    if (acc_old_mag)
+        for (std::size_t i = 0; i < s.n(); ++i) acc_old_mag[i] = s.acc_old_mag[i];
 }
 
 void gtref_sim_get_state(void* h, double* pos, double* vel, double* acc, double* acc_old_mag, std::uint8_t* level,

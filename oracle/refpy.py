@@ -333,6 +333,50 @@ class RefSimulation:
         return {"pos": pos, "vel": vel, "acc": acc, "acc_old_mag": am, "level": lv, "time": t.value}
 
 
+class RefLoop:
+    """All-active stepping loop over the reference's public API (ref_shim.cpp gtref_loop_*):
+    Simulation::step (integrator.cpp:97-164) with every particle at level 0 and a rebuild every
+    step.  acc/acc_old_mag None: the reference's bootstrap runs at construction (untimed)."""
+
+    def __init__(self, ref: Ref, mass, pos, vel, G=1.0, eps=0.0, dacc=2.0 ** -9, threads=0, acc=None,
+                 acc_old_mag=None):
+        self.ref, self.lib = ref, ref.lib
+        mass, pos, vel = _f64(mass), _f64(pos), _f64(vel)
+        self.n = len(mass)
+        self.h = C.c_void_p()
+        acc_p = _f64(acc).ctypes.data_as(C.c_void_p) if acc is not None else None
+        self._keep = (_f64(acc) if acc is not None else None, _f64(acc_old_mag) if acc_old_mag is not None else None)
+        am_p = self._keep[1].ctypes.data_as(C.c_void_p) if acc_old_mag is not None else None
+        if acc is not None:
+            acc_p = self._keep[0].ctypes.data_as(C.c_void_p)
+        ref._chk(self.lib.gtref_loop_create(_sz(self.n), mass.ctypes.data_as(C.c_void_p),
+                                            pos.ctypes.data_as(C.c_void_p), vel.ctypes.data_as(C.c_void_p),
+                                            acc_p, am_p, C.c_double(G), C.c_double(eps), C.c_double(dacc),
+                                            C.c_uint(threads), C.byref(self.h)))
+        self._keep = None
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.gtref_loop_destroy(self.h)
+            self.h = None
+
+    def step(self, dt):
+        out = np.zeros(6)
+        ev = np.zeros(3, np.uint64)
+        self.ref._chk(self.lib.gtref_loop_step(self.h, C.c_double(dt), out.ctypes.data_as(C.c_void_p),
+                                               ev.ctypes.data_as(C.c_void_p)))
+        return {"predict": out[0], "make_tree": out[1], "calc_node": out[2], "walk_tree": out[3], "correct": out[4],
+                "total": out[5],
+                "events": {"interactions": int(ev[0]), "mac_evals": int(ev[1]), "list_pushes": int(ev[2])}}
+
+    def state(self):
+        n = self.n
+        pos, vel, acc, am = np.empty((n, 3)), np.empty((n, 3)), np.empty((n, 3)), np.empty(n)
+        self.lib.gtref_loop_get_state(self.h, pos.ctypes.data_as(C.c_void_p), vel.ctypes.data_as(C.c_void_p),
+                                      acc.ctypes.data_as(C.c_void_p), am.ctypes.data_as(C.c_void_p))
+        return {"pos": pos, "vel": vel, "acc": acc, "acc_old_mag": am}
+
+
 class Oracle:
     """The plain-C restatement (oracle/g2_oracle.c), mirroring Ref's interface."""
 

@@ -531,6 +531,7 @@ int g2_sim_create_from_snapshot(const char* path, double dacc, const g2_step_sch
                                 const g2_tuner_config* t, int device, g2_sim** out) {
     return guarded([&] {
         const g2::SnapshotHeader h = g2::read_snapshot_header(path);
+        g2::check_snapshot_size(path, h);  // before sizing any buffer by the file's count
         const size_t n = size_t(h.n);
         G2_CUDA(cudaSetDevice(device));
         double* buf = nullptr;  // pinned: the reads land where the H2D copies stream from

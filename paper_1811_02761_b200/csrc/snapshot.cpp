@@ -76,8 +76,28 @@ SnapshotHeader read_snapshot_header(const std::string& path) {
     return s;
 }
 
+void check_snapshot_size(const std::string& path, const SnapshotHeader& s) {
+    // an untrusted count: 40 + 56 n must not wrap, and the file must hold the three arrays (the
+    // error is the one read_snapshot would raise, same byte offset, without allocating n first)
+    if (s.n > (uint64_t(SIZE_MAX) - kHeader) / 56) throw SnapshotError(path + ": particle count too large at byte 8");
+    File in(std::fopen(path.c_str(), "rb"));
+    if (!in.f) throw SnapshotError(path + ": cannot open");
+    if (std::fseek(in.f, 0, SEEK_END) != 0) throw SnapshotError(path + ": cannot seek");
+    const long end = std::ftell(in.f);
+    if (end < 0) throw SnapshotError(path + ": cannot seek");
+    const uint64_t size = uint64_t(end), n = s.n;
+    const uint64_t ends[3] = {kHeader + 8 * n, kHeader + 32 * n, kHeader + 56 * n};
+    const char* what[3] = {"mass array", "position array", "velocity array"};
+    uint64_t start = kHeader;
+    for (int k = 0; k < 3; ++k) {
+        if (size < ends[k]) truncated(path, what[k], size_t(start + (size > start ? (size - start) / 8 * 8 : 0)));
+        start = ends[k];
+    }
+}
+
 SnapshotHeader read_snapshot(const std::string& path, double* mass, double* pos, double* vel, size_t cap) {
     const SnapshotHeader s = read_snapshot_header(path);
+    check_snapshot_size(path, s);
     if (s.n > cap) throw SnapshotError(path + ": particle count exceeds the caller's buffers");
     File in(std::fopen(path.c_str(), "rb"));
     if (!in.f) throw SnapshotError(path + ": cannot open");

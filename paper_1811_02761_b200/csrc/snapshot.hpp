@@ -18,6 +18,8 @@ struct SnapshotHeader {
 };
 
 SnapshotHeader read_snapshot_header(const std::string& path);
+// throws unless 40 + 56 n fits size_t and the file holds all three arrays (untrusted n)
+void check_snapshot_size(const std::string& path, const SnapshotHeader& h);
 // mass[n], pos[3n], vel[3n] into the caller's buffers (cap = their particle capacity)
 SnapshotHeader read_snapshot(const std::string& path, double* mass, double* pos, double* vel, size_t cap);
 void write_snapshot(const std::string& path, size_t n, const double* mass, const double* pos, const double* vel,

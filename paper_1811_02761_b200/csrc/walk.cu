@@ -27,6 +27,7 @@
 //     (group, cells) batches, which split the heavy-tailed "whole-system"
 //     groups across warps.  Partial accelerations are combined
 //     with FP32 atomics.
+#include <cfloat>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -146,6 +147,11 @@ __device__ __forceinline__ f2 sub2(f2 a, f2 b) {
     asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
     return d;
 }
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
 __device__ __forceinline__ f2 mul2(f2 a, f2 b) {
     f2 d;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
@@ -222,19 +228,32 @@ struct Acc2 {
     float ph;
 };
 
-template <bool kPot, bool kEps0>
+// kGuard: eps^2 rounds below FLT_MIN in FP32 (eps == 0 included): a zero separation (the self pair,
+// or coincident particles) contributes nothing (traversal.cpp:73).  kPot: the potential term is
+// dropped exactly when the UN-softened separation is zero, |d|^2 == 0 (traversal.cpp:78), not when
+// r^2 rounds to eps^2.  Both need |d|^2 on its own; the plain force path folds eps^2 into the chain.
+template <bool kPot, bool kGuard>
 __device__ __forceinline__ void pair_force(const ulonglong2 A, const ulonglong2 B, f2 sx, f2 sy, f2 sz, f2 eps2,
                                            Acc2& a) {
     const f2 dx = sub2(A.x, sx), dy = sub2(A.y, sy), dz = sub2(B.x, sz);
-    f2 r2 = fma2(dx, dx, eps2);
-    r2 = fma2(dy, dy, r2);
-    r2 = fma2(dz, dz, r2);
-    float r0, r1;
+    f2 r2, d2 = 0;
+    if (kPot || kGuard) {
+        d2 = mul2(dx, dx);
+        d2 = fma2(dy, dy, d2);
+        d2 = fma2(dz, dz, d2);
+        r2 = kGuard ? d2 : add2(d2, eps2);
+    } else {
+        r2 = fma2(dx, dx, eps2);
+        r2 = fma2(dy, dy, r2);
+        r2 = fma2(dz, dz, r2);
+    }
+    float r0, r1, q0 = 0.f, q1 = 0.f;
     upk(r2, r0, r1);
+    if (kPot || kGuard) upk(d2, q0, q1);
     float i0 = rsqrt_ftz(r0), i1 = rsqrt_ftz(r1);
-    if (kEps0) {  // r2 == 0 self term contributes nothing (traversal.cpp:73)
-        i0 = r0 > 0.0f ? i0 : 0.0f;
-        i1 = r1 > 0.0f ? i1 : 0.0f;
+    if (kGuard) {
+        i0 = q0 > 0.0f ? i0 : 0.0f;
+        i1 = q1 > 0.0f ? i1 : 0.0f;
     }
     const f2 inv = pk(i0, i1);
     const f2 mi = mul2(B.y, inv);
@@ -242,11 +261,10 @@ __device__ __forceinline__ void pair_force(const ulonglong2 A, const ulonglong2 
     a.x = fma2(f, dx, a.x);
     a.y = fma2(f, dy, a.y);
     a.z = fma2(f, dz, a.z);
-    if (kPot) {  // self potential excluded (traversal.cpp:78)
-        float m0, m1, e0, e1;
+    if (kPot) {
+        float m0, m1;
         upk(mi, m0, m1);
-        upk(eps2, e0, e1);
-        a.ph -= (r0 - e0 > 0.0f ? m0 : 0.0f) + (r1 - e1 > 0.0f ? m1 : 0.0f);
+        a.ph -= (q0 > 0.0f ? m0 : 0.0f) + (q1 > 0.0f ? m1 : 0.0f);
     }
 }
 
@@ -1011,7 +1029,9 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
     }
     G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi, b.shard, gs);
     G2_COUNT(1), walk_init_kernel<<<1, 32, 0, s>>>(b);
-    const bool eps0 = p.eps == 0.0;
+    // the guarded flush whenever eps^2 is not a normal FP32 number (eps == 0 included): with eps^2
+    // flushed to zero the self pair would otherwise meet rsqrt(0) = inf and 0 * inf = NaN
+    const bool eps0 = !(float(p.eps * p.eps) >= FLT_MIN);
     const bool check = b.level_count != nullptr;
     if (check) {
         if (with_pot)

@@ -295,6 +295,10 @@ class GravityEngine:
         if targets is not None:
             tg = np.ascontiguousarray(targets, dtype=np.uint32)
             nt = len(tg)
+            if nt == 0:  # engine.cpp:35: nothing to walk (a null pointer would mean "all" at the C ABI)
+                if not self.has_tree():
+                    raise DataError("GravityEngine::evaluate: no tree built")
+                return TraversalEvents()
         pot = None
         if pot_out is not None:
             pot = np.ascontiguousarray(pot_out, dtype=np.float64)
@@ -496,6 +500,8 @@ def read_snapshot(path) -> Snapshot:
     """read_snapshot (snapshot.cpp:97-121): DataError with the reference's byte-offset messages."""
     n, t, G, eps = C.c_size_t(), C.c_double(), C.c_double(), C.c_double()
     _chk(_lib.g2_snapshot_info(str(path).encode(), C.byref(n), C.byref(t), C.byref(G), C.byref(eps)))
+    if 40 + 56 * n.value > os.path.getsize(path):  # untrusted count: fail before allocating n particles
+        _chk(_lib.g2_read_snapshot(str(path).encode(), C.c_size_t(0), None, None, None, None, None, None, None))
     mass, pos, vel = np.empty(n.value), np.empty((n.value, 3)), np.empty((n.value, 3))
     _chk(_lib.g2_read_snapshot(str(path).encode(), C.c_size_t(n.value), _ptr(mass), _ptr(pos), _ptr(vel), None,
                                None, None, None))

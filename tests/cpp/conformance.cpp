@@ -242,6 +242,20 @@ TEST_CASE(engine_contracts, "config and call-order errors, count_ops=false (engi
     eng.build(s);
     CHECK(eng.has_tree());
     CHECK(eng.evaluate(s) == gravitree::TraversalEvents{});
+    // engine.cpp:33-35: an empty target span walks nothing and leaves acc alone; a potential span
+    // that does not cover the system is a data_error (before any walk)
+    gravitree::GravityEngine counted(gravitree::GravParams{});
+    counted.build(s);
+    for (auto& a : s.acc) a = Vec3{7.0, 7.0, 7.0};
+    const std::vector<std::uint32_t> none;
+    CHECK(counted.evaluate(s, std::span<const std::uint32_t>(none)) == gravitree::TraversalEvents{});
+    bool untouched = true;
+    for (const auto& a : s.acc) untouched = untouched && a.x == 7.0 && a.y == 7.0 && a.z == 7.0;
+    CHECK(untouched);
+    std::vector<double> short_pot(10);
+    const std::vector<std::uint32_t> some{1, 2, 3};
+    CHECK(throws<gravitree::data_error>([&] { counted.evaluate(s, std::span<const std::uint32_t>(some), short_pot); }));
+    CHECK(throws<gravitree::data_error>([&] { counted.evaluate(s, std::span<double>(short_pot)); }));
 }
 
 // ---- test_dynamics.cpp -------------------------------------------------------------------------

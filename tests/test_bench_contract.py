@@ -40,3 +40,23 @@ def test_reference_arm_line_contract():
     assert d["impl"] == "reference" and d["unit"] == "s/step" and d["higher_is_better"] is False
     assert d["cpu_baseline"]["value"] == d["value"] and d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_both_arms_share_metric_unit_config(ref):
+    """The reference arm, run here on a small input, prints the SAME metric string, unit and config as
+    the g2 arm would for the same arguments (the driver divides the two only when they match), and its
+    value is a measured full step: steps x value fits inside the timed wall clock (no extrapolation)."""
+    import subprocess
+    import sys
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--n", "4096",
+                          "--model", "plummer", "--steps", "2", "--warmup", "3"], capture_output=True, text=True,
+                         timeout=600, check=True).stdout.strip().splitlines()[-1]
+    d = json.loads(out)
+    sys.path.insert(0, ROOT)
+    import bench
+    args = bench.parse_args_list(["--n", "4096", "--model", "plummer", "--steps", "2", "--warmup", "3"])
+    assert d["metric"] == bench.metric_name(args)
+    assert d["config"] == bench.workload_config(args)
+    assert d["unit"] == "s/step" and d["higher_is_better"] is False
+    assert d["steps"] * d["value"] <= d["timed_wall_seconds"] * (1 + 1e-6)
+    assert d["events_last_step"]["interactions"] > 0

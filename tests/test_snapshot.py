@@ -82,6 +82,44 @@ def test_header_errors_match_reference(g2, ref, tmp_path):
         g2.read_snapshot(tmp_path / "missing.octf")
 
 
+@pytest.mark.parametrize("n", [2 ** 61 + 1, 2 ** 64 - 1, 2 ** 40, 51])
+def test_untrusted_particle_count(g2, ref, tmp_path, n):
+    """A crafted header count must fail cleanly before anything is sized by it: 40 + 56 n wraps
+    size_t for n = 2^61 + 1; otherwise the file is simply too short (the reference's truncation
+    message, same byte offset, when the reference can allocate n particles)."""
+    from oracle.refpy import RefError
+    s = system(g2, n=50)
+    full = tmp_path / "full.octf"
+    g2.write_snapshot(full, s)
+    d = bytearray(full.read_bytes())
+    d[8:16] = n.to_bytes(8, "little")
+    f = tmp_path / "crafted.octf"
+    f.write_bytes(bytes(d))
+    with pytest.raises(g2.DataError) as eg:
+        g2.read_snapshot(f)
+    if n == 51:
+        with pytest.raises(RefError) as er:
+            ref.read_snapshot(f)
+        assert str(eg.value) == er.value.msg
+    if n > (2 ** 64 - 1 - 40) // 56:
+        assert "too large" in str(eg.value)
+    else:
+        assert "truncated" in str(eg.value)
+
+
+@pytest.mark.gpu
+def test_simulation_from_snapshot_untrusted_count(g2, tmp_path):
+    s = system(g2, n=50)
+    full = tmp_path / "full.octf"
+    g2.write_snapshot(full, s)
+    d = bytearray(full.read_bytes())
+    d[8:16] = (2 ** 61 + 1).to_bytes(8, "little")
+    f = tmp_path / "crafted.octf"
+    f.write_bytes(bytes(d))
+    with pytest.raises(g2.DataError, match="too large"):
+        g2.Simulation.from_snapshot(f, dacc=2.0 ** -9)
+
+
 @pytest.mark.gpu
 def test_simulation_from_snapshot(g2, tmp_path):
     mass, pos, _ = plummer(20000, seed=8)

@@ -1,5 +1,6 @@
-"""Launch-list driver (development): M31 N block steps with dt_max = 1 and a fixed rebuild
-interval; run under `ncu --metrics gpu__time_duration.sum` to see one step's kernels."""
+"""Launch-list / walk-timeline driver (development): M31 N block steps with dt_max = 1 and a fixed
+rebuild interval of 2.  Run under `ncu --metrics gpu__time_duration.sum` to see one step's kernels,
+or with G2_WALK_TRACE=<file> for the per-task walk timeline (tools/trace_stats.py)."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1811_02761_b200 as g2
