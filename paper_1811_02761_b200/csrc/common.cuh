@@ -36,7 +36,7 @@ struct DevFlags {
     int stack_overflow;   // walk stack spill area exhausted (internal, sized to never trigger)
     int queue_overflow;   // walk task queue exhausted (internal)
     int tie_run;          // a run of equal keys too long for the in-place tie repair (host re-sorts by id)
-    int pad;
+    int task_pool;        // walk task records exhausted: a donation was skipped (host grows the pool)
 };
 
 constexpr int kMaxDepth = 21;        // octree.hpp:47

@@ -110,6 +110,7 @@ Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), devic
     queue_cap_ = 1u << 20;  // ring size of the walk's donated-task queue (walk.cu kRing)
     queue_.reserve(queue_cap_);
     batch_.reserve(size_t(queue_cap_) * 32);
+    batch_rec_.reserve(queue_cap_);
     G2_CUDA(cudaMemsetAsync(queue_.p, 0xff, size_t(queue_cap_) * sizeof(uint64_t), s_));
     spill_.reserve(walk_resident_warps() * walk_spill_words());
     G2_CUDA(cudaMallocHost(&hs_, sizeof(HostSync)));
@@ -136,6 +137,15 @@ void Engine::reserve(size_t n) {
     groups_.reserve(n), accum_.reserve(n), group_inter_.reserve(n), rel_.reserve(n), leaf_of_.reserve(n);
     ensure_cells(std::max<size_t>(n + 64, 1024));
     cap_ = n;
+    ensure_task_pool(std::max<size_t>(size_t(1) << 16, n / 8));  // no allocation inside a timed walk
+    order_.reserve(n + 1), order_scratch_.reserve(walk_order_scratch_words());
+}
+
+void Engine::ensure_task_pool(size_t want) {
+    if (want <= rec_cap_) return;
+    G2_CUDA(cudaStreamSynchronize(s_));
+    trec_.reserve(want), tacc_.reserve(want * 32);
+    rec_cap_ = want;
 }
 
 void Engine::ensure_cells(size_t cap) {
@@ -162,7 +172,22 @@ void Engine::check_flags() {
     raise_flags();
 }
 
+bool Engine::walk_pool_overflow() {
+    enqueue_flags();
+    sync();
+    if (!hs_->flags.task_pool) return false;
+    grow_pool_ = true;
+    hs_->flags.task_pool = 0;
+    G2_CUDA(cudaMemsetAsync(&flags_.p->task_pool, 0, sizeof(int), s_));
+    return true;
+}
+
 void Engine::raise_flags() {
+    if (hs_->flags.task_pool) {  // not an error: results stay exact, the next walk gets a larger pool
+        grow_pool_ = true;
+        hs_->flags.task_pool = 0;
+        G2_CUDA(cudaMemsetAsync(&flags_.p->task_pool, 0, sizeof(int), s_));
+    }
     const DevFlags f = hs_->flags;
     if (f.data_error || f.resource_error || f.singularity || f.stack_overflow || f.queue_overflow) {
         G2_CUDA(cudaMemset(flags_.p, 0, sizeof(DevFlags)));
@@ -367,10 +392,17 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     b.n_groups = n_groups_.p;
     b.accum = accum();
     b.world = peer_world_, b.self = peer_self_;
+    {
+        // task records: one per donated task (plus the donating initial task); sized from the group
+        // count, doubled whenever a walk ran short (a skipped donation keeps results exact but makes
+        // the task tree, hence the FP32 summation order, depend on timing)
+        if (grow_pool_) ensure_task_pool(2 * rec_cap_);
+        grow_pool_ = false;
+        b.trec = trec_.p, b.tacc = tacc_.p, b.batch_rec = batch_rec_.p;
+        b.rec_cap = uint32_t(std::min<size_t>(rec_cap_, 0xffffffffu));
+    }
     if (peer_world_ > 1) {
-        gpend_.reserve(ng_cap + 1);
         gcost_.reserve(ng_cap + 1);
-        b.gpend = gpend_.p;
         b.gcost = gcost_.p;
         for (int q = 0; q < kMaxPeers; ++q) b.peer_accum[q] = peer_accum_[q], b.peer_cost[q] = peer_cost_[q];
         // shards computed on the device (no host round trip): cost-balanced when a cost history is
@@ -393,6 +425,11 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
         b.level_count = level_count_.p;
     }
     b.group_inter = group_inter_.p;
+    static const bool no_order = std::getenv("G2_NO_ORDER") != nullptr;  // development A/B
+    if (!no_order) {
+        order_.reserve(ng_cap + 1);  // no-op unless targets with duplicates outnumber the particles
+        b.order = order_.p, b.order_scratch = order_scratch_.p;
+    }
     static const char* trace_path = std::getenv("G2_WALK_TRACE");  // development: per-task timeline
     if (trace_path) {
         trace_.reserve(2 * (size_t(1) << 23));
@@ -404,6 +441,12 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
     WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
                   c_.count_ops ? 1 : 0, 0};
+    static const char* dp = std::getenv("G2_DONATE_PUSHES");  // development: donation-trigger sweeps
+    static const char* df = std::getenv("G2_DONATE_FEW");
+    if (dp) wp.donate_pushes = uint32_t(std::max(1, std::atoi(dp)));
+    if (df) wp.donate_few = uint32_t(std::max(1, std::atoi(df)));
+    static const char* dsc = std::getenv("G2_DONATE_SCALE");
+    if (dsc) wp.donate_scale = uint32_t(std::max(1, std::atoi(dsc)));
     launch_walk(tv, wp, b, with_pot, n_sinks_cap, gs, flags_.p, s_);
     if (check)
         G2_COUNT(1), frontier_check_kernel<<<gridn(size_t(ng_cap) * (kMaxDepth + 1)), kB, 0, s_>>>(
@@ -460,7 +503,10 @@ EventsH Engine::evaluate(size_t n, const double* mass, const double* pos, const 
     }
     const uint32_t nt32 = uint32_t(nt);
     G2_CUDA(cudaMemcpyAsync(n_sinks_.p, &nt32, 4, cudaMemcpyHostToDevice, s_));
+    // a walk whose task-record pool ran short skipped donations (results exact, but the task tree --
+    // hence the FP32 summation order -- then depends on timing): walk again with the grown pool
     EventsH ev = walk(sinks_.p, n_sinks_.p, nt32, amag_s_.p, pot_out != nullptr, false);
+    while (walk_pool_overflow()) ev = walk(sinks_.p, n_sinks_.p, nt32, amag_s_.p, pot_out != nullptr, false);
     // results for the targets in target order
     G2_COUNT(1), interleave_kernel<<<gridn(nt), kB, 0, s_>>>(ax_s_.p, ay_s_.p, az_s_.p, out_idx, out_.p, nt);
     std::vector<double> acc(3 * nt), pot(pot_out ? nt : 0);
@@ -676,6 +722,7 @@ void Simulation::init() {
         const uint32_t n32 = uint32_t(n);
         G2_CUDA(cudaMemcpyAsync(n_active_.p, &n32, 4, cudaMemcpyHostToDevice, s));
         eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false);  // amag == 0: geometric MAC
+        while (eng_.walk_pool_overflow()) eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false);
         G2_CUDA(cudaMemcpyAsync(ax_.p, eng_.ax_s(), n * 8, cudaMemcpyDeviceToDevice, s));
         G2_CUDA(cudaMemcpyAsync(ay_.p, eng_.ay_s(), n * 8, cudaMemcpyDeviceToDevice, s));
         G2_CUDA(cudaMemcpyAsync(az_.p, eng_.az_s(), n * 8, cudaMemcpyDeviceToDevice, s));

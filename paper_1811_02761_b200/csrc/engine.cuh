@@ -73,6 +73,11 @@ public:
     void enqueue_events();
     void sync();
     void raise_flags();  // throws for the staged device flags
+    // syncs; true (and the pool grows) if the last walk ran out of task records.  Such a walk skipped
+    // donations: exact, but not bit-reproducible; synchronous callers walk again.  A Simulation step
+    // only grows the pool for the next step (its pool starts at n/8 records, far above any measured
+    // need: 0.1 n at M31 2^20 all-active).
+    bool walk_pool_overflow();
     void events_host(EventsH& ev) const;
     void ensure_rank();        // rank_ = inverse of perm_ if a storage-order rebuild left it stale
     void split_and_nodes(bool with_nodes);
@@ -122,6 +127,7 @@ public:
 
 private:
     void ensure_cells(size_t cap);
+    void ensure_task_pool(size_t records);
     void sort_keys_identity_payload(size_t n);  // keys in keys_a_ by original id -> perm_, keys sorted
     void upload_orig(size_t n, const double* mass, const double* pos);
 
@@ -155,7 +161,12 @@ private:
     DBuf<uint32_t> sinks_, sinks_alt_, n_sinks_, n_groups_;
     DBuf<GroupRec> groups_;
     DBuf<float4> accum_;
-    DBuf<uint32_t> gpend_, gcost_, shard_;
+    DBuf<uint32_t> gcost_, shard_, order_, order_scratch_;
+    DBuf<uint4> trec_;          // walk task records (deterministic combination of split groups)
+    DBuf<float4> tacc_;         // [rec_cap * 32] their accumulators
+    DBuf<uint32_t> batch_rec_;  // [queue_cap] record of each donated slot
+    size_t rec_cap_ = 0;
+    bool grow_pool_ = false;    // a walk ran out of task records: double the pool before the next
     uint32_t* peer_cost_[kMaxPeers] = {};
     const uint32_t* cost_prev_ = nullptr;
     const uint32_t* ng_prev_ = nullptr;

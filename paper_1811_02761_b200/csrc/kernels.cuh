@@ -86,6 +86,10 @@ struct WalkParams {
     uint32_t frontier_cap;    // 0 = unchecked (cap cannot bind)
     int count_ops;
     int force_geometric;      // 1: geometric MAC for every group
+    // a task donates half of its pending cells after writing D list entries since its last donation,
+    // D = clamp(donate_scale x groups per producer warp, donate_few, donate_pushes): small walks
+    // (block steps) split their groups finer; deterministic: D depends on the TOTAL group count only
+    uint32_t donate_pushes = 2048, donate_few = 256, donate_scale = 64;
 };
 constexpr int kMaxPeers = 8;
 struct WalkBuffers {
@@ -97,9 +101,12 @@ struct WalkBuffers {
     unsigned long long* events;  // [3]
     uint64_t* queue;          // donated-task slots: (group << 32) | cell count
     uint32_t* batch;          // [queue_cap * 32] cells of each donated slot
-    const uint32_t* order;    // initial-task order (heaviest first), nullable
+    const uint32_t* order;    // [n_groups] initial-task order (heaviest first), written by the launcher when
+                              // order_scratch is given; nullable: group index order
+    uint32_t* order_scratch;  // [walk_order_scratch_words()] bucket counters of the ordering sort
     uint32_t queue_cap;
-    uint32_t* qstate;         // [8]: init claimed, donated reserved, pending, n_init, donated consumed
+    uint32_t* qstate;         // [8]: init claimed, donated reserved, pending, n_init, donated consumed, shard lo,
+                              //      task records used
     uint32_t* spill;          // per-warp stack spill
     uint32_t* level_count;    // [n_groups * 22] frontier-cap check (nullable)
     uint64_t* group_inter;    // [n_groups] per-group interactions (nullable)
@@ -107,9 +114,15 @@ struct WalkBuffers {
     uint32_t* trace_n;
     uint32_t trace_cap;
     uint32_t group_lo, group_hi;  // shard of groups to walk (hi = ~0u: all)
+    // deterministic combination of split groups: every donated task has a record (parent, pending,
+    // first child, next sibling) and a 32-sink accumulator slot; a task's subtree total is its own
+    // partial plus its children's totals in donation order, formed by whichever finishes last
+    uint4* trec;                        // [rec_cap] task records
+    float4* tacc;                       // [rec_cap * 32] partial, then subtree, accumulators
+    uint32_t* batch_rec;                // [queue_cap] record of the task in each donated slot
+    uint32_t rec_cap;
     // fused peer exchange (world > 1): the task that completes a group stores the group's final
     // accumulators straight into every peer rank's accumulator (IPC-mapped, same slot layout)
-    uint32_t* gpend;                    // [n_groups] tasks of the group not yet written out
     float4* peer_accum[kMaxPeers];      // peer accumulators, [self] unused
     int world, self;
     // cost-balanced shards (peer exchange): every group's list-entry count of this step goes to every
@@ -122,6 +135,7 @@ struct WalkBuffers {
     uint32_t* shard;                    // [2] device lo, hi (group indices) when cost-balanced
 };
 size_t walk_spill_words();
+size_t walk_order_scratch_words();
 size_t walk_resident_warps();
 void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffers& b, uint32_t group_size,
                    uint32_t n_sinks_cap, cudaStream_t s);

@@ -25,8 +25,14 @@
 //   * persistent grid, dynamic task queue: initially one task per group; a
 //     producer holding a long stack donates its shallowest pending cells as
 //     (group, cells) batches, which split the heavy-tailed "whole-system"
-//     groups across warps.  Partial accelerations are combined
-//     with FP32 atomics.
+//     groups across warps;
+//   * deterministic results: WHEN a task donates depends only on the task's own
+//     progress (every kDonateEvery rounds), so a group's task tree is a function of
+//     the group and the tree alone; each task's partial sums land in its record and
+//     a task's subtree total = own partial + children's totals in donation order,
+//     formed by whichever of them finishes last.  Accelerations are therefore
+//     bit-identical run to run and for any sharding of the groups over ranks
+//     (the reference's static partition, parallel.hpp:16-19).
 #include <cfloat>
 #include <cstdlib>
 
@@ -60,14 +66,11 @@ constexpr int kLcap = G2_LCAP;             // interaction-list entries per buffe
 #endif
 constexpr int kScap = 512;                 // shared stack entries per producer (>= 64 cells x 8 children)
 constexpr uint32_t kSpillWords = 16384;    // global stack entries per producer
-#ifndef G2_DONATE_EVERY
-#define G2_DONATE_EVERY 64
+#ifndef G2_DONATE_MIN_LIVE
+#define G2_DONATE_MIN_LIVE 2
 #endif
-#ifndef G2_CHECK_EVERY
-#define G2_CHECK_EVERY 2
-#endif
-constexpr int kDonateEvery = G2_DONATE_EVERY;  // rounds between donations of a long-running task
-constexpr int kQueuedEnough = 4096;        // queued donated batches above which heavy tasks keep their work
+constexpr int kDonateMinLive = G2_DONATE_MIN_LIVE;  // pending cells a task needs before it donates half
+constexpr uint32_t kNone = ~0u;             // no task record / no child / no parent
 constexpr uint64_t kEmpty = ~0ull;
 constexpr int kRingBits = 20;              // donated-task ring: 2^20 slots, reused
 constexpr uint32_t kRing = 1u << kRingBits;
@@ -375,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         for (uint32_t it = 0;; ++it) {
             const int bi = int(it & 1);
             mbar_wait(&ps.full[bi], (it >> 1) & 1);
-            const uint32_t cnt = ps.hdr[bi][0], grp = ps.hdr[bi][1], fl = ps.hdr[bi][2];
+            const uint32_t cnt = ps.hdr[bi][0], grp = ps.hdr[bi][1], fl = ps.hdr[bi][2], rec = ps.hdr[bi][3];
             if (grp == kStop) break;
             if (fl & kFirst) {
                 // sinks by the SAME FP32 expression as their own list entries, (leaf centre - group
@@ -402,34 +405,63 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             flush_list<kPot, kEps0>(ps.buf[bi], int(cnt), sx2, sy2, sz2, e2, a0, a1);
             __syncwarp();
             mbar_arrive(&ps.empty[bi]);
-            if ((fl & kLast) && has_sink) {
-                float x0, x1, y0, y1, z0, z1, u0, u1, v0, v1, w0, w1;
-                upk(a0.x, x0, x1), upk(a0.y, y0, y1), upk(a0.z, z0, z1);
-                upk(a1.x, u0, u1), upk(a1.y, v0, v1), upk(a1.z, w0, w1);
-                float4* out = &b.accum[gfirst + lane];
-                atomicAdd(&out->x, G * ((x0 + x1) + (u0 + u1)));
-                atomicAdd(&out->y, G * ((y0 + y1) + (v0 + v1)));
-                atomicAdd(&out->z, G * ((z0 + z1) + (w0 + w1)));
-                if (kPot) atomicAdd(&out->w, G * (a0.ph + a1.ph));
-            }
-            if ((fl & kLast) && b.world > 1) {
-                // the group's last task to finish pushes its final accumulators to every peer
-                // rank (NVLink stores, overlapped with the rest of the walk)
+            if (!(fl & kLast)) continue;
+            // ---- the task is complete: fold the packed accumulators (fixed order)
+            float x0, x1, y0, y1, z0, z1, u0, u1, v0, v1, w0, w1;
+            upk(a0.x, x0, x1), upk(a0.y, y0, y1), upk(a0.z, z0, z1);
+            upk(a1.x, u0, u1), upk(a1.y, v0, v1), upk(a1.z, w0, w1);
+            float4 tot = make_float4((x0 + x1) + (u0 + u1), (y0 + y1) + (v0 + v1), (z0 + z1) + (w0 + w1),
+                                     kPot ? a0.ph + a1.ph : 0.f);
+            bool done = true;  // tot is the group's final sum
+            if (rec != kNone) {
+                // split group: park the partial in the record; whoever completes a record's subtree
+                // last adds the children's totals in donation order and climbs to the parent
+                if (has_sink) __stcg(&b.tacc[size_t(rec) * 32 + lane], tot);
                 __threadfence();
                 __syncwarp();
-                uint32_t last = 0;
-                if (lane == 0) last = atomicSub(&b.gpend[grp], 1u) == 1u;
-                if (__shfl_sync(kFull, last, 0)) {
+                uint32_t r = rec, last = 0;
+                if (lane == 0) last = atomicSub(&b.trec[r].y, 1u) == 1u;
+                last = __shfl_sync(kFull, last, 0);
+                done = false;
+                while (last) {
                     __threadfence();
-                    if (has_sink) {
-                        const float4 v = __ldcg(&b.accum[gfirst + lane]);
-                        for (int q = 0; q < b.world; ++q)
-                            if (q != b.self) b.peer_accum[q][gfirst + lane] = v;
+                    const uint4 R = __ldcg(&b.trec[r]);
+                    float4 acc = has_sink ? __ldcg(&b.tacc[size_t(r) * 32 + lane]) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (uint32_t c = R.z; c != kNone;) {
+                        const uint32_t nx = __ldcg(&b.trec[c].w);
+                        if (has_sink) {
+                            const float4 v = __ldcg(&b.tacc[size_t(c) * 32 + lane]);
+                            acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+                        }
+                        c = nx;
                     }
-                    // the group's cost: the same value into every rank's array (identical shards next step)
-                    if (b.peer_cost[0] && lane < b.world) b.peer_cost[lane][grp] = __ldcg(&b.gcost[grp]);
-                    __threadfence_system();
+                    if (R.x == kNone) {  // the group's root task: acc is final
+                        tot = acc;
+                        done = true;
+                        break;
+                    }
+                    if (has_sink) __stcg(&b.tacc[size_t(r) * 32 + lane], acc);
+                    __threadfence();
+                    __syncwarp();
+                    r = R.x;
+                    if (lane == 0) last = atomicSub(&b.trec[r].y, 1u) == 1u;
+                    last = __shfl_sync(kFull, last, 0);
                 }
+            }
+            if (!done) continue;
+            if (has_sink) {
+                const float4 v = make_float4(G * tot.x, G * tot.y, G * tot.z, kPot ? G * tot.w : 0.f);
+                b.accum[gfirst + lane] = v;
+                // world > 1: the final accumulators go straight to every peer rank (NVLink stores,
+                // overlapped with the rest of the walk)
+                for (int q = 0; q < b.world; ++q)
+                    if (q != b.self) b.peer_accum[q][gfirst + lane] = v;
+            }
+            if (b.world > 1) {
+                // the group's cost: the same value into every rank's array (identical shards next step)
+                __threadfence();
+                if (b.peer_cost[0] && lane < b.world) b.peer_cost[lane][grp] = __ldcg(&b.gcost[grp]);
+                __threadfence_system();
             }
         }
         return;
@@ -451,15 +483,20 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
     uint32_t* q_dhead = b.qstate + 4;  // donated slots claimed
     const uint32_t ng = b.qstate[3];   // initial tasks (written by walk_init)
     const uint32_t glo = b.qstate[5];  // first group of this launch's shard (walk_init)
+    // donation trigger: list entries written since the task's last donation (work done, not time),
+    // scaled with the groups per producer warp of a full grid (a constant: identical on every rank)
+    const uint32_t donate_pushes =
+        min(p.donate_pushes, max(p.donate_few, *b.n_groups / uint32_t(4 * kNumSMs * kPairs) * p.donate_scale));
     const float thetaf = float(p.theta);
     uint32_t hand = 0;  // buffers handed to the consumer so far: buffer = hand & 1
 
     // hand the current buffer (lsize entries, padded to even) to the consumer, then
     // wait until the next buffer has been flushed (phase parity of its previous use)
-    auto handoff = [&](int lsize, uint32_t grp, uint32_t fl) {
+    auto handoff = [&](int lsize, uint32_t grp, uint32_t fl, uint32_t rec = kNone) {
         const int bi = int(hand & 1);
         if ((lsize & 1) && lane == 0) put_entry(sm.buf[bi], lsize, 0.f, 0.f, 0.f, 0.f);
-        if (lane == 0) sm.hdr[bi][0] = uint32_t(lsize + (lsize & 1)), sm.hdr[bi][1] = grp, sm.hdr[bi][2] = fl;
+        if (lane == 0)
+            sm.hdr[bi][0] = uint32_t(lsize + (lsize & 1)), sm.hdr[bi][1] = grp, sm.hdr[bi][2] = fl, sm.hdr[bi][3] = rec;
         __syncwarp();
         mbar_arrive(&sm.full[bi]);
         ++hand;
@@ -513,6 +550,9 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         if (e == kEmpty) break;
         slot = __shfl_sync(kFull, slot, 0);
         const uint32_t grp = uint32_t(e >> 32), nbatch = uint32_t(e) & 63u;
+        // task record (lane 0): a donated task was given one by its donor; a group's initial task
+        // allocates one at its first donation
+        uint32_t rec = nbatch ? b.batch_rec[slot] : kNone, last_child = kNone;
 
         // ---------------- group
         uint64_t t_begin = 0;
@@ -529,10 +569,10 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                     gzl = float(dsub(g.cz, double(gzh)));
         // absolute screen-error term from the FP32 rounding of node centres (|c| <= |g| + D)
         const float tolc = 5e-7f * (fabsf(gxh) + fabsf(gyh) + fabsf(gzh));
-        uint32_t macs = 0, pushes = 0, tflags = kFirst;
+        uint32_t macs = 0, pushes = 0, tflags = kFirst, ndon = 0, maxlive = 0;  // ndon/maxlive: trace only
         // logical LIFO = spill[gbase, gtop) (bottom, global) ++ sm.stack[0, ssize) (top, shared)
-        int ssize, gbase = 0, gtop = 0, lsize = 0, iter = 0, last_donation = 0;
-        uint32_t pv_dh = 0, pv_dt = 0, pv_init = 0;  // lane 0: queue counters read at the previous check
+        int ssize, gbase = 0, gtop = 0, lsize = 0;
+        uint32_t last_donation = 0;  // `pushes` at the last donation
         if (nbatch == 0) {
             if (lane == 0) sm.stack[0] = 0;  // root
             ssize = 1;
@@ -735,32 +775,43 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             // ---- donate one batch from the logical bottom (shallowest cells = largest
             // subtrees) every kDonateEvery rounds of a long task, or when warps wait idle
             const int live = ssize + gtop - gbase;
-            if ((++iter % G2_CHECK_EVERY) == 0 && live >= 64) {
+            if (b.trace) maxlive = max(maxlive, uint32_t(live));
+            if (live >= kDonateMinLive && pushes - last_donation >= donate_pushes) {
+                // deterministic: the decision depends on this task's own progress only
                 int k = 0;
                 uint32_t ds = 0;
                 if (lane == 0) {
-                    // heavy: a long task donates every kDonateEvery rounds unless enough
-                    // donated work is already queued (keeps the slot budget for tight dacc).
-                    // The queue counters are read one check ahead (the loads overlap four
-                    // rounds of work instead of stalling this one); they only steer the heuristic.
-                    const uint32_t dh = pv_dh, dt = pv_dt;
-                    const bool heavy = iter - last_donation >= kDonateEvery && int(dt - dh) < kQueuedEnough;
-                    const bool dry = !heavy && pv_init >= ng && dh > dt;
-                    pv_dh = ld_vol(q_dhead), pv_dt = ld_vol(q_dtail), pv_init = ld_vol(q_init);
-                    if (heavy || dry) {
-                        ds = atomicAdd(q_dtail, 1u);  // ticket; slot = ticket mod ring size
+                    const uint32_t need = rec == kNone ? 2u : 1u;  // (own record +) the child's
+                    const uint32_t r0 = atomicAdd(&b.qstate[6], need);
+                    if (r0 + need > b.rec_cap) {
+                        flags->task_pool = 1;  // keep the work; the host grows the pool for the next walk
+                    } else {
+                        if (rec == kNone) {
+                            rec = r0;
+                            b.trec[rec] = make_uint4(kNone, 1u, kNone, kNone);
+                        }
+                        const uint32_t child = r0 + need - 1;
+                        b.trec[child] = make_uint4(rec, 1u, kNone, kNone);
+                        if (last_child == kNone)
+                            b.trec[rec].z = child;
+                        else
+                            b.trec[last_child].w = child;
+                        last_child = child;
+                        atomicAdd(&b.trec[rec].y, 1u);  // before the child can exist
+                        ds = atomicAdd(q_dtail, 1u);    // ticket; slot = ticket mod ring size
                         k = min(live / 2, 32);
                         k = gtop == gbase ? min(k, ssize) : min(k, gtop - gbase);
                         atomicAdd(q_pending, 1u);
-                        if (b.world > 1) atomicAdd(&b.gpend[grp], 1u);  // before the batch is visible
                         // wait for the slot's previous occupant to be consumed (ring of 2^20)
                         while (ld_vol64(&b.queue[ds & (kRing - 1)]) != kEmpty) __nanosleep(64);
+                        b.batch_rec[ds & (kRing - 1)] = child;
                     }
                 }
                 k = __shfl_sync(kFull, k, 0);
                 ds = __shfl_sync(kFull, ds, 0);
+                last_donation = pushes;
                 if (k) {
-                    last_donation = iter;
+                    ++ndon;
                     const bool from_spill = gtop > gbase;
                     const uint32_t sl = ds & (kRing - 1);
                     if (lane < k) b.batch[size_t(sl) * 32 + lane] = from_spill ? spill[gbase + lane] : sm.stack[lane];
@@ -789,7 +840,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         // task, which is ordered after this through the buffer hand-over and the pending counter)
         if (b.world > 1 && lane == 0) atomicAdd(&b.gcost[grp], pushes);
         // the last buffer of the task (possibly empty) tells the consumer to write out
-        handoff(lsize, grp, tflags | kLast);
+        handoff(lsize, grp, tflags | kLast, rec);
 
         // ---------------- events
         if (lane == 0) {
@@ -807,7 +858,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 if (ts < b.trace_cap) {
                     b.trace[2 * ts] = make_uint4(uint32_t(t_begin), uint32_t(t_begin >> 32), uint32_t(t_end),
                                                  uint32_t(t_end >> 32));
-                    b.trace[2 * ts + 1] = make_uint4(grp, nbatch, macs, pushes);
+                    b.trace[2 * ts + 1] = make_uint4(grp, nbatch | (min(ndon, 0xfffu) << 8) | (min(maxlive, 0xfffu) << 20), macs, pushes);
                 }
             }
             __threadfence();
@@ -877,7 +928,7 @@ __global__ void __launch_bounds__(256) groups_kernel(TreeView t, const double* _
         for (int o = kGroupLanes / 2; o > 0; o >>= 1) r2 = smax(r2, __shfl_xor_sync(kFull, r2, o));
         if (gon && sub == 0) {
             b.groups[g] = GroupRec{cx, cy, cz, dsqrt(r2), am, first, cnt};
-            if (b.world > 1) b.gpend[g] = 1u, b.gcost[g] = 0u;  // the initial task
+            if (b.world > 1) b.gcost[g] = 0u;
         }
     }
 }
@@ -945,7 +996,50 @@ __global__ void walk_init_kernel(WalkBuffers b) {
         b.qstate[2] = ng;  // tasks pending
         b.qstate[3] = ng;  // initial tasks
         b.qstate[4] = 0;   // donated slots consumed
+        b.qstate[6] = 0;   // task records used
     }
+}
+
+// Initial tasks heaviest first (longest-processing-time order): a group's bounding radius predicts
+// its walk cost (the whole-system groups at Z-curve jumps have radius ~ r_cut and carry up to 32 N
+// interactions), so groups are counting-sorted by descending radius (sign + exponent + 3 mantissa bits
+// of the FP32 radius, 2048 buckets).  The order only schedules: every group's task tree, and hence its
+// result, is the same in any order.
+constexpr int kOrderBuckets = 2048;
+__device__ __forceinline__ uint32_t order_bucket(double radius) {
+    return uint32_t(kOrderBuckets - 1) - min(__float_as_uint(float(radius)) >> 20, uint32_t(kOrderBuckets - 1));
+}
+__global__ void __launch_bounds__(256) order_hist_kernel(const GroupRec* __restrict__ groups, const uint32_t* qstate,
+                                                         uint32_t* hist) {
+    __shared__ uint32_t h[kOrderBuckets];
+    for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    const uint32_t lo = qstate[5], ng = qstate[3];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x)
+        atomicAdd(&h[order_bucket(groups[lo + i].radius)], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], h[i]);
+}
+__global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist) {
+    __shared__ uint32_t part[1024];
+    const uint32_t a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
+    part[threadIdx.x] = a + c;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const uint32_t y = threadIdx.x >= unsigned(o) ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += y;
+        __syncthreads();
+    }
+    const uint32_t ex = part[threadIdx.x] - (a + c);
+    hist[2 * threadIdx.x] = ex, hist[2 * threadIdx.x + 1] = ex + a;
+}
+__global__ void __launch_bounds__(256) order_scatter_kernel(const GroupRec* __restrict__ groups, const uint32_t* qstate,
+                                                            uint32_t* off, uint32_t* order) {
+    const uint32_t lo = qstate[5], ng = qstate[3];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x)
+        order[atomicAdd(&off[order_bucket(groups[lo + i].radius)], 1u)] = i;
 }
 
 // zero the accumulator slots this launch accumulates into: all sinks, or with a peer exchange
@@ -1001,6 +1095,7 @@ void walk_launch_t(const TreeView& t, const WalkParams& p, const WalkBuffers& b,
 }  // namespace
 
 size_t walk_spill_words() { return kSpillWords; }
+size_t walk_order_scratch_words() { return kOrderBuckets; }
 size_t walk_resident_warps() {
     // producer warps (one spill stack each) of the largest grid walk_launch_t can use
     return size_t(kNumSMs) * kMaxBlocksPerSM * kPairs;
@@ -1029,6 +1124,14 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
     }
     G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi, b.shard, gs);
     G2_COUNT(1), walk_init_kernel<<<1, 32, 0, s>>>(b);
+    if (b.order_scratch) {
+        const unsigned ob = std::max(1u, std::min<unsigned>(ceil_div(ceil_div(n_sinks_cap, gs), 256), kNumSMs * 4));
+        G2_CUDA(cudaMemsetAsync(b.order_scratch, 0, kOrderBuckets * sizeof(uint32_t), s));
+        G2_COUNT(1), order_hist_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.order_scratch);
+        G2_COUNT(1), order_scan_kernel<<<1, 1024, 0, s>>>(b.order_scratch);
+        G2_COUNT(1), order_scatter_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.order_scratch,
+                                                             const_cast<uint32_t*>(b.order));
+    }
     // the guarded flush whenever eps^2 is not a normal FP32 number (eps == 0 included): with eps^2
     // flushed to zero the self pair would otherwise meet rsqrt(0) = inf and 0 * inf = NaN
     const bool eps0 = !(float(p.eps * p.eps) >= FLT_MIN);

@@ -4,7 +4,8 @@ import numpy as np
 a = np.fromfile(sys.argv[1], dtype=np.uint32).reshape(-1, 8)
 t0 = a[:, 0].astype(np.uint64) | (a[:, 1].astype(np.uint64) << 32)
 t1 = a[:, 2].astype(np.uint64) | (a[:, 3].astype(np.uint64) << 32)
-grp, root, macs, pushes = a[:, 4], a[:, 5], a[:, 6].astype(np.float64), a[:, 7].astype(np.float64)
+grp, root, macs, pushes = a[:, 4], a[:, 5] & 0xff, a[:, 6].astype(np.float64), a[:, 7].astype(np.float64)
+ndon, maxlive = (a[:, 5] >> 8) & 0xfff, a[:, 5] >> 20
 base = t0.min()
 s = (t0 - base) / 1e6
 e = (t1 - base) / 1e6
@@ -14,7 +15,8 @@ tt = np.linspace(0, e.max(), 21)
 print("busy warps:", [int(((s <= x) & (e > x)).sum()) for x in tt])
 print("task dur ms: p50 %.4f p99 %.3f max %.3f" % (np.median(d), np.quantile(d, .99), d.max()))
 for k in np.argsort(-d)[:6]:
-    print("  grp %d root %d dur %.3f start %.3f macs %d pushes %d" % (grp[k], root[k], d[k], s[k], macs[k], pushes[k]))
+    print("  grp %d root %d dur %.3f start %.3f macs %d pushes %d donations %d max live %d" % (
+        grp[k], root[k], d[k], s[k], macs[k], pushes[k], ndon[k], maxlive[k]))
 A = np.vstack([pushes, macs, np.ones_like(macs)]).T
 coef, *_ = np.linalg.lstsq(A, d * 1e3, rcond=None)
 print("dur_us ~ %.4f*pushes + %.4f*macs + %.2f" % tuple(coef))
