@@ -163,6 +163,7 @@ void Engine::enqueue_flags() {
 }
 void Engine::enqueue_events() {
     G2_CUDA(cudaMemcpyAsync(hs_->events, events_.p, sizeof hs_->events, cudaMemcpyDeviceToHost, s_));
+    G2_CUDA(cudaMemcpyAsync(&hs_->recs, qstate_.p + 6, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
 }
 void Engine::sync() { G2_CUDA(cudaStreamSynchronize(s_)); }
 
@@ -396,7 +397,8 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
         // task records: one per donated task (plus the donating initial task); sized from the group
         // count, doubled whenever a walk ran short (a skipped donation keeps results exact but makes
         // the task tree, hence the FP32 summation order, depend on timing)
-        if (grow_pool_) ensure_task_pool(2 * rec_cap_);
+        // the pool follows the previous walk's use (x1.5); a shortfall doubles it
+        ensure_task_pool(std::max<size_t>(grow_pool_ ? 2 * rec_cap_ : 0, size_t(hs_->recs) * 3 / 2));
         grow_pool_ = false;
         b.trec = trec_.p, b.tacc = tacc_.p, b.batch_rec = batch_rec_.p;
         b.rec_cap = uint32_t(std::min<size_t>(rec_cap_, 0xffffffffu));
@@ -441,6 +443,13 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
     WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
                   c_.count_ops ? 1 : 0, 0};
+    // tighter dacc means more work per group, none of which needs splitting finer than before:
+    // the donation trigger grows as (2^-9 / dacc)^(1/3), x1 .. x8 (a function of dacc only, so every
+    // rank and every run uses the same one)
+    {
+        const double f = std::clamp(std::cbrt(0.001953125 / p_.dacc), 1.0, 8.0);
+        wp.donate_pushes = uint32_t(wp.donate_pushes * f), wp.donate_few = uint32_t(wp.donate_few * f);
+    }
     static const char* dp = std::getenv("G2_DONATE_PUSHES");  // development: donation-trigger sweeps
     static const char* df = std::getenv("G2_DONATE_FEW");
     if (dp) wp.donate_pushes = uint32_t(std::max(1, std::atoi(dp)));

@@ -33,6 +33,7 @@ struct HostSync {
     unsigned long long tnext;
     uint32_t na;
     uint32_t ls[kMaxDepth + 3];
+    uint32_t recs;  // task records the last walk allocated (sizes the pool for the next)
 };
 
 class Engine {
