@@ -170,6 +170,13 @@ int g2_sim_write_snapshot(g2_sim* s, const char* path);
 /* extension: rebuild the tree every step (the all-active "full step" benchmark) */
 int g2_sim_set_rebuild_every_step(g2_sim* s, int on);
 int g2_sim_tuner_interval(g2_sim* s, size_t* interval);
+/* extension: the rebuild tuner's clock (RebuildTuner::record_walk/record_build, rebuild_tuner.hpp:18-31).
+ * flop_rate <= 0: CUDA-event phase times (default).  flop_rate > 0: a deterministic model -- walk
+ * seconds = (27 interactions + 5 MAC evaluations) / flop_rate (op_counters.hpp:50-63), build seconds =
+ * build_seconds_per_particle x n -- so the rebuild schedule, hence the trajectory, is reproducible.
+ * On a mesh every rank feeds its tuner the same inputs either way (sum of the ranks' modelled walk
+ * times, or max of measured ones), so every rank takes the same rebuild decisions. */
+int g2_sim_set_tuner_model(g2_sim* s, double flop_rate, double build_seconds_per_particle);
 
 /* the CUDA stream (cudaStream_t) all of the simulation's work is issued on,
  * so callers can time it with their own events */

@@ -72,6 +72,8 @@ struct Nccl {
     ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
     ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
     ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
     bool ok = false;
@@ -82,9 +84,10 @@ struct Nccl {
         get_unique_id = reinterpret_cast<decltype(get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
         comm_init_rank = reinterpret_cast<decltype(comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
         all_gather = reinterpret_cast<decltype(all_gather)>(dlsym(h, "ncclAllGather"));
+        all_reduce = reinterpret_cast<decltype(all_reduce)>(dlsym(h, "ncclAllReduce"));
         comm_destroy = reinterpret_cast<decltype(comm_destroy)>(dlsym(h, "ncclCommDestroy"));
         error_string = reinterpret_cast<decltype(error_string)>(dlsym(h, "ncclGetErrorString"));
-        ok = get_unique_id && comm_init_rank && all_gather && comm_destroy && error_string;
+        ok = get_unique_id && comm_init_rank && all_gather && all_reduce && comm_destroy && error_string;
     }
 };
 Nccl& nccl() {
@@ -146,6 +149,18 @@ struct NcclExchange final : ShardExchange {
     void transport(g2::Simulation& sim, const float4* send, size_t per_rank) override {
         G2_NCCL(nccl().all_gather(send, gathered.p, per_rank * 4, ncclFloat32, comm, sim.engine().stream()));
     }
+    g2::DBuf<double> tbuf;
+    void agree_times(g2::Simulation& sim, double& walk, double& build, bool sum_walk) override {
+        cudaStream_t s = sim.engine().stream();
+        tbuf.reserve(2);
+        double h[2] = {walk, build};
+        G2_CUDA(cudaMemcpyAsync(tbuf.p, h, sizeof h, cudaMemcpyHostToDevice, s));
+        G2_NCCL(nccl().all_reduce(tbuf.p, tbuf.p, 1, ncclFloat64, sum_walk ? ncclSum : ncclMax, comm, s));
+        G2_NCCL(nccl().all_reduce(tbuf.p + 1, tbuf.p + 1, 1, ncclFloat64, ncclMax, comm, s));
+        G2_CUDA(cudaMemcpyAsync(h, tbuf.p, sizeof h, cudaMemcpyDeviceToHost, s));
+        G2_CUDA(cudaStreamSynchronize(s));
+        walk = h[0], build = h[1];
+    }
 };
 
 // In-process mesh: several Simulations (one host thread each, any devices)
@@ -156,6 +171,22 @@ struct LocalMesh {
     std::condition_variable cv;
     int arrived = 0;
     uint64_t phase = 0;
+    std::vector<double> tw, tb;
+    void agree(int rank, double& walk, double& build, bool sum_walk) {
+        {
+            std::lock_guard<std::mutex> lk(m);
+            if (tw.size() != sims.size()) tw.assign(sims.size(), 0.0), tb.assign(sims.size(), 0.0);
+            tw[rank] = walk, tb[rank] = build;
+        }
+        barrier();
+        double w = sum_walk ? 0.0 : tw[0], b = tb[0];
+        for (size_t q = 0; q < sims.size(); ++q) {  // fixed rank order: identical on every rank
+            w = sum_walk ? w + tw[q] : std::max(w, tw[q]);
+            b = std::max(b, tb[q]);
+        }
+        barrier();  // nobody overwrites its slot before everyone has read
+        walk = w, build = b;
+    }
     void barrier() {
         std::unique_lock<std::mutex> lk(m);
         const uint64_t ph = phase;
@@ -184,6 +215,9 @@ struct LocalExchange final : ShardExchange {
         G2_CUDA(cudaStreamSynchronize(s));
         mesh->barrier();  // nobody reuses its accumulator before everyone copied
     }
+    void agree_times(g2::Simulation& sim, double& walk, double& build, bool sum_walk) override {
+        mesh->agree(sim.rank(), walk, build, sum_walk);
+    }
 };
 
 // ---- fused peer exchange (SURVEY §8e "fused-collective option") -----------------
@@ -202,6 +236,19 @@ struct PeerFlags {
 __global__ void peer_signal_kernel(PeerFlags peers, int world, int self, uint64_t epoch) {
     const int q = threadIdx.x;
     __threadfence_system();
+    if (q < world)
+        asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peers.f[q] + self), "l"(epoch) : "memory");
+}
+// the tuner inputs of this rank into slot [self] of every rank's times array, then the epoch flag
+struct PeerTimes {
+    double* t[g2::kMaxPeers];
+};
+__global__ void peer_times_kernel(PeerTimes times, PeerFlags peers, int world, int self, uint64_t epoch, double walk,
+                                  double build) {
+    const int q = threadIdx.x;
+    if (q < world) times.t[q][2 * self] = walk, times.t[q][2 * self + 1] = build;
+    __threadfence_system();
+    __syncwarp();
     if (q < world)
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peers.f[q] + self), "l"(epoch) : "memory");
 }
@@ -225,6 +272,12 @@ struct PeerExchange final : g2::Exchange {
     float4* buf[2] = {};                        // own accumulators (exported)
     uint64_t* flags = nullptr;                  // own arrival flags [kMaxPeers] (exported)
     uint32_t* cost[2] = {};                     // own per-group cost arrays (exported)
+    double* times = nullptr;                    // own tuner-input slots [kMaxPeers][2] (exported)
+    uint64_t* tflags = nullptr;                 // own arrival flags of the tuner exchange (exported)
+    uint64_t tepoch = 0;
+    double* ptimes[g2::kMaxPeers] = {};
+    uint64_t* ptflags[g2::kMaxPeers] = {};
+    double* htimes = nullptr;                   // pinned read-back
     uint32_t* ngrec = nullptr;                  // [2] group counts behind cost[0], cost[1] (local)
     float4* pbuf[g2::kMaxPeers][2] = {};        // every rank's accumulators as seen from here
     uint64_t* pflags[g2::kMaxPeers] = {};
@@ -251,8 +304,13 @@ struct PeerExchange final : g2::Exchange {
         for (auto& c : cost) G2_CUDA(cudaMalloc(&c, groups * sizeof(uint32_t)));
         G2_CUDA(cudaMalloc(&ngrec, 2 * sizeof(uint32_t)));
         G2_CUDA(cudaMemset(ngrec, 0xff, 2 * sizeof(uint32_t)));  // no history: equal shards first
+        G2_CUDA(cudaMalloc(&times, 2 * g2::kMaxPeers * sizeof(double)));
+        G2_CUDA(cudaMalloc(&tflags, g2::kMaxPeers * sizeof(uint64_t)));
+        G2_CUDA(cudaMemset(tflags, 0, g2::kMaxPeers * sizeof(uint64_t)));
+        G2_CUDA(cudaMallocHost(&htimes, 2 * g2::kMaxPeers * sizeof(double)));
         pbuf[self][0] = buf[0], pbuf[self][1] = buf[1], pflags[self] = flags;
         pcost[self][0] = cost[0], pcost[self][1] = cost[1];
+        ptimes[self] = times, ptflags[self] = tflags;
     }
     ~PeerExchange() override {
         for (void* p : opened) cudaIpcCloseMemHandle(p);
@@ -262,6 +320,9 @@ struct PeerExchange final : g2::Exchange {
             if (c) cudaFree(c);
         if (flags) cudaFree(flags);
         if (ngrec) cudaFree(ngrec);
+        if (times) cudaFree(times);
+        if (tflags) cudaFree(tflags);
+        if (htimes) cudaFreeHost(htimes);
     }
     bool device_shards() const override { return true; }
     void before_walk(g2::Simulation& sim) override {
@@ -287,8 +348,31 @@ struct PeerExchange final : g2::Exchange {
         G2_COUNT(1), peer_wait_kernel<<<1, 32, 0, s>>>(flags, world, epoch);
         G2_CUDA(cudaGetLastError());
     }
+    void agree_times(g2::Simulation& sim, double& walk, double& build, bool sum_walk) override {
+        if (mesh) {
+            mesh->agree(self, walk, build, sum_walk);
+            return;
+        }
+        cudaStream_t s = sim.engine().stream();
+        ++tepoch;
+        PeerTimes pt{};
+        PeerFlags pf{};
+        for (int q = 0; q < world; ++q) pt.t[q] = ptimes[q], pf.f[q] = ptflags[q];
+        G2_COUNT(1), peer_times_kernel<<<1, 32, 0, s>>>(pt, pf, world, self, tepoch, walk, build);
+        G2_COUNT(1), peer_wait_kernel<<<1, 32, 0, s>>>(tflags, world, tepoch);
+        G2_CUDA(cudaGetLastError());
+        G2_CUDA(cudaMemcpyAsync(htimes, times, 2 * world * sizeof(double), cudaMemcpyDeviceToHost, s));
+        G2_CUDA(cudaStreamSynchronize(s));
+        double w = sum_walk ? 0.0 : htimes[0], b = htimes[1];
+        for (int q = 0; q < world; ++q) {
+            w = sum_walk ? w + htimes[2 * q] : std::max(w, htimes[2 * q]);
+            b = std::max(b, htimes[2 * q + 1]);
+        }
+        walk = w, build = b;
+    }
 };
-constexpr size_t kP2PHandleBytes = 5 * sizeof(cudaIpcMemHandle_t);
+constexpr int kP2PHandles = 7;
+constexpr size_t kP2PHandleBytes = kP2PHandles * sizeof(cudaIpcMemHandle_t);
 
 }  // namespace
 
@@ -589,6 +673,13 @@ int g2_sim_set_state(g2_sim* s, const double* pos, const double* vel) {
 int g2_sim_set_rebuild_every_step(g2_sim* s, int on) {
     return guarded([&] { s->s->set_rebuild_every_step(on != 0); });
 }
+int g2_sim_set_tuner_model(g2_sim* s, double flop_rate, double build_seconds_per_particle) {
+    return guarded([&] {
+        if (flop_rate > 0.0 && !(build_seconds_per_particle >= 0.0))
+            throw g2::Error(G2_DATA_ERROR, "set_tuner_model: build time per particle must be >= 0");
+        s->s->set_tuner_model(flop_rate, build_seconds_per_particle);
+    });
+}
 int g2_sim_tuner_interval(g2_sim* s, size_t* interval) {
     return guarded([&] { *interval = s->s->tuner().interval(); });
 }
@@ -621,10 +712,8 @@ int g2_nccl_unique_id(unsigned char id[128]) {
 int g2_sim_set_mesh(g2_sim* s, int rank, int world, const unsigned char id[128]) {
     return guarded([&] {
         if (world < 1 || rank < 0 || rank >= world) throw g2::Error(G2_DATA_ERROR, "set_mesh: bad rank/world");
-        if (world == 1) {
-            s->s->set_shard(0, 1, nullptr);
-            return;
-        }
+        // world == 1 is a real (one-rank) communicator: the step runs the same sharded path and
+        // NCCL collectives as on a larger mesh
         auto ex = std::make_unique<NcclExchange>();
         ncclUniqueId u;
         std::memcpy(&u, id, 128);
@@ -650,6 +739,8 @@ int g2_sim_p2p_export(g2_sim* s, int rank, int world, void* handle) {
         G2_CUDA(cudaIpcGetMemHandle(&h[2], ex->flags));
         G2_CUDA(cudaIpcGetMemHandle(&h[3], ex->cost[0]));
         G2_CUDA(cudaIpcGetMemHandle(&h[4], ex->cost[1]));
+        G2_CUDA(cudaIpcGetMemHandle(&h[5], ex->times));
+        G2_CUDA(cudaIpcGetMemHandle(&h[6], ex->tflags));
         s->pending = std::move(ex);
     });
 }
@@ -663,11 +754,12 @@ int g2_sim_set_mesh_p2p(g2_sim* s, int rank, int world, const void* handles) {
         G2_CUDA(cudaSetDevice(ex->device));
         for (int q = 0; q < world; ++q) {
             if (q == rank) continue;
-            void* p[5];
-            for (int k = 0; k < 5; ++k) {
-                G2_CUDA(cudaIpcOpenMemHandle(&p[k], h[5 * q + k], cudaIpcMemLazyEnablePeerAccess));
+            void* p[kP2PHandles];
+            for (int k = 0; k < kP2PHandles; ++k) {
+                G2_CUDA(cudaIpcOpenMemHandle(&p[k], h[kP2PHandles * q + k], cudaIpcMemLazyEnablePeerAccess));
                 ex->opened.push_back(p[k]);
             }
+            ex->ptimes[q] = static_cast<double*>(p[5]), ex->ptflags[q] = static_cast<uint64_t*>(p[6]);
             ex->pbuf[q][0] = static_cast<float4*>(p[0]), ex->pbuf[q][1] = static_cast<float4*>(p[1]);
             ex->pflags[q] = static_cast<uint64_t*>(p[2]);
             ex->pcost[q][0] = static_cast<uint32_t*>(p[3]), ex->pcost[q][1] = static_cast<uint32_t*>(p[4]);
@@ -695,6 +787,7 @@ int g2_sim_set_mesh_local_p2p(g2_sim** sims, int world) {
                 ex[r]->pbuf[q][0] = ex[q]->buf[0], ex[r]->pbuf[q][1] = ex[q]->buf[1];
                 ex[r]->pflags[q] = ex[q]->flags;
                 ex[r]->pcost[q][0] = ex[q]->cost[0], ex[r]->pcost[q][1] = ex[q]->cost[1];
+                ex[r]->ptimes[q] = ex[q]->times, ex[r]->ptflags[q] = ex[q]->tflags;
                 if (ex[q]->device != ex[r]->device) {
                     int ok = 0;
                     G2_CUDA(cudaDeviceCanAccessPeer(&ok, ex[r]->device, ex[q]->device));

@@ -779,7 +779,7 @@ StepResultH Simulation::step() {
     // active set in (new) Morton order == reference's rank-sorted targets (engine.cpp:39-41)
     launch_compact(active_.p, n, sinks_.p, n_active_.p, compact_status_.p, compact_ctr_.p, s);
     uint32_t lo = 0, hi = ~0u;
-    if (world_ > 1) {
+    if (exchange_) {
         // contiguous equal shard of the groups (cost-balanced sharding: see DESIGN.md)
         uint32_t na = 0;
         if (!exchange_ || !exchange_->device_shards()) {  // host-side equal shards (copy / NCCL meshes)
@@ -794,7 +794,7 @@ StepResultH Simulation::step() {
         hi = uint32_t(uint64_t(ng) * (rank_ + 1) / world_);
     }
     shard_lo_ = lo, shard_hi_ = hi;
-    const bool sharded = world_ > 1 && exchange_;
+    const bool sharded = exchange_ != nullptr;  // a mesh (a one-rank NCCL mesh included)
     if (sharded) exchange_->before_walk(*this);
     eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false, lo, hi, false);
     G2_CUDA(cudaEventRecord(ev_[4], s));
@@ -822,8 +822,16 @@ StepResultH Simulation::step() {
     r.timings.calc_node = elapsed(ev_[2], ev_[3]);
     r.timings.walk_tree = elapsed(ev_[3], ev_[4]);
     r.timings.correct = elapsed(ev_[5], ev_[6]);
-    tuner_.record_walk(r.timings.walk_tree);
-    if (rebuild) tuner_.record_build(r.timings.make_tree + r.timings.calc_node);
+    double tw = r.timings.walk_tree, tb = r.timings.make_tree + r.timings.calc_node;
+    const bool model = model_rate_ > 0.0;
+    if (model) {
+        tw = (27.0 * double(r.events.interactions) + 5.0 * double(r.events.mac_evals)) / model_rate_;
+        tb = model_build_ * double(n);
+    }
+    // every rank must take the same rebuild decisions: identical tuner inputs
+    if (exchange_ && autotune_ && !rebuild_every_step_) exchange_->agree_times(*this, tw, tb, model);
+    tuner_.record_walk(tw);
+    if (rebuild) tuner_.record_build(tb);
     last_active_ = na;
     r.active = na;
     now_ = tn;

@@ -242,6 +242,10 @@ struct Exchange {
     virtual void before_walk(class Simulation&) {}  // e.g. point the walk at this step's exchange buffers
     virtual bool device_shards() const { return false; }  // the walk splits the groups on the device
     virtual void allgather_acc(class Simulation& sim) = 0;
+    // make the rebuild tuner's inputs identical on every rank (the rebuild decision reorders all state,
+    // and the exchange addresses accumulators by slot): walk := sum (modelled time: each rank's share of
+    // the walk work; the sum is the single-rank value) or max (measured) over ranks; build := max
+    virtual void agree_times(class Simulation& sim, double& walk, double& build, bool sum_walk) = 0;
 };
 
 class Simulation {
@@ -265,6 +269,13 @@ public:
     bool initialized() const { return initialized_; }
     size_t n() const { return n_; }
     void set_rebuild_every_step(bool v) { rebuild_every_step_ = v; }
+    // the rebuild tuner's clock: CUDA-event phase times (flop_rate <= 0, the default), or a
+    // deterministic model -- walk = walk Flop (27 I + 5 M, op_counters.hpp:50-63) / flop_rate, build =
+    // build_s_per_particle x n -- which makes the rebuild schedule, hence the trajectory, reproducible
+    void set_tuner_model(double flop_rate, double build_s_per_particle) {
+        model_rate_ = flop_rate, model_build_ = build_s_per_particle;
+    }
+    int rank() const { return rank_; }
     void set_shard(int rank, int world, Exchange* ex) {
         rank_ = rank, world_ = world, exchange_ = ex;
     }
@@ -289,6 +300,7 @@ private:
     RebuildTuner tuner_;
     size_t n_;
     bool initialized_ = false, autotune_ = true, rebuild_every_step_ = false;
+    double model_rate_ = 0.0, model_build_ = 0.0;
     uint64_t now_ = 0;
     double tick_ = 0.0, time_ = 0.0;
     uint32_t last_active_ = 0;

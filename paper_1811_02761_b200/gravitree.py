@@ -406,6 +406,11 @@ class Simulation:
     def set_rebuild_every_step(self, on: bool = True):
         _chk(_lib.g2_sim_set_rebuild_every_step(self._h, C.c_int(int(on))))
 
+    def set_tuner_model(self, flop_rate: float, build_seconds_per_particle: float = 0.0):
+        """The rebuild tuner's clock: CUDA-event times (flop_rate <= 0) or the deterministic model
+        walk = (27 I + 5 M) / flop_rate, build = build_seconds_per_particle x n (reproducible schedule)."""
+        _chk(_lib.g2_sim_set_tuner_model(self._h, C.c_double(flop_rate), C.c_double(build_seconds_per_particle)))
+
     def tuner_interval(self) -> int:
         v = C.c_size_t()
         _chk(_lib.g2_sim_tuner_interval(self._h, C.byref(v)))

@@ -127,9 +127,40 @@ def test_counter_and_error_trend_over_dacc(g2):
     assert all(a > b for a, b in zip(med, med[1:])), med
 
 
-# acceptance.cpp:222-258 (autotuner direction) is not restated: its verdict rests on wall-clock walk
-# timings of a 2^13 system, which on the B200 are tens of microseconds and flip between runs; the
-# tuner's logic itself is pinned on closed forms (tests/test_oracle.py, g2_autotune).
+def steady_state_interval(g2, base, dacc):
+    """acceptance.cpp:222-250 with the tuner fed by the deterministic clock (set_tuner_model): the
+    reference criterion's wall-clock walk timings of a 2^13 system are tens of microseconds on the
+    B200 and flip between runs; the model's walk time is the walk's Flop count (which grows as the
+    tree goes stale) over a fixed rate, so the criterion becomes reproducible."""
+    mass, pos, vel = base
+    params = g2.GravParams(1.0, 0.02, dacc)
+    scheme = g2.StepScheme(adaptive=False, dt_max=2.0 ** -7)
+    cfg = g2.EngineConfig(leaf_cap=1)
+    sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), params, scheme, cfg,
+                        g2.TunerConfig(min_interval=1, max_interval=32, initial_interval=8))
+    sim.set_tuner_model(1e9, 1e-6)  # a CPU-like cost ratio (threads=1): 1 GFlop/s walk, 1 us/particle build
+    sim.init()
+    for _ in range(16):
+        sim.step()
+    retunes, last = [], sim.tuner_interval()
+    for _ in range(192):
+        r = sim.step()
+        if r.rebuilt:
+            retunes.append(r.rebuild_interval)
+        last = r.rebuild_interval
+    if not retunes:
+        return last
+    tail = sorted(retunes[len(retunes) // 2:])
+    return tail[len(tail) // 2]
+
+
+def test_acceptance_autotuner_direction(g2, ref):
+    """acceptance.cpp:252-258: the steady-state rebuild interval is longer at loose dacc (2^-1) than
+    at tight dacc (2^-12) -- cheap walks amortise a rebuild over more steps."""
+    base = ref.sample_model("plummer", 8192, 3)
+    loose = steady_state_interval(g2, base, 2.0 ** -1)
+    tight = steady_state_interval(g2, base, 2.0 ** -12)
+    assert loose > tight, (loose, tight)
 
 
 def test_acceptance_phase_dominance(g2):

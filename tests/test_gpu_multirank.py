@@ -66,6 +66,102 @@ def test_sharded_steps_match_single_rank(world, mesh):
         assert work.max() / work.mean() < 1.03, work
 
 
+def run_mesh(sims, steps):
+    out = []
+    for _ in range(steps):
+        res = [None] * len(sims)
+
+        def run(k):
+            res[k] = sims[k].step()
+
+        th = [threading.Thread(target=run, args=(k,)) for k in range(len(sims))]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        assert all(o is not None for o in res)
+        out.append(res)
+    return out
+
+
+@pytest.mark.parametrize("world,mesh", [(2, "copy"), (3, "p2p")])
+def test_autotuned_mesh_matches_single_rank(world, mesh):
+    """Block steps with the reference's rebuild auto-tuner on a mesh: every rank must take
+    the same rebuild decisions.  With the deterministic tuner clock the ranks feed their tuners the
+    SUM of their modelled walk times = the single-rank value, so the mesh reproduces the single-rank
+    run bit for bit, rebuild schedule included."""
+    import paper_1811_02761_b200 as g2
+    from paper_1811_02761_b200.gravitree import sample_model
+    m, p, v = sample_model("m31", 60000, 3)
+    params = g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9)
+
+    def make():
+        s = g2.Simulation(g2.ParticleSystem(m, p, v), params, g2.StepScheme(dt_max=1.0))
+        s.set_tuner_model(4e13, 3e-12)  # cheap builds: the tuner shortens the interval (several rebuilds)
+        return s
+
+    ref = make()
+    ref.init()
+    sims = [make() for _ in range(world)]
+    (g2.Simulation.set_mesh_local if mesh == "copy" else g2.Simulation.set_mesh_local_p2p)(sims)
+    for s in sims:
+        s.init()
+    single = [ref.step() for _ in range(24)]
+    multi = run_mesh(sims, 24)
+    assert sum(r.rebuilt for r in single) >= 2  # the first build and one auto-tuned rebuild at least
+    for r0, rs in zip(single, multi):
+        assert all(r.rebuilt == r0.rebuilt and r.rebuild_interval == r0.rebuild_interval for r in rs)
+        assert all(r.active == r0.active for r in rs)
+    a = ref.system()
+    for s in sims:
+        b = s.system()
+        for k in ("acc", "pos", "vel", "level"):
+            assert np.array_equal(getattr(b, k), getattr(a, k)), k
+
+
+def test_autotuned_mesh_measured_times_consistent():
+    """With the default (CUDA-event) tuner clock the ranks agree on the max of their measured times:
+    rebuild decisions and the evolved state are identical on every rank."""
+    import paper_1811_02761_b200 as g2
+    from paper_1811_02761_b200.gravitree import sample_model
+    m, p, v = sample_model("m31", 60000, 4)
+    sims = [g2.Simulation(g2.ParticleSystem(m, p, v), g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9),
+                          g2.StepScheme(dt_max=1.0)) for _ in range(2)]
+    g2.Simulation.set_mesh_local_p2p(sims)
+    for s in sims:
+        s.init()
+    for rs in run_mesh(sims, 14):
+        assert rs[0].rebuilt == rs[1].rebuilt and rs[0].rebuild_interval == rs[1].rebuild_interval
+    a, b = sims[0].system(), sims[1].system()
+    for k in ("acc", "pos", "vel", "level"):
+        assert np.array_equal(getattr(a, k), getattr(b, k)), k
+
+
+def test_nccl_one_rank_mesh():
+    """The NCCL exchange through product code (g2_sim_set_mesh): a one-rank communicator runs the
+    sharded step path -- host-side shard, ncclAllGather of the accumulator window, unpack kernel, and
+    the tuner agreement's ncclAllReduce -- and equals the plain single-rank run bit for bit.  (NCCL
+    refuses two ranks on one device; the multi-rank window/unpack logic is the LocalExchange tests'.)"""
+    import paper_1811_02761_b200 as g2
+    from paper_1811_02761_b200.gravitree import sample_model
+    m, p, v = sample_model("m31", 60000, 6)
+    params = g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9)
+    a = g2.Simulation(g2.ParticleSystem(m, p, v), params, g2.StepScheme(dt_max=1.0))
+    b = g2.Simulation(g2.ParticleSystem(m, p, v), params, g2.StepScheme(dt_max=1.0))
+    for s in (a, b):
+        s.set_tuner_model(4e13, 3e-10)
+    b.set_mesh(0, 1, g2.nccl_unique_id())
+    for s in (a, b):
+        s.init()
+    ra = [a.step() for _ in range(10)]
+    rb = [b.step() for _ in range(10)]
+    assert [r.rebuilt for r in ra] == [r.rebuilt for r in rb]
+    assert [r.events.interactions for r in ra] == [r.events.interactions for r in rb]
+    sa, sb = a.system(), b.system()
+    for k in ("acc", "pos", "vel", "level"):
+        assert np.array_equal(getattr(sa, k), getattr(sb, k)), k
+
+
 def test_deterministic_accelerations():
     """Two walks of the same M31 2^20 system (all active, many donated subtrees) and a block-step
     run repeated: bit-identical accelerations (the reference is thread-count independent,
