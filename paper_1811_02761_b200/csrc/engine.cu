@@ -244,6 +244,27 @@ __global__ void disorder_kernel(const uint64_t* __restrict__ k, size_t n, unsign
     atomicAdd(&out[0], d);
     atomicAdd(&out[1], big);
 }
+// development: displacement |k - src[k]| of the new Morton order against the storage order
+__global__ void displacement_kernel(const uint32_t* __restrict__ src, size_t n, unsigned long long* out) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+        const long long d = llabs((long long)src[i] - (long long)i);
+        const int b = d == 0 ? 0 : min(31, 64 - __clzll((unsigned long long)d));  // bucket: bit length
+        atomicAdd(&out[b], 1ull);
+    }
+}
+static void debug_displacement(const uint32_t* src, size_t n, cudaStream_t s) {
+    static unsigned long long* buf = nullptr;
+    if (!buf) cudaMalloc(&buf, 32 * 8);
+    cudaMemsetAsync(buf, 0, 32 * 8, s);
+    displacement_kernel<<<148 * 4, 256, 0, s>>>(src, n, buf);
+    unsigned long long h[32];
+    cudaMemcpyAsync(h, buf, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::fprintf(stderr, "[g2 build] displacement bit-length histogram:");
+    for (int b = 0; b < 32; ++b)
+        if (h[b]) std::fprintf(stderr, " %d:%llu", b, h[b]);
+    std::fprintf(stderr, "\n");
+}
 static void debug_disorder(const uint64_t* k, size_t n, cudaStream_t s) {
     static unsigned long long* buf = nullptr;
     if (!buf) cudaMalloc(&buf, 16);
@@ -285,6 +306,7 @@ const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank
         }
         uint32_t* src = alt ? vals_b_.p : vals_a_.p;
         launch_fix_ties(keys_a_.p, src, ids, n, flags_.p, s_);
+        if (phase_debug()) debug_displacement(src, n, s_);
         G2_CUDA(cudaMemcpyAsync(src_.p, src, n * 4, cudaMemcpyDeviceToDevice, s_));
         launch_gather_u32(ids, src_.p, perm_.p, n, s_);  // perm[k] = original id at new position k
         rank_valid_ = false;

@@ -70,6 +70,10 @@ constexpr uint32_t kSpillWords = 16384;    // global stack entries per producer
 #define G2_DONATE_MIN_LIVE 2
 #endif
 constexpr int kDonateMinLive = G2_DONATE_MIN_LIVE;  // pending cells a task needs before it donates half
+#ifndef G2_DONATE_BATCHES
+#define G2_DONATE_BATCHES 2
+#endif
+constexpr int kMaxBatches = G2_DONATE_BATCHES;       // donated batches (tasks) of 32 cells per donation
 constexpr uint32_t kNone = ~0u;             // no task record / no child / no parent
 constexpr uint64_t kEmpty = ~0ull;
 constexpr int kRingBits = 20;              // donated-task ring: 2^20 slots, reused
@@ -777,61 +781,77 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             const int live = ssize + gtop - gbase;
             if (b.trace) maxlive = max(maxlive, uint32_t(live));
             if (live >= kDonateMinLive && pushes - last_donation >= donate_pushes) {
-                // deterministic: the decision depends on this task's own progress only
-                int k = 0;
-                uint32_t ds = 0;
-                if (lane == 0) {
-                    const uint32_t need = rec == kNone ? 2u : 1u;  // (own record +) the child's
+                // deterministic: the decision depends on this task's own progress only.  Half of the
+                // pending cells (from the logical bottom: shallowest = largest subtrees) leave as up to
+                // kMaxBatches batches of 32, one task (record) each, children in batch order.
+                const bool from_spill = gtop - gbase >= 32 || (gtop > gbase && ssize == 0);
+                const int avail = from_spill ? gtop - gbase : ssize;
+                const int give = min(live / 2, min(avail, 32 * kMaxBatches));
+                const int nb = (give + 31) / 32;
+                uint32_t ds = 0, child0 = 0;
+                int ok = 0;
+                if (lane == 0 && give > 0) {
+                    const uint32_t need = (rec == kNone ? 1u : 0u) + uint32_t(nb);  // (own record +) children
                     const uint32_t r0 = atomicAdd(&b.qstate[6], need);
                     if (r0 + need > b.rec_cap) {
                         flags->task_pool = 1;  // keep the work; the host grows the pool for the next walk
                     } else {
+                        ok = 1;
                         if (rec == kNone) {
                             rec = r0;
                             b.trec[rec] = make_uint4(kNone, 1u, kNone, kNone);
                         }
-                        const uint32_t child = r0 + need - 1;
-                        b.trec[child] = make_uint4(rec, 1u, kNone, kNone);
-                        if (last_child == kNone)
-                            b.trec[rec].z = child;
-                        else
-                            b.trec[last_child].w = child;
-                        last_child = child;
-                        atomicAdd(&b.trec[rec].y, 1u);  // before the child can exist
-                        ds = atomicAdd(q_dtail, 1u);    // ticket; slot = ticket mod ring size
-                        k = min(live / 2, 32);
-                        k = gtop == gbase ? min(k, ssize) : min(k, gtop - gbase);
-                        atomicAdd(q_pending, 1u);
-                        // wait for the slot's previous occupant to be consumed (ring of 2^20)
-                        while (ld_vol64(&b.queue[ds & (kRing - 1)]) != kEmpty) __nanosleep(64);
-                        b.batch_rec[ds & (kRing - 1)] = child;
+                        child0 = r0 + need - uint32_t(nb);
+                        for (int j = 0; j < nb; ++j) {
+                            const uint32_t child = child0 + uint32_t(j);
+                            b.trec[child] = make_uint4(rec, 1u, kNone, kNone);
+                            if (last_child == kNone)
+                                b.trec[rec].z = child;
+                            else
+                                b.trec[last_child].w = child;
+                            last_child = child;
+                        }
+                        atomicAdd(&b.trec[rec].y, uint32_t(nb));  // before the children can exist
+                        ds = atomicAdd(q_dtail, uint32_t(nb));    // consecutive tickets; slot = ticket mod ring
+                        atomicAdd(q_pending, uint32_t(nb));
+                        for (int j = 0; j < nb; ++j) {
+                            // wait for the slot's previous occupant to be consumed (ring of 2^20)
+                            const uint32_t sl = (ds + uint32_t(j)) & (kRing - 1);
+                            while (ld_vol64(&b.queue[sl]) != kEmpty) __nanosleep(64);
+                            b.batch_rec[sl] = child0 + uint32_t(j);
+                        }
                     }
                 }
-                k = __shfl_sync(kFull, k, 0);
+                ok = __shfl_sync(kFull, ok, 0);
                 ds = __shfl_sync(kFull, ds, 0);
                 last_donation = pushes;
-                if (k) {
-                    ++ndon;
-                    const bool from_spill = gtop > gbase;
-                    const uint32_t sl = ds & (kRing - 1);
-                    if (lane < k) b.batch[size_t(sl) * 32 + lane] = from_spill ? spill[gbase + lane] : sm.stack[lane];
+                if (ok) {
+                    ndon += uint32_t(nb);
+                    for (int j = 0; j < nb; ++j) {
+                        const uint32_t sl = (ds + uint32_t(j)) & (kRing - 1);
+                        const int i = 32 * j + lane;
+                        if (i < give) b.batch[size_t(sl) * 32 + lane] = from_spill ? spill[gbase + i] : sm.stack[i];
+                    }
                     __threadfence();
                     __syncwarp();
-                    if (lane == 0)
-                        st_rel64(&b.queue[sl], (uint64_t(grp) << 32) | ((uint64_t(ds >> kRingBits) & kGenMask) << 6) |
-                                                   uint32_t(k));
+                    if (lane < nb) {
+                        const uint32_t t = ds + uint32_t(lane);
+                        const uint32_t k = uint32_t(min(32, give - 32 * lane));
+                        st_rel64(&b.queue[t & (kRing - 1)],
+                                 (uint64_t(grp) << 32) | ((uint64_t(t >> kRingBits) & kGenMask) << 6) | k);
+                    }
                     if (from_spill) {
-                        gbase += k;
+                        gbase += give;
                         if (gbase == gtop) gbase = gtop = 0;
                     } else {
-                        for (int base = 0; base < ssize - k; base += 32) {
+                        for (int base = 0; base < ssize - give; base += 32) {
                             const int i = base + lane;
-                            const uint32_t x = i < ssize - k ? sm.stack[i + k] : 0u;
+                            const uint32_t x = i < ssize - give ? sm.stack[i + give] : 0u;
                             __syncwarp();
-                            if (i < ssize - k) sm.stack[i] = x;
+                            if (i < ssize - give) sm.stack[i] = x;
                             __syncwarp();
                         }
-                        ssize -= k;
+                        ssize -= give;
                     }
                 }
             }
