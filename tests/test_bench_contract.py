@@ -1,4 +1,4 @@
-"""The committed bench line (profiles/r1_bench_line.json, produced by `python bench.py` on a B200)
+"""The committed bench line (profiles/r2_bench_line.json, produced by `python bench.py` on a B200)
 carries every key of the bench contract, and the reference arm's line its own."""
 import json
 import os
@@ -12,7 +12,7 @@ def load(name):
 
 
 def test_bench_line_contract():
-    d = load("r1_bench_line.json")
+    d = load("r2_bench_line.json")
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
               "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
         assert k in d, k
@@ -36,7 +36,12 @@ def test_bench_line_contract():
 
 
 def test_reference_arm_line_contract():
-    d = load("r1_reference_arm.json")
+    d = load("r2_reference_arm.json")
+    g = load("r2_bench_line.json")
+    # the driver divides the arms only when metric, unit and config match
+    assert d["metric"] == g["metric"] and d["unit"] == g["unit"] and d["config"] == g["config"]
+    # measured, not extrapolated: the timed steps fit in the timed wall clock
+    assert d["steps"] * d["value"] <= d["timed_wall_seconds"] * (1 + 1e-6)
     assert d["impl"] == "reference" and d["unit"] == "s/step" and d["higher_is_better"] is False
     assert d["cpu_baseline"]["value"] == d["value"] and d["e2e"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
