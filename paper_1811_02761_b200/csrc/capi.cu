@@ -684,6 +684,13 @@ int g2_sim_tuner_interval(g2_sim* s, size_t* interval) {
     return guarded([&] { *interval = s->s->tuner().interval(); });
 }
 
+int g2_sim_sort_stats(g2_sim* s, unsigned long long* bucket_sorts, unsigned long long* radix_fallbacks) {
+    return guarded([&] {
+        *bucket_sorts = s->s->engine().bucket_sorts();
+        *radix_fallbacks = s->s->engine().bucket_fallbacks();
+    });
+}
+
 int g2_sim_stream(g2_sim* s, void** stream) {
     return guarded([&] { *stream = reinterpret_cast<void*>(s->s->engine().stream()); });
 }

@@ -2,6 +2,7 @@
 #include "engine.cuh"
 
 #include <algorithm>
+#include <cfloat>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -102,7 +103,7 @@ Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), devic
     level_start_.reserve(kMaxDepth + 3);
     tile_counters_.reserve(kMaxDepth + 1);
     cube_.reserve(1);
-    bbox_part_.reserve(6 * kNumSMs * 4);
+    bbox_part_.reserve(6 * std::max<size_t>(kNumSMs * 16, kNumSMs * 4));  // launch_bbox or predict_blocks records
     n_sinks_.reserve(1);
     n_groups_.reserve(1);
     events_.reserve(3);
@@ -200,7 +201,18 @@ void Engine::raise_flags() {
     }
 }
 
+void Engine::note_masses(size_t n, const double* mass) {
+    double mx = 0.0, tot = 0.0;
+    for (size_t i = 0; i < n; ++i) mx = std::max(mx, mass[i]), tot += mass[i];
+    // node masses and list entries are FP32 in the walk: their sums must stay finite there (NaN
+    // masses pass, as in the reference, which does not validate an engine's system)
+    if (std::fabs(p_.G) * tot > double(FLT_MAX) / 2)
+        throw Error(kDataError, "particle system: total mass x G exceeds the FP32 range of the walk");
+    mass_max_ = mx;
+}
+
 void Engine::upload_orig(size_t n, const double* mass, const double* pos) {
+    note_masses(n, mass);
     G2_CUDA(cudaMemcpyAsync(pos3_.p, pos, 3 * n * sizeof(double), cudaMemcpyHostToDevice, s_));
     G2_CUDA(cudaMemcpyAsync(mass_.p, mass, n * sizeof(double), cudaMemcpyHostToDevice, s_));
 }
@@ -289,17 +301,28 @@ static void dbg_mark(int i, cudaStream_t s) {
     cudaEventRecord(dbg_ev[i], s);
 }
 
-const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur) {
+const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur, bool cube_partials) {
     const size_t n = n_;
     dbg_mark(0, s_);
-    launch_bbox(xyzm_s_.p, n, bbox_part_.p, cube_.p, flags_.p, s_);
+    if (cube_partials)
+        launch_bbox_final(bbox_part_.p, predict_blocks(n), cube_.p, s_);
+    else
+        launch_bbox(xyzm_s_.p, n, bbox_part_.p, cube_.p, flags_.p, s_);
     if (!rank_cur) {
         // keys in storage order sorted with the storage position as payload (no scatter into id
-        // order, no rank gather); equal-key runs are then put in original-id order in place
-        launch_keys(xyzm_s_.p, nullptr, n, cube_.p, keys_a_.p, flags_.p, s_);
-        if (phase_debug()) debug_disorder(keys_a_.p, n, s_);
+        // order, no rank gather); equal-key runs are then put in original-id order in place.  The
+        // storage order is the previous Morton order, so the bucket sort (bucket_sort.cu) normally
+        // sorts; the key kernel + onesweep radix sort behind it run only if its gate opened
+        static const bool no_bucket = std::getenv("G2_NO_BUCKET_SORT") != nullptr;  // development A/B
+        bool alt = false;
+        bucket_pending_ =
+            !no_bucket && launch_bucket_sort(xyzm_s_.p, n, cube_.p, bucket_, keys_a_.p, vals_a_.p, flags_.p, s_);
+        if (!bucket_pending_) {
+            launch_keys(xyzm_s_.p, nullptr, n, cube_.p, keys_a_.p, flags_.p, s_);
+            if (phase_debug()) debug_disorder(keys_a_.p, n, s_);
+            alt = radix_sort_pairs<uint64_t>(keys_a_.p, vals_a_.p, keys_b_.p, vals_b_.p, n, 63, true, sort_, s_);
+        }
         dbg_mark(1, s_);
-        const bool alt = radix_sort_pairs<uint64_t>(keys_a_.p, vals_a_.p, keys_b_.p, vals_b_.p, n, 63, true, sort_, s_);
         if (alt) {
             std::swap(keys_a_.p, keys_b_.p);
             std::swap(keys_a_.cap, keys_b_.cap);
@@ -326,6 +349,12 @@ void Engine::ensure_rank() {
     rank_valid_ = true;
 }
 
+bool Engine::take_bucket_overflow() {
+    const bool o = bucket_overflow_;
+    bucket_overflow_ = false;
+    return o;
+}
+
 bool Engine::take_tie_overflow() {
     // the flags were staged with the level sizes at split_and_nodes' synchronisation
     if (!hs_->flags.tie_run) return false;
@@ -350,8 +379,15 @@ void Engine::split_and_nodes(bool with_nodes) {
         dbg_mark(4, s_);
         uint32_t* ls = hs_->ls;
         G2_CUDA(cudaMemcpyAsync(ls, level_start_.p, sizeof hs_->ls, cudaMemcpyDeviceToHost, s_));
+        if (bucket_pending_)
+            G2_CUDA(cudaMemcpyAsync(&hs_->bucket_gate, bucket_.gate.p, sizeof(int), cudaMemcpyDeviceToHost, s_));
         enqueue_flags();
         sync();
+        if (bucket_pending_) {
+            ++(hs_->bucket_gate ? bucket_fallbacks_ : bucket_sorts_);
+            bucket_overflow_ = hs_->bucket_gate != 0;
+            bucket_pending_ = false;
+        }
         if (phase_debug() && dbg_ev[0]) {
             float t[4] = {0, 0, 0, 0};
             cudaEventElapsedTime(&t[0], dbg_ev[0], dbg_ev[1]);
@@ -465,6 +501,7 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
     WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
                   c_.count_ops ? 1 : 0, 0};
+    wp.mass_max = mass_max_;
     // tighter dacc means more work per group, none of which needs splitting finer than before:
     // the donation trigger grows as (2^-9 / dacc)^(1/3), x1 .. x8 (a function of dacc only, so every
     // rank and every run uses the same one)
@@ -662,6 +699,7 @@ Simulation::Simulation(size_t n, const double* mass, const double* pos, const do
                 throw Error(kDataError, "particle system: non-finite state");
     }
     tick_ = sc_.dt_max / double(uint64_t(1) << kMaxBlockLevel);
+    eng_.note_masses(n, mass);
     eng_.reserve(n);
     eng_.set_n(n);
     cudaStream_t s = eng_.stream();
@@ -721,12 +759,14 @@ const uint32_t* Simulation::rank_cur() {
     return rank_cur_.p;
 }
 
-void Simulation::rebuild_order() {
-    const uint32_t* src = eng_.rebuild_sorted(ids_.p, nullptr);
+void Simulation::rebuild_order(bool cube_partials) {
+    const uint32_t* src = eng_.rebuild_sorted(ids_.p, nullptr, cube_partials);
     reorder(src);
     eng_.split_and_nodes(false);  // syncs once to size the levels
-    if (eng_.take_tie_overflow()) {
-        // a long run of equal keys: redo the ordering with the (key, original id) sort
+    // a bucket over capacity (its output was the identity order: the state is unchanged) or a long
+    // run of equal keys: redo the ordering with the (key, original id) sort
+    const bool bucket_overflow = eng_.take_bucket_overflow();
+    if (eng_.take_tie_overflow() || bucket_overflow) {
         src = eng_.rebuild_sorted(ids_.p, rank_cur());
         reorder(src);
         eng_.split_and_nodes(false);
@@ -779,16 +819,18 @@ StepResultH Simulation::step() {
 
     G2_CUDA(cudaEventRecord(ev_[0], s));
     launch_tnext(st, n, t_next_.p, s);
-    launch_predict(st, n, t_next_.p, now_, tick_, active_.p, s);
+    const bool rebuild = !eng_.has_tree() || rebuild_every_step_ || tuner_.should_rebuild();
+    // a rebuilding step's predict also reduces the bounding-cube partials (no separate pass)
+    launch_predict(st, n, t_next_.p, now_, tick_, active_.p, s, rebuild ? eng_.bbox_partials() : nullptr,
+                   eng_.dev_flags());
     G2_CUDA(cudaEventRecord(ev_[1], s));
 
-    const bool rebuild = !eng_.has_tree() || rebuild_every_step_ || tuner_.should_rebuild();
     if (rebuild) {
         if (autotune_)
             tuner_.on_rebuild();
         else
             tuner_.reset_cycle();
-        rebuild_order();
+        rebuild_order(true);
         G2_CUDA(cudaEventRecord(ev_[2], s));
         eng_.calc_nodes();
         G2_CUDA(cudaEventRecord(ev_[3], s));

@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "kernels.cuh"
+#include "bucket_sort.cuh"
 #include "radix_sort.cuh"
 
 namespace g2 {
@@ -34,6 +35,7 @@ struct HostSync {
     uint32_t na;
     uint32_t ls[kMaxDepth + 3];
     uint32_t recs;  // task records the last walk allocated (sizes the pool for the next)
+    int bucket_gate;  // the last rebuild's bucket sort overflowed (its radix fallback ran)
 };
 
 class Engine {
@@ -66,8 +68,16 @@ public:
     // id ids[k]); reorders xyzm_s and returns src (new position k <- old src[k]).
     // new Morton order of the resident state; returns src (new k <- old position).  rank_cur null:
     // storage-order sort + tie repair (rank_ left stale); else the (key, id) sort via key_by_id.
-    const uint32_t* rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur);
+    // cube_partials: the bbox partials of the current positions are already in bbox_partials() (the
+    // predict kernel wrote them), only the final reduction runs
+    const uint32_t* rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur, bool cube_partials = false);
+    double* bbox_partials() { return bbox_part_.p; }
+    DevFlags* dev_flags() { return flags_.p; }
     bool take_tie_overflow();  // true (and clears) if a tie run was too long for the repair (staged by split)
+    bool take_bucket_overflow();  // true (and clears) if the last rebuild's bucket sort overflowed (ditto)
+    // rebuild sorts so far: by the bucket sort, and by its radix fallback (an overflowed bucket)
+    unsigned long long bucket_sorts() const { return bucket_sorts_; }
+    unsigned long long bucket_fallbacks() const { return bucket_fallbacks_; }
     // boundary read-backs: enqueue copies into the pinned staging block, one sync, then inspect
     HostSync* host_sync() { return hs_; }
     void enqueue_flags();
@@ -108,6 +118,9 @@ public:
     size_t accum_cap() const { return accum_.cap; }
     void reserve_accum(size_t slots) { accum_.reserve(slots); }
     void direct_sum_orig(const double4* xyzm_orig, size_t n, double* ax, double* ay, double* az);
+    // FP32 range of the walk: G x total mass must be a finite float (data_error otherwise);
+    // the largest mass selects the guarded flush when the self-pair factor G m / eps^3 could overflow
+    void note_masses(size_t n, const double* mass);
     void check_flags();  // syncs and throws on device-side errors
     void read_events(EventsH& ev);
 
@@ -141,6 +154,7 @@ private:
     bool has_tree_ = false;
     bool rank_valid_ = true;  // rank_ matches perm_ (false after a storage-order rebuild)
     uint32_t max_level_width_ = 0;
+    double mass_max_ = 0.0;  // largest particle mass seen by note_masses
 
     DBuf<double> pos3_, mass_, amag_o_;   // host-order staging
     DBuf<double4> xyzm_o_, xyzm_s_, xyzm_alt_;
@@ -157,6 +171,10 @@ private:
     DBuf<uint32_t> level_start_, tile_counters_;
     DBuf<uint64_t> split_status_;
     DBuf<uint32_t> split_tiles_;
+    BucketScratch bucket_;  // rebuild bucket sort (bucket_sort.cu)
+    bool bucket_pending_ = false;  // the last rebuild_sorted launched a bucket sort (gate read at the split sync)
+    bool bucket_overflow_ = false;
+    unsigned long long bucket_sorts_ = 0, bucket_fallbacks_ = 0;
     DBuf<double> bbox_part_;
     DBuf<Cube> cube_;
     DBuf<uint32_t> sinks_, sinks_alt_, n_sinks_, n_groups_;
@@ -290,7 +308,7 @@ public:
 private:
     StepState state();
     void reorder(const uint32_t* src);
-    void rebuild_order();          // new Morton order + topology of the resident state
+    void rebuild_order(bool cube_partials = false);          // new Morton order + topology of the resident state
     const uint32_t* rank_cur();    // original id -> current position (computed on demand)
     double elapsed(cudaEvent_t a, cudaEvent_t b);
 

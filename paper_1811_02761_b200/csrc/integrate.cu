@@ -84,12 +84,23 @@ __device__ __forceinline__ void predict_one(double4& p, double& vx, double& vy, 
     vy = dadd(vy, dmul(ay, dt));
     vz = dadd(vz, dmul(az, dt));
 }
+// bbox (nullable): also the bounding-cube partials of the predicted positions (bounding_cube,
+// octree.cpp:24-49: min / max are exact in any order), one record of 6 per block, so a rebuild
+// that follows needs only bbox_final_kernel instead of another pass over the positions
 __global__ void __launch_bounds__(kBlock) predict_kernel(StepState st, size_t n, const unsigned long long* t_next_p,
-                                                          uint64_t now, double tick, uint8_t* __restrict__ active) {
+                                                          uint64_t now, double tick, uint8_t* __restrict__ active,
+                                                          double* __restrict__ bbox, DevFlags* flags) {
     const uint64_t t_next = *t_next_p;
     const double dt = dmul(double(t_next - now), tick);
     const double h = dmul(dmul(0.5, dt), dt);
     const size_t np = n / 2;
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    bool bad = false;
+    auto fold = [&](const double4& p) {
+        bad |= !(isfinite(p.x) && isfinite(p.y) && isfinite(p.z));
+        lo[0] = smin(lo[0], p.x), lo[1] = smin(lo[1], p.y), lo[2] = smin(lo[2], p.z);
+        hi[0] = smax(hi[0], p.x), hi[1] = smax(hi[1], p.y), hi[2] = smax(hi[2], p.z);
+    };
     for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < np; i += size_t(gridDim.x) * kBlock) {
         double4 p0 = st.xyzm[2 * i], p1 = st.xyzm[2 * i + 1];
         double2 vx = reinterpret_cast<const double2*>(st.vx)[i], vy = reinterpret_cast<const double2*>(st.vy)[i];
@@ -101,6 +112,7 @@ __global__ void __launch_bounds__(kBlock) predict_kernel(StepState st, size_t n,
         predict_one(p0, vx.x, vy.x, vz.x, ax.x, ay.x, az.x, dt, h);
         predict_one(p1, vx.y, vy.y, vz.y, ax.y, ay.y, az.y, dt, h);
         st.xyzm[2 * i] = p0, st.xyzm[2 * i + 1] = p1;
+        if (bbox) fold(p0), fold(p1);
         reinterpret_cast<double2*>(st.vx)[i] = vx, reinterpret_cast<double2*>(st.vy)[i] = vy;
         reinterpret_cast<double2*>(st.vz)[i] = vz;
         if (active)
@@ -114,6 +126,27 @@ __global__ void __launch_bounds__(kBlock) predict_kernel(StepState st, size_t n,
         predict_one(p, vx, vy, vz, st.ax[i], st.ay[i], st.az[i], dt, h);
         st.xyzm[i] = p, st.vx[i] = vx, st.vy[i] = vy, st.vz[i] = vz;
         if (active) active[i] = (st.last_update[i] + level_ticks(st.level[i]) == t_next) ? 1 : 0;
+        if (bbox) fold(p);
+    }
+    if (!bbox) return;
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) flags->data_error = 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = smin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+            hi[a] = smax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+        }
+    __shared__ double sh[kBlock / 32][6];
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0)
+        for (int a = 0; a < 3; ++a) sh[w][a] = lo[a], sh[w][3 + a] = hi[a];
+    __syncthreads();
+    if (threadIdx.x < 6) {
+        double v = sh[0][threadIdx.x];
+        for (int k = 1; k < kBlock / 32; ++k)
+            v = threadIdx.x < 3 ? smin(v, sh[k][threadIdx.x]) : smax(v, sh[k][threadIdx.x]);
+        bbox[blockIdx.x * 6 + threadIdx.x] = v;
     }
 }
 
@@ -405,9 +438,11 @@ void launch_tnext(const StepState& st, size_t n, unsigned long long* t_next, cud
     G2_COUNT(1), tnext_kernel<<<grid_for(n), kBlock, 0, s>>>(st.level, st.last_update, n, t_next);
 }
 
+unsigned predict_blocks(size_t n) { return grid_for(n / 2 + 1); }
 void launch_predict(const StepState& st, size_t n, const unsigned long long* t_next, uint64_t now, double tick,
-                    uint8_t* active_flag, cudaStream_t s) {
-    G2_COUNT(1), predict_kernel<<<grid_for(n / 2 + 1), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag);
+                    uint8_t* active_flag, cudaStream_t s, double* bbox_partials, DevFlags* flags) {
+    G2_COUNT(1), predict_kernel<<<predict_blocks(n), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag,
+                                                                     bbox_partials, flags);
 }
 
 void launch_compact(const uint8_t* flags, size_t n, uint32_t* out, uint32_t* n_out, uint64_t* status,

@@ -31,6 +31,7 @@ struct TreeView {
 // ---- tree.cu -----------------------------------------------------------------
 // bbox partials -> cube; then keys in ORIGINAL index order (key_by_id[id]).
 void launch_bbox(const double4* xyzm, size_t n, double* partials, Cube* cube, DevFlags* flags, cudaStream_t s);
+void launch_bbox_final(const double* partials, unsigned nb, Cube* cube, cudaStream_t s);
 // key of the particle stored at position i goes to key_by_id[id_of_pos[i]] (nullptr: identity)
 void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const Cube* cube, uint64_t* key_by_id,
                  DevFlags* flags, cudaStream_t s);
@@ -90,6 +91,7 @@ struct WalkParams {
     // D = clamp(donate_scale x groups per producer warp, donate_few, donate_pushes): small walks
     // (block steps) split their groups finer; deterministic: D depends on the TOTAL group count only
     uint32_t donate_pushes = 2048, donate_few = 256, donate_scale = 64;
+    double mass_max = 0.0;    // largest particle mass (host-known): guards the FP32 self-pair factor
 };
 constexpr int kMaxPeers = 8;
 struct WalkBuffers {
@@ -162,8 +164,11 @@ struct StepState {
     uint64_t* last_update;
 };
 void launch_tnext(const StepState& st, size_t n, unsigned long long* t_next, cudaStream_t s);
+// bbox_partials (nullable): also the bounding-cube partials of the predicted positions, predict_blocks(n)
+// records of 6 (launch_bbox_final turns them into the cube)
 void launch_predict(const StepState& st, size_t n, const unsigned long long* t_next, uint64_t now, double tick,
-                    uint8_t* active_flag, cudaStream_t s);
+                    uint8_t* active_flag, cudaStream_t s, double* bbox_partials = nullptr, DevFlags* flags = nullptr);
+unsigned predict_blocks(size_t n);
 // stream compaction of flags into sinks (order preserving), count into *n_out
 void launch_compact(const uint8_t* flags, size_t n, uint32_t* out, uint32_t* n_out, uint64_t* status,
                     uint32_t* counter, cudaStream_t s);

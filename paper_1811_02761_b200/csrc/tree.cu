@@ -5,7 +5,7 @@
 // gravitree's build_tree / calc_node (octree.cpp:24-162, morton.hpp:14-49).
 #include <cstdlib>
 
-#include "kernels.cuh"
+#include "morton.cuh"
 
 namespace g2 {
 namespace {
@@ -75,38 +75,18 @@ __global__ void bbox_final_kernel(const double* __restrict__ partials, int nb, C
 }
 
 // ---- morton_key (morton.hpp:14-44) --------------------------------------------
-__device__ __forceinline__ uint64_t expand_bits(uint64_t v) {
-    v &= 0x1fffff;
-    v = (v | v << 32) & 0x001f00000000ffffULL;
-    v = (v | v << 16) & 0x001f0000ff0000ffULL;
-    v = (v | v << 8) & 0x100f00f00f00f00fULL;
-    v = (v | v << 4) & 0x10c30c30c30c30c3ULL;
-    v = (v | v << 2) & 0x1249249249249249ULL;
-    return v;
-}
-
-__device__ __forceinline__ uint64_t quantize(double v, double lo, double width) {
-    const double t = dmul(ddiv(dsub(v, lo), width), 2097152.0);
-    if (t <= 0.0) return 0;
-    const unsigned long long q = __double2ull_rz(t);
-    return q > 2097151ull ? 2097151ull : q;
-}
-
 __global__ void __launch_bounds__(kBlock) keys_kernel(const double4* __restrict__ xyzm,
                                                       const uint32_t* __restrict__ id_of_pos, size_t n,
                                                       const Cube* __restrict__ cube, uint64_t* __restrict__ key_by_id,
                                                       DevFlags* flags) {
-    const Cube c = *cube;
-    const double lox = dsub(c.cx, c.half), loy = dsub(c.cy, c.half), loz = dsub(c.cz, c.half);
-    const double hix = dadd(c.cx, c.half), hiy = dadd(c.cy, c.half), hiz = dadd(c.cz, c.half);
-    const double width = dmul(2.0, c.half);
+    __shared__ SpreadTable st;
+    spread_init(st);
+    const KeyFrame f(*cube);
+    __syncthreads();
     for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock) {
         const double4 p = xyzm[i];
-        const bool inside = p.x >= lox && p.x <= hix && p.y >= loy && p.y <= hiy && p.z >= loz && p.z <= hiz;
-        if (!inside) flags->data_error = 2;
-        const uint64_t key = (expand_bits(quantize(p.x, lox, width)) << 2) |
-                             (expand_bits(quantize(p.y, loy, width)) << 1) | expand_bits(quantize(p.z, loz, width));
-        key_by_id[id_of_pos ? id_of_pos[i] : i] = key;
+        if (!f.inside(p)) flags->data_error = 2;
+        key_by_id[id_of_pos ? id_of_pos[i] : i] = f.key(p, st);
     }
 }
 
@@ -749,6 +729,10 @@ void launch_bbox(const double4* xyzm, size_t n, double* partials, Cube* cube, De
     G2_COUNT(1), bbox_partial_kernel<<<nb, kBlock, 0, s>>>(xyzm, n, partials, flags);
     G2_COUNT(1), bbox_final_kernel<<<1, 32, 0, s>>>(partials, int(nb), cube);
     G2_CUDA(cudaGetLastError());
+}
+
+void launch_bbox_final(const double* partials, unsigned nb, Cube* cube, cudaStream_t s) {
+    G2_COUNT(1), bbox_final_kernel<<<1, 32, 0, s>>>(partials, int(nb), cube);
 }
 
 void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const Cube* cube, uint64_t* key_by_id,

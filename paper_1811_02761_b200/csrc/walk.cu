@@ -138,6 +138,40 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
             : "memory");
     } while (!ok);
 }
+// The consumer's wait for a full buffer: a waiting consumer must not spin on the issue slots its
+// producer needs (a plain try_wait loop was 20 % of the walk's instructions).  G2_MBAR_HINT > 0: the
+// try_wait suspends up to that many ns (it wakes when the phase completes); G2_MBAR_SLEEP > 0:
+// test_wait with __nanosleep back-off between polls.
+#ifndef G2_MBAR_HINT
+#define G2_MBAR_HINT 0
+#endif
+#ifndef G2_MBAR_SLEEP
+#define G2_MBAR_SLEEP 0
+#endif
+__device__ __forceinline__ void mbar_wait_idle(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = smem_addr(bar);
+    uint32_t ok = 0;
+#if G2_MBAR_SLEEP
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    while (!ok) {
+        __nanosleep(G2_MBAR_SLEEP);
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+    }
+#elif G2_MBAR_HINT
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity), "n"(G2_MBAR_HINT)
+            : "memory");
+    } while (!ok);
+#else
+    (void)ok;
+    mbar_wait(bar, parity);
+#endif
+}
 
 // ---- packed f32x2 helpers (sm_100a PTX) --------------------------------------
 using f2 = unsigned long long;
@@ -381,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         bool has_sink = false;
         for (uint32_t it = 0;; ++it) {
             const int bi = int(it & 1);
-            mbar_wait(&ps.full[bi], (it >> 1) & 1);
+            mbar_wait_idle(&ps.full[bi], (it >> 1) & 1);
             const uint32_t cnt = ps.hdr[bi][0], grp = ps.hdr[bi][1], fl = ps.hdr[bi][2], rec = ps.hdr[bi][3];
             if (grp == kStop) break;
             if (fl & kFirst) {
@@ -1153,8 +1187,10 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
                                                              const_cast<uint32_t*>(b.order));
     }
     // the guarded flush whenever eps^2 is not a normal FP32 number (eps == 0 included): with eps^2
-    // flushed to zero the self pair would otherwise meet rsqrt(0) = inf and 0 * inf = NaN
-    const bool eps0 = !(float(p.eps * p.eps) >= FLT_MIN);
+    // flushed to zero the self pair would otherwise meet rsqrt(0) = inf and 0 * inf = NaN.  Likewise
+    // when the self pair's factor m / eps^3 could overflow FP32 (tiny eps with large masses).
+    const bool eps0 = !(float(p.eps * p.eps) >= FLT_MIN) ||
+                      !(p.mass_max / (p.eps * p.eps * p.eps) < 1e30);
     const bool check = b.level_count != nullptr;
     if (check) {
         if (with_pot)

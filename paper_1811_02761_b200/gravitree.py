@@ -416,6 +416,12 @@ class Simulation:
         _chk(_lib.g2_sim_tuner_interval(self._h, C.byref(v)))
         return v.value
 
+    def sort_stats(self) -> tuple:
+        """(bucket sorts, radix fallbacks) of the rebuilds so far (diagnostics)."""
+        a, b = C.c_ulonglong(), C.c_ulonglong()
+        _chk(_lib.g2_sim_sort_stats(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def system(self) -> ParticleSystem:
         n = self._n
         pos, vel, acc = np.empty((n, 3)), np.empty((n, 3)), np.empty((n, 3))

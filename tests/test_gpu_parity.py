@@ -124,6 +124,22 @@ def walk_case(g2, oracle, mass, pos, am, p, cfg=None, targets=None, pot=False):
     return s, ev, err
 
 
+def test_walk_fp32_range_guards(g2, oracle):
+    """ADVICE r1 (walk.cu guard): a tiny but FP32-normal softening with unit masses makes the self
+    pair's factor m / eps^3 overflow FP32 (1e42); the guarded flush drops the exact zero separation
+    (traversal.cpp:73) and the forces stay finite and within the FP32 bar.  A total mass x G beyond
+    the FP32 range is rejected as a data error instead of producing inf list entries."""
+    mass, pos, _ = plummer(4096, seed=5)
+    mass = np.ones_like(mass)
+    am = np.full(len(mass), 4096.0)
+    s, _, _ = walk_case(g2, oracle, mass, pos, am, g2.GravParams(1.0, 1e-14, 2.0 ** -9))
+    assert np.isfinite(s.acc).all()
+    big = np.full(len(mass), 1e36)
+    with pytest.raises(g2.DataError):
+        eng = g2.GravityEngine(g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9))
+        eng.build(g2.ParticleSystem(big, pos))
+
+
 @pytest.mark.parametrize("dacc", [2.0 ** -1, 2.0 ** -3, 2.0 ** -9, 2.0 ** -15])
 def test_walk_plummer_dacc(g2, oracle, dacc):
     mass, pos, _ = plummer(32768, seed=2)
@@ -324,6 +340,37 @@ def test_simulation_rebuild_ties(g2, oracle, cluster):
         ref = oracle.build_tree(mass, st.pos)
         for k in ("keys", "perm", "rank", "cells", "depth"):
             assert np.array_equal(getattr(t, k), getattr(ref, k)), k
+
+
+@pytest.mark.parametrize("cluster", [0, 40, 5000, 9000])
+def test_simulation_rebuild_bucket_sort(g2, oracle, cluster):
+    """Rebuild sorts of n >= 2^15 go through the bucket sort of the nearly sorted storage order
+    (bucket_sort.cu): after every rebuilding step the tree equals build_tree on the step's positions
+    bit for bit.  cluster > 0 puts that many particles on one position: 40 exercises the in-place tie
+    repair inside one bucket; 5000 fills a bucket beyond the small local sort (4096 keys), so the
+    1024-thread instance sorts it (and the over-long tie run then takes the id-order sort); 9000
+    overflows a bucket region (8192): the sort's gate opens and the id-order sort redoes the build."""
+    mass, pos, vel = plummer(1 << 17, seed=7)
+    if cluster:
+        at = np.random.default_rng(cluster).choice(len(mass), cluster, replace=False)
+        pos[at] = pos[at[0]]
+        vel[at] = 0.0
+    sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), g2.GravParams(1.0, 2.0 ** -5, 2.0 ** -9),
+                        g2.StepScheme(dt_max=1 / 64))
+    sim.init()
+    sim.set_rebuild_every_step(True)
+    for _ in range(3):
+        sim.step()
+        t, st = sim.tree(), sim.system()
+        ref = oracle.build_tree(mass, st.pos)
+        for k in ("bbox", "keys", "perm", "rank", "cells", "depth"):
+            assert np.array_equal(getattr(t, k), getattr(ref, k)), k
+    sorts, fallbacks = sim.sort_stats()
+    assert sorts + fallbacks == 4  # init + 3 steps
+    if cluster == 9000:
+        assert fallbacks == 4
+    else:
+        assert sorts >= 3  # the steps' rebuilds (the init build's storage order is the sampler's)
 
 
 @pytest.mark.slow
