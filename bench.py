@@ -128,6 +128,18 @@ def measured_peaks():
         return {}
 
 
+def fp32_peak_measured():
+    """The FP32 CUDA-core peak measured on this GPU by tools/fp32_peak.cu (built by build() into
+    _build/fp32_peak): the larger of scalar FFMA and packed FFMA2 throughput, TFLOP/s; None if absent."""
+    exe = os.path.join(ROOT, "paper_1811_02761_b200", "_build", "fp32_peak")
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60, check=True).stdout
+        d = json.loads(out.strip().splitlines()[-1])
+        return max(d["ffma_tflops"], d["ffma2_tflops"]), d
+    except (OSError, subprocess.SubprocessError, ValueError, KeyError, IndexError):
+        return None, None
+
+
 def walk_traffic_per_launch():
     """dram bytes per walk launch from the committed ncu capture, if any."""
     p = os.path.join(ROOT, "profiles", "walk_traffic.json")  # from the committed ncu --set full capture
@@ -322,6 +334,8 @@ def run_g2(args):
     import paper_1811_02761_b200 as g2
     from paper_1811_02761_b200.gravitree import lib, sample_model
 
+    # the walk's roofline denominator, measured on this GPU (rank 0, before anything is timed)
+    fp32_meas, fp32_meas_d = fp32_peak_measured() if rank == 0 else (None, None)
     mass, pos, vel = sample_model(args.model, args.n, 1)
     params = g2.GravParams(1.0, EPS, DACC)
     scheme = g2.StepScheme(eta=0.5, dt_max=1.0 / 16, adaptive=False, fixed_level=0)  # every particle active
@@ -375,7 +389,14 @@ def run_g2(args):
         flops = float(t[0])
     peaks = measured_peaks()
     f_max = float(peaks.get("sm_max_mhz", 1965.0))
-    fp32_peak = 148 * 128 * 2 * f_max * 1e6 / 1e12  # TFLOP/s
+    fp32_peak = 148 * 128 * 2 * f_max * 1e6 / 1e12  # TFLOP/s (nominal fallback)
+    peak_note = (f"nominal: 148 SM x 128 FP32 lanes x 2 x {f_max:.0f} MHz (sm_max_mhz of MEASURED_PEAKS.json); "
+                 "the FP32 micro-benchmark was not available")
+    if fp32_meas:
+        fp32_peak = fp32_meas
+        peak_note = (f"measured on this GPU before the timed region by tools/fp32_peak.cu (max of scalar FFMA "
+                     f"{fp32_meas_d['ffma_tflops']} and packed FFMA2 {fp32_meas_d['ffma2_tflops']} TFLOP/s; nominal "
+                     f"{148 * 128 * 2 * f_max * 1e6 / 1e12:.2f})")
     achieved = flops / walk_s / 1e12 if walk_s > 0 else 0.0
     clocks = clk.summary()
 
@@ -446,8 +467,7 @@ def run_g2(args):
             "config": workload_config(args),
             "roofline": {"bound": "fp32", "kernel": "walk_kernel", "achieved": achieved, "peak": fp32_peak,
                          "unit": "TFLOP/s", "frac": achieved / fp32_peak, "traffic": walk_traffic_per_launch() if (args.n == 1 << 23 and world == 1) else None,
-                         "peak_note": f"148 SM x 128 FP32 lanes x 2 x {f_max:.0f} MHz (sm_max_mhz of "
-                                      "MEASURED_PEAKS.json); no FP32 peak is measured there",
+                         "peak_note": peak_note,
                          "flop_per_launch": flops, "walk_seconds": walk_s},
             "phases_last_step": vars(r0.timings), "events_last_step": vars(r0.events), "active": r0.active,
             "init_seconds": t_init, "e2e": e2e, "gpu_launches": launches * args.steps,
