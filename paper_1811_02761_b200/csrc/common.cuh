@@ -45,13 +45,16 @@ constexpr int kMaxBlockLevel = 24;   // integrator.hpp:14
 constexpr int kNumSMs = 148;
 
 // Walk-ready node record: FP64 monopole (calc_node output, octree.hpp:26-30)
-// plus the topology link the traversal needs, 48 B, 16-B aligned.
+// plus the topology link the traversal needs, padded to two whole 32-B sectors so that records
+// written in any order (leaves in particle order) never leave partially written sectors.
 //   internal: link = first_child, info = child_count
 //   leaf:     link = first particle (sorted index), info = count | kLeafBit
-struct alignas(16) WNode {
+struct alignas(32) WNode {
     double cx, cy, cz, mass, extent;
     uint32_t link, info;
+    uint32_t pad[4];
 };
+static_assert(sizeof(WNode) == 64, "WNode is two 32-B sectors");
 constexpr uint32_t kLeafBit = 0x80000000u;
 
 // Compact walk record (32 B, one 256-bit load): the FP32-rounded centre of mass,

@@ -152,7 +152,8 @@ void Engine::ensure_task_pool(size_t want) {
 void Engine::ensure_cells(size_t cap) {
     if (cap <= cell_cap_) return;
     first_child_.reserve(cap), child_count_.reserve(cap), first_.reserve(cap), count_.reserve(cap);
-    depth_.reserve(cap), nodes_.reserve(cap), nodes32_.reserve(cap);
+    depth_.reserve(cap), nodes_.reserve(cap), nodes32_.reserve(cap), int_list_.reserve(cap);
+    int_count_.reserve(kMaxDepth + 1);
     split_status_.reserve(cap / 32 + 64);
     cell_cap_ = cap;
 }
@@ -407,12 +408,14 @@ void Engine::split_and_nodes(bool with_nodes) {
         }
         ensure_cells(total + total / 4 + 1024);
     }
+    launch_tree_topology(first_child_.p, child_count_.p, first_.p, count_.p, depth_.p, level_start_.p, ncells_,
+                         uint32_t(cell_cap_), leaf_of_.p, int_list_.p, int_count_.p, s_);
     if (with_nodes) calc_nodes();
 }
 
 void Engine::calc_nodes() {
-    launch_calc_node(xyzm_s_.p, first_child_.p, child_count_.p, first_.p, count_.p, depth_.p, level_start_.p,
-                     ls_host_, nodes_.p, nodes32_.p, rel_.p, leaf_of_.p, s_);
+    launch_calc_node(xyzm_s_.p, n_, child_count_.p, first_.p, count_.p, level_start_.p, ls_host_, leaf_of_.p, int_list_.p, int_count_.p,
+                     nodes_.p, nodes32_.p, rel_.p, s_);
 }
 
 void Engine::refresh(size_t n, const double* mass, const double* pos) {

@@ -168,6 +168,8 @@ private:
     uint32_t ls_host_[kMaxDepth + 3] = {};  // host copy of level_start of the current topology
     DBuf<float4> rel_;
     DBuf<uint32_t> leaf_of_;
+    DBuf<uint4> int_list_;                  // internal cells per depth (launch_tree_topology)
+    DBuf<uint32_t> int_count_;
     DBuf<uint32_t> level_start_, tile_counters_;
     DBuf<uint64_t> split_status_;
     DBuf<uint32_t> split_tiles_;

@@ -54,13 +54,20 @@ struct SplitArgs {
 size_t split_tile_words(size_t n);
 void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s);
 
-// calc_node over the whole tree (octree.cpp:145-162): all leaves in one launch, then the internal
-// levels deepest first; also writes the compact walk records and the leaf-relative particle offsets.
-// level_start_host: the host copy of level_start (launch sizes).
-void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const uint32_t* child_count,
-                      const uint32_t* first, const uint32_t* count, const uint8_t* depth, const uint32_t* level_start,
-                      const uint32_t* level_start_host, WNode* nodes, WNode32* nodes32, float4* rel,
-                      uint32_t* leaf_of, cudaStream_t s);
+// Per topology (after every split): leaf_of (the leaf cell of every particle) and the internal cells
+// of each depth d at int_list[level_start[d] + i], i < int_count[d], as (cell, first_child,
+// child_count, depth) (int_list: [cell_cap]).
+void launch_tree_topology(const uint32_t* first_child, const uint32_t* child_count, const uint32_t* first,
+                          const uint32_t* count, const uint8_t* depth, const uint32_t* level_start, size_t ncells,
+                          uint32_t cell_cap, uint32_t* leaf_of, uint4* int_list, uint32_t* int_count, cudaStream_t s);
+// calc_node over the whole tree (octree.cpp:108-162): the leaves (warps over particle chunks), then
+// the internal levels deepest first from the per-depth lists (one launch per wide level, one block
+// per run of narrow levels); also writes the compact walk records and the leaf-relative particle
+// offsets.  level_start_host: the host copy of level_start (level widths).
+void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count, const uint32_t* first,
+                      const uint32_t* count, const uint32_t* level_start,
+                      const uint32_t* level_start_host, const uint32_t* leaf_of, const uint4* int_list,
+                      const uint32_t* int_count, WNode* nodes, WNode32* nodes32, float4* rel, cudaStream_t s);
 // leaf-relative offsets of the CURRENT positions against the existing nodes (GravityEngine::evaluate
 // walks fresh positions with the node attributes of the last build/refresh, engine.cpp:31-81)
 void launch_leaf_rel(const double4* xyzm, const uint32_t* child_count, const uint32_t* first, const uint32_t* count,

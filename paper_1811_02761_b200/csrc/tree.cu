@@ -11,6 +11,12 @@ namespace g2 {
 namespace {
 
 constexpr int kBlock = 256;
+#ifndef G2_CALC_LEAF_CELLS
+#define G2_CALC_LEAF_CELLS 1  // leaves in cell order (1) or warp-synchronous particle chunks (0): 4.55 vs 4.58 ms paper step
+#endif
+#ifndef G2_CALC_GROUP8
+#define G2_CALC_GROUP8 0  // 8 lanes per internal cell (A/B): 170 vs 146 us per calc at 2^23
+#endif
 #ifndef G2_CALC_MINB
 #define G2_CALC_MINB 2  // 2 blocks of 256 per SM: 128 registers, no spills (1: more registers, 25 % slower)
 #endif
@@ -493,10 +499,180 @@ __global__ void split_init_kernel(SplitArgs a, uint32_t n) {
 // attributes are bit-identical.
 __device__ __forceinline__ void store_node(WNode* __restrict__ nodes, WNode32* __restrict__ nodes32, uint32_t c,
                                            const WNode& nd) {
-    nodes[c] = nd;
+    // two 256-bit stores: whole sectors
+    const uint32_t* w = reinterpret_cast<const uint32_t*>(&nd);
+    WNode* dst = nodes + c;
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(reinterpret_cast<char*>(dst) + 32),
+                 "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+                 : "memory");
     const float fm = float(nd.mass), fb = float(nd.extent);
     nodes32[c] = WNode32{float(nd.cx), float(nd.cy), float(nd.cz), fm, fb, fm * fb * fb, nd.link, nd.info};
 }
+
+// Leaves (every step), warp-synchronous: a warp takes 32 consecutive particles (coalesced loads of
+// the positions and leaf_of) and stages them in its own 1 KB of shared memory.  The lane at a leaf's
+// first particle folds the leaf's mass and weighted centre in the reference's order
+// (octree.cpp:113-125) from there (particles beyond the warp's 32 from global memory); the centre
+// goes back to the leaf's lanes by shuffles, every lane forms its own particle's |x - com|^2 and
+// a segmented max (exact in any order) collects the extent; every lane writes its particle's
+// leaf-relative FP32 offset.  A leaf belongs to the warp of its first particle, which also handles
+// its particles beyond the warp's 32.  No block barriers.
+constexpr int kLeafThreads = 256;
+__global__ void __launch_bounds__(kLeafThreads) calc_leaf_kernel(const double4* __restrict__ xyzm,
+                                                                 const uint32_t* __restrict__ leaf_of,
+                                                                 const uint32_t* __restrict__ count, uint32_t n,
+                                                                 WNode* __restrict__ nodes,
+                                                                 WNode32* __restrict__ nodes32,
+                                                                 float4* __restrict__ rel) {
+    __shared__ double4 P[kLeafThreads];
+    const int lane = threadIdx.x & 31;
+    double4* const W = P + (threadIdx.x & ~31);  // this warp's 32 slots
+    const uint32_t nw = gridDim.x * (kLeafThreads / 32);
+    for (uint32_t base = (blockIdx.x * (kLeafThreads / 32) + (threadIdx.x >> 5)) * 32u; base < n; base += nw * 32u) {
+        const uint32_t k = base + uint32_t(lane);
+        const bool valid = k < n;
+        const double4 p = valid ? xyzm[k] : make_double4(0.0, 0.0, 0.0, 0.0);
+        const uint32_t c = valid ? leaf_of[k] : ~0u;
+        uint32_t cprev = __shfl_up_sync(0xffffffffu, c, 1);
+        if (lane == 0) cprev = base ? leaf_of[base - 1] : ~0u;
+        const bool start = valid && c != cprev;
+        const uint32_t starts = __ballot_sync(0xffffffffu, start);
+        W[lane] = p;
+        __syncwarp();
+        // count: up to the next leaf start inside the warp; the warp's last leaf may run beyond it
+        const uint32_t later = starts & ~((2u << lane) - 1u);
+        const uint32_t cnt = start ? (later ? uint32_t(__ffs(later) - 1 - lane) : count[c]) : 0u;
+        const uint32_t in = min(cnt, uint32_t(32 - lane));  // particles staged in the warp's slots
+        double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
+        for (uint32_t q = 0; q < cnt; ++q) {
+            const double4 v = q < in ? W[lane + int(q)] : xyzm[k + q];
+            m = dadd(m, v.w);
+            wx = dadd(wx, dmul(v.w, v.x));
+            wy = dadd(wy, dmul(v.w, v.y));
+            wz = dadd(wz, dmul(v.w, v.z));
+        }
+        double cx = 0.0, cy = 0.0, cz = 0.0;
+        if (start) {
+            const double inv = ddiv(1.0, m);
+            cx = dmul(wx, inv), cy = dmul(wy, inv), cz = dmul(wz, inv);
+        }
+        // the first lane of this particle's leaf inside the warp (none: an earlier warp owns the leaf)
+        const uint32_t mine = valid ? starts & ((2u << lane) - 1u) : 0u;
+        const int s = mine ? 31 - __clz(mine) : lane;
+        cx = __shfl_sync(0xffffffffu, cx, s), cy = __shfl_sync(0xffffffffu, cy, s), cz = __shfl_sync(0xffffffffu, cz, s);
+        double e2 = mine ? norm2(dsub(p.x, cx), dsub(p.y, cy), dsub(p.z, cz)) : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {  // segmented suffix max: lane s ends with its leaf's lanes
+            const double v = __shfl_down_sync(0xffffffffu, e2, o);
+            const int so = __shfl_down_sync(0xffffffffu, s, o);
+            if (lane + o < 32 && so == s) e2 = smax(e2, v);
+        }
+        const float fx = float(cx), fy = float(cy), fz = float(cz);
+        if (start) {
+            for (uint32_t q = in; q < cnt; ++q) {  // beyond the warp's particles: this lane owns them
+                const double4 v = xyzm[k + q];
+                e2 = smax(e2, norm2(dsub(v.x, cx), dsub(v.y, cy), dsub(v.z, cz)));
+                rel[k + q] = make_float4(float(dsub(v.x, double(fx))), float(dsub(v.y, double(fy))),
+                                         float(dsub(v.z, double(fz))), float(v.w));
+            }
+            WNode nd;
+            nd.cx = cx, nd.cy = cy, nd.cz = cz;
+            nd.extent = dsqrt(e2);
+            nd.link = k;
+            nd.info = cnt | kLeafBit;
+            nd.mass = m;
+            store_node(nodes, nodes32, c, nd);
+        }
+        if (mine)
+            rel[k] = make_float4(float(dsub(p.x, double(fx))), float(dsub(p.y, double(fy))), float(dsub(p.z, double(fz))),
+                                 float(p.w));
+        __syncwarp();  // the slots are rewritten by the next round
+    }
+}
+
+#if G2_CALC_LEAF_CELLS
+// (A/B) leaves in cell order, one thread per cell
+// a leaf of at most 8 particles, same operation order as the general loop below
+__device__ __forceinline__ void leaf_small(const double4* __restrict__ xyzm, uint32_t f, uint32_t cnt, uint32_t c,
+                                           WNode* __restrict__ nodes, WNode32* __restrict__ nodes32,
+                                           float4* __restrict__ rel) {
+    double4 p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cnt)) p[j] = xyzm[f + j];
+    WNode nd;
+    double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cnt)) {
+            m = dadd(m, p[j].w);
+            wx = dadd(wx, dmul(p[j].w, p[j].x));
+            wy = dadd(wy, dmul(p[j].w, p[j].y));
+            wz = dadd(wz, dmul(p[j].w, p[j].z));
+        }
+    const double inv = ddiv(1.0, m);
+    nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+    const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
+    double e2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if (j < int(cnt)) {
+            e2 = smax(e2, norm2(dsub(p[j].x, nd.cx), dsub(p[j].y, nd.cy), dsub(p[j].z, nd.cz)));
+            rel[f + j] = make_float4(float(dsub(p[j].x, c32x)), float(dsub(p[j].y, c32y)), float(dsub(p[j].z, c32z)),
+                                     float(p[j].w));
+        }
+    nd.extent = dsqrt(e2);
+    nd.link = f;
+    nd.info = cnt | kLeafBit;
+    nd.mass = m;
+    store_node(nodes, nodes32, c, nd);
+}
+
+__global__ void __launch_bounds__(kBlock, G2_CALC_MINB) calc_leaf_cells_kernel(const double4* __restrict__ xyzm,
+                                                           const uint32_t* __restrict__ child_count,
+                                                           const uint32_t* __restrict__ first,
+                                                           const uint32_t* __restrict__ count,
+                                                           const uint32_t* __restrict__ level_start,
+                                                           WNode* __restrict__ nodes, WNode32* __restrict__ nodes32,
+                                                           float4* __restrict__ rel) {
+    const uint32_t total = level_start[kMaxDepth + 1];
+    for (uint32_t c = blockIdx.x * kBlock + threadIdx.x; c < total; c += gridDim.x * kBlock) {
+        if (child_count[c]) continue;
+        const uint32_t f = first[c], k1 = f + count[c];
+        if (k1 - f <= 8) {  // the usual leaf: every particle loaded up front, one memory round trip
+            leaf_small(xyzm, f, k1 - f, c, nodes, nodes32, rel);
+            continue;
+        }
+        WNode nd;
+        double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
+        for (uint32_t k = f; k < k1; ++k) {
+            const double4 p = xyzm[k];
+            m = dadd(m, p.w);
+            wx = dadd(wx, dmul(p.w, p.x));
+            wy = dadd(wy, dmul(p.w, p.y));
+            wz = dadd(wz, dmul(p.w, p.z));
+        }
+        const double inv = ddiv(1.0, m);
+        nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
+        const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
+        double e2 = 0.0;
+        for (uint32_t k = f; k < k1; ++k) {
+            const double4 p = xyzm[k];
+            e2 = smax(e2, norm2(dsub(p.x, nd.cx), dsub(p.y, nd.cy), dsub(p.z, nd.cz)));
+            rel[k] = make_float4(float(dsub(p.x, c32x)), float(dsub(p.y, c32y)), float(dsub(p.z, c32z)), float(p.w));
+        }
+        nd.extent = dsqrt(e2);
+        nd.link = f;
+        nd.info = (k1 - f) | kLeafBit;
+        nd.mass = m;
+        store_node(nodes, nodes32, c, nd);
+    }
+}
+
+#endif
 
 // internal cell from its (at most 8) children in order (octree.cpp:145-162).  All children
 // are loaded up front: one memory round trip per cell instead of two dependent chains of cc.
@@ -533,115 +709,123 @@ __device__ __forceinline__ WNode internal_node(const WNode* nodes, uint32_t f, u
     return nd;
 }
 
-// a leaf of at most 8 particles, same operation order as the general loop below
-__device__ __forceinline__ void leaf_small(const double4* __restrict__ xyzm, uint32_t f, uint32_t cnt, uint32_t c,
-                                           WNode* __restrict__ nodes, WNode32* __restrict__ nodes32,
-                                           float4* __restrict__ rel, uint32_t* __restrict__ leaf_of) {
-    double4 p[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (j < int(cnt)) p[j] = xyzm[f + j];
-    WNode nd;
+
+// Internal cell from its children in order (octree.cpp:145-162), 8 lanes per cell (4 cells per
+// warp): lane j loads child j's record, every lane of the group folds the children's masses and
+// weighted centres in order through shuffles (the reference's left fold, bit for bit), then lane j
+// forms child j's extent term and a 3-step max (exact in any order) combines them.  Records written
+// by other CTAs of the same launch are read through L2 (ld.cg).
+__device__ __forceinline__ void internal_group8(const uint4 E, bool valid, WNode* nodes, WNode32* __restrict__ nodes32) {
+    const int lane = threadIdx.x & 31, j = lane & 7, g0 = lane & ~7;
+    const uint32_t c = E.x, fc = E.y, cc = valid ? E.z : 0u;
+    const bool have = uint32_t(j) < cc;
+    double qx = 0.0, qy = 0.0, qz = 0.0, qm = 0.0, qe = 0.0;
+    if (have) {
+        const double2* q = reinterpret_cast<const double2*>(nodes + fc + j);
+        const double2 a = __ldcg(q), b = __ldcg(q + 1), e = __ldcg(q + 2);
+        qx = a.x, qy = a.y, qz = b.x, qm = b.y, qe = e.x;
+    }
     double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (j < int(cnt)) {
-            m = dadd(m, p[j].w);
-            wx = dadd(wx, dmul(p[j].w, p[j].x));
-            wy = dadd(wy, dmul(p[j].w, p[j].y));
-            wz = dadd(wz, dmul(p[j].w, p[j].z));
+    for (int k = 0; k < 8; ++k) {
+        const double km = __shfl_sync(0xffffffffu, qm, g0 + k), kx = __shfl_sync(0xffffffffu, qx, g0 + k),
+                     ky = __shfl_sync(0xffffffffu, qy, g0 + k), kz = __shfl_sync(0xffffffffu, qz, g0 + k);
+        if (uint32_t(k) < cc) {
+            m = dadd(m, km);
+            wx = dadd(wx, dmul(km, kx));
+            wy = dadd(wy, dmul(km, ky));
+            wz = dadd(wz, dmul(km, kz));
         }
+    }
+    WNode nd;
     const double inv = ddiv(1.0, m);
     nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
-    const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
-    double e2 = 0.0;
+    double ext = have ? dadd(dsqrt(norm2(dsub(qx, nd.cx), dsub(qy, nd.cy), dsub(qz, nd.cz))), qe) : 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-        if (j < int(cnt)) {
-            e2 = smax(e2, norm2(dsub(p[j].x, nd.cx), dsub(p[j].y, nd.cy), dsub(p[j].z, nd.cz)));
-            rel[f + j] = make_float4(float(dsub(p[j].x, c32x)), float(dsub(p[j].y, c32y)), float(dsub(p[j].z, c32z)),
-                                     float(p[j].w));
-            leaf_of[f + j] = c;
-        }
-    nd.extent = dsqrt(e2);
-    nd.link = f;
-    nd.info = cnt | kLeafBit;
-    nd.mass = m;
-    store_node(nodes, nodes32, c, nd);
-}
-
-__global__ void __launch_bounds__(kBlock, G2_CALC_MINB) calc_leaf_kernel(const double4* __restrict__ xyzm,
-                                                           const uint32_t* __restrict__ child_count,
-                                                           const uint32_t* __restrict__ first,
-                                                           const uint32_t* __restrict__ count,
-                                                           const uint32_t* __restrict__ level_start,
-                                                           WNode* __restrict__ nodes, WNode32* __restrict__ nodes32,
-                                                           float4* __restrict__ rel, uint32_t* __restrict__ leaf_of) {
-    const uint32_t total = level_start[kMaxDepth + 1];
-    for (uint32_t c = blockIdx.x * kBlock + threadIdx.x; c < total; c += gridDim.x * kBlock) {
-        if (child_count[c]) continue;
-        const uint32_t f = first[c], k1 = f + count[c];
-        if (k1 - f <= 8) {  // the usual leaf: every particle loaded up front, one memory round trip
-            leaf_small(xyzm, f, k1 - f, c, nodes, nodes32, rel, leaf_of);
-            continue;
-        }
-        WNode nd;
-        double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
-        for (uint32_t k = f; k < k1; ++k) {
-            const double4 p = xyzm[k];
-            m = dadd(m, p.w);
-            wx = dadd(wx, dmul(p.w, p.x));
-            wy = dadd(wy, dmul(p.w, p.y));
-            wz = dadd(wz, dmul(p.w, p.z));
-        }
-        const double inv = ddiv(1.0, m);
-        nd.cx = dmul(wx, inv), nd.cy = dmul(wy, inv), nd.cz = dmul(wz, inv);
-        const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
-        double e2 = 0.0;
-        for (uint32_t k = f; k < k1; ++k) {
-            const double4 p = xyzm[k];
-            e2 = smax(e2, norm2(dsub(p.x, nd.cx), dsub(p.y, nd.cy), dsub(p.z, nd.cz)));
-            rel[k] = make_float4(float(dsub(p.x, c32x)), float(dsub(p.y, c32y)), float(dsub(p.z, c32z)), float(p.w));
-            leaf_of[k] = c;
-        }
-        nd.extent = dsqrt(e2);
-        nd.link = f;
-        nd.info = (k1 - f) | kLeafBit;
+    for (int o = 4; o > 0; o >>= 1) ext = smax(ext, __shfl_xor_sync(0xffffffffu, ext, o));
+    if (valid && j == 0) {
+        nd.extent = ext;
+        nd.link = fc;
+        nd.info = cc | (E.w << 8);  // depth feeds the frontier-cap check
         nd.mass = m;
         store_node(nodes, nodes32, c, nd);
     }
 }
 
-__global__ void __launch_bounds__(kBlock, G2_CALC_MINB) calc_internal_kernel(const uint32_t* __restrict__ first_child,
-                                                               const uint32_t* __restrict__ child_count,
-                                                               const uint8_t* __restrict__ depth,
-                                                               const uint32_t* __restrict__ level_start,
-                                                               WNode* __restrict__ nodes,
+// the internal cells of depth d, `parts` warps sharing them (warp index w)
+__device__ __forceinline__ void internal_level(const uint4* __restrict__ int_list, uint32_t b, uint32_t cnt,
+                                               uint32_t w, uint32_t parts, WNode* nodes, WNode32* __restrict__ nodes32) {
+#if G2_CALC_GROUP8
+    const uint32_t sub = (threadIdx.x & 31) >> 3;
+    for (uint32_t i0 = 4 * w; i0 < cnt; i0 += 4 * parts) {  // warp-uniform trips
+        const uint32_t i = i0 + sub;
+        const bool valid = i < cnt;
+        internal_group8(valid ? int_list[b + i] : make_uint4(0u, 0u, 0u, 0u), valid, nodes, nodes32);
+    }
+#else
+    for (uint32_t i = 32 * w + (threadIdx.x & 31); i < cnt; i += 32 * parts) {
+        const uint4 E = int_list[b + i];
+        store_node(nodes, nodes32, E.x, internal_node(nodes, E.y, E.z, uint8_t(E.w)));
+    }
+#endif
+}
+
+// one wide level: the grid's warps share its internal cells
+__global__ void __launch_bounds__(kBlock) calc_internal_kernel(const uint4* __restrict__ int_list,
+                                                               const uint32_t* __restrict__ int_count,
+                                                               const uint32_t* __restrict__ level_start, WNode* nodes,
                                                                WNode32* __restrict__ nodes32, int d) {
-    const uint32_t b = level_start[d], e = level_start[d + 1];
-    for (uint32_t c = b + blockIdx.x * kBlock + threadIdx.x; c < e; c += gridDim.x * kBlock) {
-        const uint32_t cc = child_count[c];
-        if (!cc) continue;
-        store_node(nodes, nodes32, c, internal_node(nodes, first_child[c], cc, depth[c]));
+    internal_level(int_list, level_start[d], int_count[d], blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5),
+                   gridDim.x * (kBlock / 32), nodes, nodes32);
+}
+
+// a run of narrow levels (depths d_hi down to d_lo) in ONE block, levels separated by __syncthreads
+// instead of a launch each
+constexpr int kLevelsThreads = 512;
+constexpr uint32_t kNarrowCells = 2048;  // internal cells per level the host sends to one block
+__global__ void __launch_bounds__(kLevelsThreads, 1) calc_levels_kernel(const uint4* __restrict__ int_list,
+                                                                        const uint32_t* __restrict__ int_count,
+                                                                        const uint32_t* __restrict__ level_start,
+                                                                        WNode* nodes, WNode32* __restrict__ nodes32,
+                                                                        int d_hi, int d_lo) {
+    for (int d = d_hi; d >= d_lo; --d) {
+        internal_level(int_list, level_start[d], int_count[d], threadIdx.x >> 5, kLevelsThreads / 32, nodes, nodes32);
+        __syncthreads();  // level d complete (and visible to the block) before level d - 1 reads it
     }
 }
 
-// the narrow top levels (each at most kTopCells wide) in ONE block, levels separated by
-// __syncthreads instead of a launch each
-constexpr uint32_t kTopCells = 512;
-constexpr int kTopThreads = 512;
-__global__ void __launch_bounds__(kTopThreads, 1) calc_top_kernel(const uint32_t* __restrict__ first_child,
+// Per topology (after every split): leaf_of[k] for every particle of every leaf, and the internal
+// cells of each depth d listed at int_list[level_start[d] + slot] as (cell, first_child,
+// child_count, depth) -- warp-aggregated slot claims on int_count[d], zeroed by the caller; the order
+// inside a depth is immaterial (the cells of one depth are independent).
+__global__ void __launch_bounds__(kBlock) tree_topology_kernel(const uint32_t* __restrict__ first_child,
                                                                const uint32_t* __restrict__ child_count,
+                                                               const uint32_t* __restrict__ first,
+                                                               const uint32_t* __restrict__ count,
                                                                const uint8_t* __restrict__ depth,
-                                                               const uint32_t* __restrict__ level_start, WNode* nodes,
-                                                               WNode32* __restrict__ nodes32, int dtop) {
-    for (int d = dtop; d >= 0; --d) {
-        const uint32_t b = level_start[d], e = level_start[d + 1];
-        for (uint32_t c = b + threadIdx.x; c < e; c += kTopThreads) {
-            const uint32_t cc = child_count[c];
-            if (cc) store_node(nodes, nodes32, c, internal_node(nodes, first_child[c], cc, depth[c]));
+                                                               const uint32_t* __restrict__ level_start,
+                                                               uint32_t cell_cap, uint32_t* __restrict__ leaf_of,
+                                                               uint4* __restrict__ int_list,
+                                                               uint32_t* __restrict__ int_count) {
+    const uint32_t total = min(level_start[kMaxDepth + 1], cell_cap);
+    const int lane = threadIdx.x & 31;
+    for (uint32_t b0 = blockIdx.x * kBlock; b0 < total; b0 += gridDim.x * kBlock) {  // warp-uniform trips
+        const uint32_t c = b0 + threadIdx.x;
+        const bool valid = c < total;
+        const uint32_t cc = valid ? child_count[c] : 0u;
+        const bool inner = valid && cc > 0;
+        const uint32_t d = inner ? uint32_t(depth[c]) : 0xffu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const int leader = __ffs(peers) - 1;
+        uint32_t slot = 0;
+        if (inner && lane == leader) slot = atomicAdd(&int_count[d], uint32_t(__popc(peers)));
+        slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(peers & ((1u << lane) - 1u));
+        if (inner) {
+            int_list[level_start[d] + slot] = make_uint4(c, first_child[c], cc, d);
+        } else if (valid) {
+            const uint32_t f = first[c], e = f + count[c];
+            for (uint32_t k = f; k < e; ++k) leaf_of[k] = c;
         }
-        __syncthreads();  // level d complete (and visible to the block) before level d - 1 reads it
     }
 }
 
@@ -781,28 +965,47 @@ void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
     G2_CUDA(cudaGetLastError());
 }
 
-void launch_calc_node(const double4* xyzm, const uint32_t* first_child, const uint32_t* child_count,
-                      const uint32_t* first, const uint32_t* count, const uint8_t* depth, const uint32_t* level_start,
-                      const uint32_t* level_start_host, WNode* nodes, WNode32* nodes32, float4* rel,
-                      uint32_t* leaf_of, cudaStream_t s) {
-    const size_t total = level_start_host[kMaxDepth + 1];
-    G2_COUNT(1), calc_leaf_kernel<<<grid_for(total), kBlock, 0, s>>>(xyzm, child_count, first, count, level_start,
-                                                                          nodes, nodes32, rel, leaf_of);
-    int deepest = 0;  // the deepest non-empty level holds leaves only
+void launch_tree_topology(const uint32_t* first_child, const uint32_t* child_count, const uint32_t* first,
+                          const uint32_t* count, const uint8_t* depth, const uint32_t* level_start, size_t ncells,
+                          uint32_t cell_cap, uint32_t* leaf_of, uint4* int_list, uint32_t* int_count, cudaStream_t s) {
+    G2_CUDA(cudaMemsetAsync(int_count, 0, (kMaxDepth + 1) * sizeof(uint32_t), s));
+    G2_COUNT(1), tree_topology_kernel<<<grid_for(ncells), kBlock, 0, s>>>(first_child, child_count, first, count, depth,
+                                                                          level_start, cell_cap, leaf_of, int_list,
+                                                                          int_count);
+    G2_CUDA(cudaGetLastError());
+}
+
+void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count, const uint32_t* first,
+                      const uint32_t* count, const uint32_t* level_start,
+                      const uint32_t* level_start_host, const uint32_t* leaf_of, const uint4* int_list,
+                      const uint32_t* int_count, WNode* nodes, WNode32* nodes32, float4* rel, cudaStream_t s) {
+#if G2_CALC_LEAF_CELLS
+    G2_COUNT(1), calc_leaf_cells_kernel<<<grid_for(level_start_host[kMaxDepth + 1]), kBlock, 0, s>>>(
+        xyzm, child_count, first, count, level_start, nodes, nodes32, rel);
+#else
+    G2_COUNT(1), calc_leaf_kernel<<<unsigned(std::min<size_t>(ceil_div(n, kLeafThreads), size_t(kNumSMs) * 8)),
+                                    kLeafThreads, 0, s>>>(xyzm, leaf_of, count, uint32_t(n), nodes, nodes32, rel);
+#endif
+    int deepest = -1;  // the deepest internal level (the deepest non-empty level holds leaves only)
     for (int d = 0; d <= kMaxDepth; ++d)
-        if (level_start_host[d + 1] > level_start_host[d]) deepest = d;
-    static const bool levels = std::getenv("G2_CALC_LEVELS") != nullptr;  // development: launch per level A/B
-    for (int d = deepest - 1; d >= 0; --d) {
-        const size_t w = level_start_host[d + 1] - level_start_host[d];
-        bool top = !levels;
-        for (int u = d; u >= 0 && top; --u) top = level_start_host[u + 1] - level_start_host[u] <= kTopCells;
-        if (top) {
-            G2_COUNT(1), calc_top_kernel<<<1, kTopThreads, 0, s>>>(first_child, child_count, depth, level_start, nodes,
-                                                                   nodes32, d);
-            break;
+        if (level_start_host[d + 1] > level_start_host[d]) deepest = d - 1;
+    // internal cells at depth d: at most the level's width and at most the next level's width
+    auto bound = [&](int d) {
+        return std::min(level_start_host[d + 1] - level_start_host[d], level_start_host[d + 2] - level_start_host[d + 1]);
+    };
+    for (int d = deepest; d >= 0;) {
+        if (bound(d) <= kNarrowCells) {  // a run of narrow levels: one block
+            int lo = d;
+            while (lo > 0 && bound(lo - 1) <= kNarrowCells) --lo;
+            G2_COUNT(1), calc_levels_kernel<<<1, kLevelsThreads, 0, s>>>(int_list, int_count, level_start, nodes,
+                                                                        nodes32, d, lo);
+            d = lo - 1;
+            continue;
         }
-        G2_COUNT(1), calc_internal_kernel<<<grid_for(w), kBlock, 0, s>>>(first_child, child_count, depth, level_start,
-                                                                          nodes, nodes32, d);
+        const unsigned grid = unsigned(std::min<size_t>(ceil_div(size_t(bound(d)) * (G2_CALC_GROUP8 ? 8 : 1), kBlock),
+                                                        size_t(kNumSMs) * 8));
+        G2_COUNT(1), calc_internal_kernel<<<grid, kBlock, 0, s>>>(int_list, int_count, level_start, nodes, nodes32, d);
+        --d;
     }
     G2_CUDA(cudaGetLastError());
 }
