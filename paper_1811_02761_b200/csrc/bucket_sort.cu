@@ -34,6 +34,11 @@ constexpr uint32_t kSmallCap = kLsSmall * kLsItems;  // 4096
 constexpr uint32_t kMaxBig = 64;                   // buckets the large instance takes per sort
 static_assert(kLsBig * kLsItems == int(kBucketCap), "the large local sort holds a full bucket region");
 constexpr unsigned kFull = 0xffffffffu;
+#ifndef G2_LS_WINDOW
+#define G2_LS_WINDOW 24
+#endif
+constexpr int kWindowBits = G2_LS_WINDOW;  // varying key bits the local sort's radix passes cover
+constexpr uint32_t kMaxFixRun = 32;         // longest run of window-equal keys the insertion fix-up takes
 
 // ---- 1. splitters -------------------------------------------------------------------------------
 // kOversample samples per bucket at evenly spaced storage positions (their NEW keys), sorted by two
@@ -308,7 +313,10 @@ __global__ void __launch_bounds__(kThreads, kBig ? 1 : G2_LS_MINB) local_sort_ke
 #pragma unroll
     for (int q = 1; q < kWarps; ++q) mn = umin64(mn, S.mm[0][q]), mx = umax64(mx, S.mm[1][q]);
     const int nbits = mn == mx ? 0 : 64 - __clzll(static_cast<long long>(mn ^ mx));
-    const int passes = (nbits + 7) / 8;
+    // radix passes over the top kWindowBits varying bits only; keys equal there (rare: ~1e-3 of the
+    // neighbours at 2^23) are then ordered by an insertion sort of their run on the full key
+    int lowbits = nbits > kWindowBits ? nbits - kWindowBits : 0;
+    int passes = (nbits - lowbits + 7) / 8;
     if (passes == 0) {  // one key value: any order (the tie repair orders the run)
 #pragma unroll
         for (int i = 0; i < kLsItems; ++i) {
@@ -318,8 +326,10 @@ __global__ void __launch_bounds__(kThreads, kBig ? 1 : G2_LS_MINB) local_sort_ke
         return;
     }
     const uint32_t lt = (1u << lane) - 1u;
+    __shared__ int long_run;
+    for (int round = 0;; ++round) {
     for (int pass = 0; pass < passes; ++pass) {
-        const int shift = 8 * pass;
+        const int shift = lowbits + 8 * pass;
         uint32_t r[kLsItems];
         auto digit = [&](int i) {
             const uint32_t q = row0 + uint32_t(i) * 32 + lane;
@@ -407,6 +417,51 @@ __global__ void __launch_bounds__(kThreads, kBig ? 1 : G2_LS_MINB) local_sort_ke
             for (int i = tid; i < kWarps * 256; i += kThreads) (&S.whist[0][0])[i] = 0;
             __syncthreads();
         }
+    }
+    if (lowbits == 0) break;
+    // runs equal in the sorted window: short ones are insertion-sorted on the full key below; a long
+    // one (keys clustered in a small part of a wide bucket) sends the bucket through every pass
+    if (tid == 0) long_run = 0;
+    __syncthreads();
+    for (uint32_t q = tid; q < cnt; q += kThreads) {
+        const uint64_t top = S.keys[q] >> lowbits;
+        if (q > 0 && (S.keys[q - 1] >> lowbits) == top) continue;
+        uint32_t e = q + 1;
+        while (e < cnt && e - q <= kMaxFixRun && (S.keys[e] >> lowbits) == top) ++e;
+        if (e - q > kMaxFixRun) long_run = 1;
+    }
+    __syncthreads();
+    if (!long_run) break;
+    // every bit, from the current (partly sorted) order: LSD needs no particular input order
+    lowbits = 0, passes = (nbits + 7) / 8;
+#pragma unroll
+    for (int i = 0; i < kLsItems; ++i) {
+        const uint32_t q = row0 + uint32_t(i) * 32 + lane;
+        if (q < cnt) k[i] = S.keys[q], v[i] = S.vals[q];
+    }
+    for (int i = tid; i < kWarps * 256; i += kThreads) (&S.whist[0][0])[i] = 0;
+    __syncthreads();
+    }
+    if (lowbits > 0) {  // runs equal in the sorted window: insertion sort on the full key (nearly sorted)
+        for (uint32_t q = tid; q < cnt; q += kThreads) {
+            const uint64_t top = S.keys[q] >> lowbits;
+            if (q > 0 && (S.keys[q - 1] >> lowbits) == top) continue;  // not the start of a run
+            uint32_t e = q + 1;
+            while (e < cnt && (S.keys[e] >> lowbits) == top) ++e;
+            for (uint32_t a = q + 1; a < e; ++a) {
+                const uint64_t x = S.keys[a];
+                const uint32_t xv = S.vals[a];
+                uint32_t b = a;
+                while (b > q && S.keys[b - 1] > x) {
+                    S.keys[b] = S.keys[b - 1];
+                    S.vals[b] = S.vals[b - 1];
+                    --b;
+                }
+                S.keys[b] = x;
+                S.vals[b] = xv;
+            }
+        }
+        __syncthreads();
     }
     for (uint32_t q = tid; q < cnt; q += kThreads) {
         keys_out[off + q] = S.keys[q];

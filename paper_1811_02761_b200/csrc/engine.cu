@@ -408,8 +408,10 @@ void Engine::split_and_nodes(bool with_nodes) {
         }
         ensure_cells(total + total / 4 + 1024);
     }
-    launch_tree_topology(first_child_.p, child_count_.p, first_.p, count_.p, depth_.p, level_start_.p, ncells_,
-                         uint32_t(cell_cap_), leaf_of_.p, int_list_.p, int_count_.p, s_);
+    // (a bucket sort over capacity produced a placeholder order: the caller redoes the ordering)
+    if (!bucket_overflow_)
+        launch_tree_topology(first_child_.p, child_count_.p, first_.p, count_.p, depth_.p, level_start_.p, ncells_,
+                             uint32_t(cell_cap_), leaf_of_.p, int_list_.p, int_count_.p, s_);
     if (with_nodes) calc_nodes();
 }
 

@@ -53,21 +53,32 @@ __global__ void __launch_bounds__(kBlock) bbox_partial_kernel(const double4* __r
     }
 }
 
-__global__ void bbox_final_kernel(const double* __restrict__ partials, int nb, Cube* cube) {
-    // one warp: min/max are exact in any order
-    const int lane = threadIdx.x;
+constexpr int kBboxFinalThreads = 1024;
+__global__ void __launch_bounds__(kBboxFinalThreads) bbox_final_kernel(const double* __restrict__ partials, int nb,
+                                                                       Cube* cube) {
+    // one block: min/max are exact in any order
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-    for (int b = lane; b < nb; b += 32)
+    for (int b = threadIdx.x; b < nb; b += kBboxFinalThreads)
         for (int a = 0; a < 3; ++a) {
             lo[a] = smin(lo[a], partials[6 * b + a]);
             hi[a] = smax(hi[a], partials[6 * b + 3 + a]);
         }
+    __shared__ double sh[kBboxFinalThreads / 32][6];
+    for (int round = 0; round < 2; ++round) {  // warps, then the warp partials
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-        for (int a = 0; a < 3; ++a) {
-            lo[a] = smin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
-            hi[a] = smax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
-        }
+        for (int o = 16; o > 0; o >>= 1)
+            for (int a = 0; a < 3; ++a) {
+                lo[a] = smin(lo[a], __shfl_xor_sync(0xffffffffu, lo[a], o));
+                hi[a] = smax(hi[a], __shfl_xor_sync(0xffffffffu, hi[a], o));
+            }
+        if (round == 1) break;
+        if (lane == 0)
+            for (int a = 0; a < 3; ++a) sh[w][a] = lo[a], sh[w][3 + a] = hi[a];
+        __syncthreads();
+        if (w != 0) return;
+        for (int a = 0; a < 3; ++a) lo[a] = sh[lane][a], hi[a] = sh[lane][3 + a];
+    }
     if (lane != 0) return;
     double c[3];
     for (int a = 0; a < 3; ++a) c[a] = dmul(dadd(lo[a], hi[a]), 0.5);  // 0.5 * (lo + hi)
@@ -820,11 +831,17 @@ __global__ void __launch_bounds__(kBlock) tree_topology_kernel(const uint32_t* _
         uint32_t slot = 0;
         if (inner && lane == leader) slot = atomicAdd(&int_count[d], uint32_t(__popc(peers)));
         slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(peers & ((1u << lane) - 1u));
-        if (inner) {
-            int_list[level_start[d] + slot] = make_uint4(c, first_child[c], cc, d);
-        } else if (valid) {
-            const uint32_t f = first[c], e = f + count[c];
-            for (uint32_t k = f; k < e; ++k) leaf_of[k] = c;
+        if (inner) int_list[level_start[d] + slot] = make_uint4(c, first_child[c], cc, d);
+        const uint32_t f = valid && !inner ? first[c] : 0u, cnt = valid && !inner ? count[c] : 0u;
+        if (cnt <= 32u) {
+            for (uint32_t k = f; k < f + cnt; ++k) leaf_of[k] = c;
+        }
+        // large leaves (coincident clusters at depth 21, large leaf_cap): the whole warp writes each
+        for (uint32_t big = __ballot_sync(0xffffffffu, cnt > 32u); big; big &= big - 1) {
+            const int src = __ffs(big) - 1;
+            const uint32_t bf = __shfl_sync(0xffffffffu, f, src), bn = __shfl_sync(0xffffffffu, cnt, src),
+                           bc = __shfl_sync(0xffffffffu, c, src);
+            for (uint32_t k = bf + lane; k < bf + bn; k += 32) leaf_of[k] = bc;
         }
     }
 }
@@ -911,12 +928,12 @@ inline unsigned grid_for(size_t n) { return std::max(1u, std::min<unsigned>(ceil
 void launch_bbox(const double4* xyzm, size_t n, double* partials, Cube* cube, DevFlags* flags, cudaStream_t s) {
     const unsigned nb = std::max(1u, std::min<unsigned>(ceil_div(n, kBlock * 4), kNumSMs * 4));
     G2_COUNT(1), bbox_partial_kernel<<<nb, kBlock, 0, s>>>(xyzm, n, partials, flags);
-    G2_COUNT(1), bbox_final_kernel<<<1, 32, 0, s>>>(partials, int(nb), cube);
+    G2_COUNT(1), bbox_final_kernel<<<1, kBboxFinalThreads, 0, s>>>(partials, int(nb), cube);
     G2_CUDA(cudaGetLastError());
 }
 
 void launch_bbox_final(const double* partials, unsigned nb, Cube* cube, cudaStream_t s) {
-    G2_COUNT(1), bbox_final_kernel<<<1, 32, 0, s>>>(partials, int(nb), cube);
+    G2_COUNT(1), bbox_final_kernel<<<1, kBboxFinalThreads, 0, s>>>(partials, int(nb), cube);
 }
 
 void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const Cube* cube, uint64_t* key_by_id,
