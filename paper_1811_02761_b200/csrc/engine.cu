@@ -366,6 +366,7 @@ bool Engine::take_tie_overflow() {
 
 void Engine::split_and_nodes(bool with_nodes) {
     const size_t n = n_;
+    bool topo_done = false;
     while (true) {
         G2_CUDA(cudaMemsetAsync(level_start_.p, 0, (kMaxDepth + 3) * sizeof(uint32_t), s_));
         G2_CUDA(cudaMemsetAsync(tile_counters_.p, 0, (kMaxDepth + 1) * sizeof(uint32_t), s_));
@@ -374,9 +375,10 @@ void Engine::split_and_nodes(bool with_nodes) {
         SplitArgs a{keys_a_.p,  first_child_.p, child_count_.p, first_.p,
                     count_.p,   depth_.p,       level_start_.p, split_status_.p,
                     tile_counters_.p, uint32_t(cell_cap_), uint32_t(std::min<size_t>(c_.leaf_cap, 0xffffffffu)),
-                    flags_.p, split_tiles_.p};
+                    flags_.p, split_tiles_.p, leaf_of_.p, int_list_.p, int_count_.p,
+                    bucket_pending_ ? bucket_.gate.p : nullptr};
         dbg_mark(3, s_);
-        launch_split(a, uint32_t(n), s_);
+        topo_done = launch_split(a, uint32_t(n), s_);
         dbg_mark(4, s_);
         uint32_t* ls = hs_->ls;
         G2_CUDA(cudaMemcpyAsync(ls, level_start_.p, sizeof hs_->ls, cudaMemcpyDeviceToHost, s_));
@@ -409,7 +411,7 @@ void Engine::split_and_nodes(bool with_nodes) {
         ensure_cells(total + total / 4 + 1024);
     }
     // (a bucket sort over capacity produced a placeholder order: the caller redoes the ordering)
-    if (!bucket_overflow_)
+    if (!bucket_overflow_ && !topo_done)
         launch_tree_topology(first_child_.p, child_count_.p, first_.p, count_.p, depth_.p, level_start_.p, ncells_,
                              uint32_t(cell_cap_), leaf_of_.p, int_list_.p, int_count_.p, s_);
     if (with_nodes) calc_nodes();

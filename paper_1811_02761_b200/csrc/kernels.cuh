@@ -50,9 +50,15 @@ struct SplitArgs {
     uint32_t leaf_cap;
     DevFlags* flags;
     uint32_t* tiles;          // split_tile_words(n) scratch for the non-recursive split (nullable)
+    // topology outputs (see launch_tree_topology), written by the non-recursive split's last pass
+    uint32_t* leaf_of;
+    uint4* int_list;
+    uint32_t* int_count;
+    const int* topo_gate;     // nullable: a set word means a placeholder order (no topology written)
 };
 size_t split_tile_words(size_t n);
-void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s);
+// returns true when the split also wrote the topology outputs (leaf_of, int_list, int_count)
+bool launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s);
 
 // Per topology (after every split): leaf_of (the leaf cell of every particle) and the internal cells
 // of each depth d at int_list[level_start[d] + i], i < int_count[d], as (cell, first_child,

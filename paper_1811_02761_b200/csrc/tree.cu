@@ -463,31 +463,66 @@ __device__ __forceinline__ uint32_t run_end(const uint64_t* __restrict__ keys, u
 
 // per cell: count = end of its digit run (8 keys probed at once, then galloping), and for split
 // cells the number of consecutive next-level cells starting inside it
+// topology outputs of cell c (see tree_topology_kernel); every lane of the warp calls it (warp-uniform)
+__device__ __forceinline__ void write_topology(uint32_t c, bool valid, uint32_t fc, uint32_t cc, uint32_t d,
+                                               uint32_t f, uint32_t cnt, const uint32_t* __restrict__ level_start,
+                                               uint32_t* __restrict__ leaf_of, uint4* __restrict__ int_list,
+                                               uint32_t* __restrict__ int_count) {
+    const int lane = threadIdx.x & 31;
+    const bool inner = valid && cc > 0;
+    const uint32_t key = inner ? d : 0xffu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, key);
+    const int leader = __ffs(peers) - 1;
+    uint32_t slot = 0;
+    if (inner && lane == leader) slot = atomicAdd(&int_count[d], uint32_t(__popc(peers)));
+    slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(peers & ((1u << lane) - 1u));
+    if (inner) int_list[level_start[d] + slot] = make_uint4(c, fc, cc, d);
+    const uint32_t lc = valid && !inner ? cnt : 0u;
+    if (lc <= 32u)
+        for (uint32_t k = f; k < f + lc; ++k) leaf_of[k] = c;
+    // large leaves (coincident clusters at depth 21, large leaf_cap): the whole warp writes each
+    for (uint32_t big = __ballot_sync(0xffffffffu, lc > 32u); big; big &= big - 1) {
+        const int src = __ffs(big) - 1;
+        const uint32_t bf = __shfl_sync(0xffffffffu, f, src), bn = __shfl_sync(0xffffffffu, lc, src),
+                       bc = __shfl_sync(0xffffffffu, c, src);
+        for (uint32_t k = bf + lane; k < bf + bn; k += 32) leaf_of[k] = bc;
+    }
+}
+
+// per cell: count = end of its digit run (8 keys probed at once, then galloping), and for split
+// cells the number of consecutive next-level cells starting inside it; then the topology outputs
 __global__ void __launch_bounds__(kBlock) split_cells_kernel(SplitArgs a, uint32_t n) {
     const uint32_t total = min(a.level_start[kMaxDepth + 1], a.cell_cap);
-    for (uint32_t c = blockIdx.x * kBlock + threadIdx.x; c < total; c += gridDim.x * kBlock) {
-        const uint32_t i = a.first[c];
-        const int d = a.depth[c];
-        const int sh = 3 * (kMaxDepth - d);
-        const uint64_t pre = a.keys[i] >> sh;
-        uint64_t kk[8];
+    const bool topo = a.leaf_of && !(a.topo_gate && *a.topo_gate);
+    for (uint32_t b0 = blockIdx.x * kBlock; b0 < total; b0 += gridDim.x * kBlock) {  // warp-uniform trips
+        const uint32_t c = b0 + threadIdx.x;
+        const bool valid = c < total;
+        uint32_t i = 0, e = 0, fc = 0, cc = 0;
+        int d = 0;
+        if (valid) {
+            i = a.first[c];
+            d = a.depth[c];
+            const int sh = 3 * (kMaxDepth - d);
+            const uint64_t pre = a.keys[i] >> sh;
+            uint64_t kk[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) kk[q] = i + 1 + q < n ? a.keys[i + 1 + q] : ~0ull;
-        uint32_t e = 0;
+            for (int q = 0; q < 8; ++q) kk[q] = i + 1 + q < n ? a.keys[i + 1 + q] : ~0ull;
 #pragma unroll
-        for (int q = 7; q >= 0; --q)
-            if (i + 1 + q >= n || (kk[q] >> sh) != pre) e = i + 1 + q;
-        if (!e) e = run_end(a.keys, n, i + 9, pre, sh);
-        e = min(e, n);
-        a.count[c] = e - i;
-        const uint32_t fc = a.first_child[c];
-        uint32_t cc = 0;
-        if (fc) {
-            const uint32_t lend = min(a.level_start[d + 2], a.cell_cap);
-            cc = 1;
-            while (fc + cc < lend && a.first[fc + cc] < e) ++cc;
+            for (int q = 7; q >= 0; --q)
+                if (i + 1 + q >= n || (kk[q] >> sh) != pre) e = i + 1 + q;
+            if (!e) e = run_end(a.keys, n, i + 9, pre, sh);
+            e = min(e, n);
+            a.count[c] = e - i;
+            fc = a.first_child[c];
+            if (fc) {
+                const uint32_t lend = min(a.level_start[d + 2], a.cell_cap);
+                cc = 1;
+                while (fc + cc < lend && a.first[fc + cc] < e) ++cc;
+            }
+            a.child_count[c] = cc;
         }
-        a.child_count[c] = cc;
+        if (topo) write_topology(c, valid, fc, cc, uint32_t(d), i, e - i, a.level_start, a.leaf_of, a.int_list,
+                                      a.int_count);
     }
 }
 
@@ -824,25 +859,9 @@ __global__ void __launch_bounds__(kBlock) tree_topology_kernel(const uint32_t* _
         const uint32_t c = b0 + threadIdx.x;
         const bool valid = c < total;
         const uint32_t cc = valid ? child_count[c] : 0u;
-        const bool inner = valid && cc > 0;
-        const uint32_t d = inner ? uint32_t(depth[c]) : 0xffu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
-        const int leader = __ffs(peers) - 1;
-        uint32_t slot = 0;
-        if (inner && lane == leader) slot = atomicAdd(&int_count[d], uint32_t(__popc(peers)));
-        slot = __shfl_sync(0xffffffffu, slot, leader) + __popc(peers & ((1u << lane) - 1u));
-        if (inner) int_list[level_start[d] + slot] = make_uint4(c, first_child[c], cc, d);
-        const uint32_t f = valid && !inner ? first[c] : 0u, cnt = valid && !inner ? count[c] : 0u;
-        if (cnt <= 32u) {
-            for (uint32_t k = f; k < f + cnt; ++k) leaf_of[k] = c;
-        }
-        // large leaves (coincident clusters at depth 21, large leaf_cap): the whole warp writes each
-        for (uint32_t big = __ballot_sync(0xffffffffu, cnt > 32u); big; big &= big - 1) {
-            const int src = __ffs(big) - 1;
-            const uint32_t bf = __shfl_sync(0xffffffffu, f, src), bn = __shfl_sync(0xffffffffu, cnt, src),
-                           bc = __shfl_sync(0xffffffffu, c, src);
-            for (uint32_t k = bf + lane; k < bf + bn; k += 32) leaf_of[k] = bc;
-        }
+        const bool leaf = valid && cc == 0;
+        write_topology(c, valid, valid && cc ? first_child[c] : 0u, cc, valid ? uint32_t(depth[c]) : 0u,
+                       leaf ? first[c] : 0u, leaf ? count[c] : 0u, level_start, leaf_of, int_list, int_count);
     }
 }
 
@@ -945,8 +964,9 @@ void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const
 // per-depth tile counts + totals, then the per-particle (lo, hi) depth ranges (u16)
 size_t split_tile_words(size_t n) { return (kMaxDepth + 1) * (ceil_div(n, kSplitTile) + 1) + 32 + (n + 1) / 2 + 4; }
 
-void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
+bool launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
     if (a.leaf_cap <= kSplitMaxCap && a.tiles) {
+        if (a.leaf_of) G2_CUDA(cudaMemsetAsync(a.int_count, 0, (kMaxDepth + 1) * sizeof(uint32_t), s));
         const uint32_t ntiles = ceil_div(n, kSplitTile);
         uint32_t* totals = a.tiles + size_t(kMaxDepth + 1) * ntiles;
         uint16_t* lohi = reinterpret_cast<uint16_t*>(a.tiles + (kMaxDepth + 1) * (size_t(ntiles) + 1) + 32);
@@ -955,7 +975,7 @@ void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
         G2_COUNT(1), split_write_kernel<<<ntiles, kSplitThreads, 0, s>>>(a, n, a.tiles, ntiles, totals, lohi);
         G2_COUNT(1), split_cells_kernel<<<grid_for(a.cell_cap), kBlock, 0, s>>>(a, n);
         G2_CUDA(cudaGetLastError());
-        return;
+        return a.leaf_of != nullptr;
     }
     // level-by-level path (leaf_cap > kSplitMaxCap)
     G2_COUNT(1), split_init_kernel<<<1, 32, 0, s>>>(a, n);
@@ -980,6 +1000,7 @@ void launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
         }
     }
     G2_CUDA(cudaGetLastError());
+    return false;
 }
 
 void launch_tree_topology(const uint32_t* first_child, const uint32_t* child_count, const uint32_t* first,
