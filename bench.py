@@ -267,7 +267,7 @@ def join_mesh(args, g2, sim, rank, world):
     sim.set_mesh(rank, world, uid[0])
 
 
-def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world):
+def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world, tuner_clock=None):
     """The paper-comparable block-step protocol: reference defaults
     (eta 0.5, adaptive levels) with dt_max = 1, timed over `paper_steps` steps after init and
     4 warm-up steps, once with the reference's own rebuild auto-tuner (fed CUDA-event times)
@@ -279,7 +279,11 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world):
     import torch
     from paper_1811_02761_b200.gravitree import lib
     out = {"what": "block steps, reference driver defaults with dt_max=1 (eta 0.5, adaptive levels)",
-           "paper_v100_s_per_step": PAPER_V100_S_PER_STEP}
+           "paper_v100_s_per_step": PAPER_V100_S_PER_STEP,
+           "tuner_clock": ("deterministic model calibrated on this run's all-active steps: walk %.2f TFLOP/s, "
+                           "build %.3g s/particle (CUDA-event times make the reference's tuner schedule "
+                           "timing-dependent: 6.8-32 ms/step across runs)" % (tuner_clock[0] / 1e12, tuner_clock[1])
+                           if tuner_clock else "CUDA-event times")}
     for label, fixed, dt_max in (("auto_tuned_rebuild", 0, 1.0), ("rebuild_every_2", 2, 1.0),
                                  ("default_scheme_dt_max_1_16_auto_tuned", 0, 1.0 / 16)):
         sim = g2.Simulation(g2.ParticleSystem(mass, pos, vel), params, g2.StepScheme(eta=0.5, dt_max=dt_max),
@@ -289,6 +293,8 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world):
         sim.init()
         if fixed:
             sim.set_fixed_rebuild_interval(fixed)
+        elif tuner_clock:
+            sim.set_tuner_model(*tuner_clock)
         hs = ctypes.c_void_p()
         lib().g2_sim_stream(sim._h, ctypes.byref(hs))
         stream = torch.cuda.ExternalStream(hs.value, device=torch.device("cuda", local))
@@ -435,7 +441,17 @@ def run_g2(args):
 
     paper = None
     if not args.no_paper:
-        paper = paper_protocol(args, g2, mass, pos, vel, params, local, rank, world)
+        # the auto-tuned runs' tuner clock: the deterministic model calibrated on this run's all-active
+        # steps (walk Flop rate, build seconds per particle), so the rebuild schedule is reproducible
+        build_pp = float(np.mean([r.timings.make_tree + r.timings.calc_node for r in results])) / args.n
+        if world > 1:  # every rank's tuner must see the same clock (collective rebuild decisions)
+            import torch.distributed as dist
+            t = torch.tensor([build_pp], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            build_pp = float(t[0])
+        # rounded to two digits: run-to-run timing noise must not move a tuner decision
+        paper = paper_protocol(args, g2, mass, pos, vel, params, local, rank, world,
+                               tuner_clock=(float(f"{achieved * 1e12:.2g}"), float(f"{build_pp:.2g}")))
 
     hbm = hbm_phases(sim, r0, args.n) if rank == 0 else None
 
