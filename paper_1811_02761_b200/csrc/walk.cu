@@ -915,7 +915,8 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                     b.trace[2 * ts + 1] = make_uint4(grp, nbatch | (min(ndon, 0xfffu) << 8) | (min(maxlive, 0xfffu) << 20), macs, pushes);
                 }
             }
-            __threadfence();
+            // no fence: the pending count only ends the walk (its own earlier increments for donated
+            // batches are ordered before this decrement: same thread, same address)
             atomicSub(q_pending, 1u);
         }
     }
