@@ -173,6 +173,9 @@ int g2_sim_tuner_interval(g2_sim* s, size_t* interval);
 /* extension (diagnostics): how the Simulation's rebuilds sorted so far -- by the bucket sort of the
  * nearly sorted storage order, and by its onesweep radix fallback (a bucket over capacity) */
 int g2_sim_sort_stats(g2_sim* s, unsigned long long* bucket_sorts, unsigned long long* radix_fallbacks);
+/* extension (diagnostics): the last step walk's whole-system groups cut into slices (one per root
+ * child) and the number of slices over all ranks; synchronises the simulation's stream */
+int g2_sim_walk_slices(g2_sim* s, unsigned* heavy_groups, unsigned* slices);
 /* extension: the rebuild tuner's clock (RebuildTuner::record_walk/record_build, rebuild_tuner.hpp:18-31).
  * flop_rate <= 0: CUDA-event phase times (default).  flop_rate > 0: a deterministic model -- walk
  * seconds = (27 interactions + 5 MAC evaluations) / flop_rate (op_counters.hpp:50-63), build seconds =

@@ -125,9 +125,16 @@ struct ShardExchange : g2::Exchange {
         const size_t gs = sim.group_size(), ng_max = (sim.n() + gs - 1) / gs;
         return ((ng_max + world - 1) / world) * gs;
     }
+    g2::DBuf<float4> gathered_slices;  // [world][walk_slice_slots()] every rank's slice region
     void prepare(g2::Simulation& sim) {  // before the first step: the accumulator must not move later
-        sim.engine().reserve_accum(2 * sim.n() + 64 * sim.group_size());
+        sim.engine().reserve_accum(std::max(2 * sim.n() + 64 * sim.group_size(),
+                                            g2::walk_slice_base(sim.n()) + g2::walk_slice_slots()));
         gathered.reserve(window(sim, world) * world);
+        gathered_slices.reserve(g2::walk_slice_slots() * world);
+    }
+    void slice_source(g2::Simulation&, const float4*& src, size_t& stride) override {
+        src = gathered_slices.p;
+        stride = g2::walk_slice_slots();
     }
     virtual void transport(g2::Simulation& sim, const float4* send, size_t per_rank) = 0;
     void allgather_acc(g2::Simulation& sim) override {
@@ -148,6 +155,8 @@ struct NcclExchange final : ShardExchange {
     }
     void transport(g2::Simulation& sim, const float4* send, size_t per_rank) override {
         G2_NCCL(nccl().all_gather(send, gathered.p, per_rank * 4, ncclFloat32, comm, sim.engine().stream()));
+        G2_NCCL(nccl().all_gather(sim.engine().slice_region(), gathered_slices.p, g2::walk_slice_slots() * 4,
+                                  ncclFloat32, comm, sim.engine().stream()));
     }
     g2::DBuf<double> tbuf;
     void agree_times(g2::Simulation& sim, double& walk, double& build, bool sum_walk) override {
@@ -211,6 +220,8 @@ struct LocalExchange final : ShardExchange {
             G2_CUDA(cudaMemcpyAsync(gathered.p + size_t(q) * per_rank,
                                     o->engine().accum() + size_t(o->shard_lo()) * o->group_size(),
                                     per_rank * sizeof(float4), cudaMemcpyDefault, s));
+            G2_CUDA(cudaMemcpyAsync(gathered_slices.p + size_t(q) * g2::walk_slice_slots(), o->engine().slice_region(),
+                                    g2::walk_slice_slots() * sizeof(float4), cudaMemcpyDefault, s));
         }
         G2_CUDA(cudaStreamSynchronize(s));
         mesh->barrier();  // nobody reuses its accumulator before everyone copied
@@ -293,7 +304,7 @@ struct PeerExchange final : g2::Exchange {
         world = w, self = r;
         device = sim.engine().device();
         G2_CUDA(cudaSetDevice(device));
-        const size_t slots = sim.n() + 64 * sim.group_size();
+        const size_t slots = g2::walk_slice_base(sim.n()) + g2::walk_slice_slots();  // groups, then slices
         for (auto& b : buf) {
             G2_CUDA(cudaMalloc(&b, slots * sizeof(float4)));
             G2_CUDA(cudaMemset(b, 0, slots * sizeof(float4)));
@@ -688,6 +699,15 @@ int g2_sim_sort_stats(g2_sim* s, unsigned long long* bucket_sorts, unsigned long
     return guarded([&] {
         *bucket_sorts = s->s->engine().bucket_sorts();
         *radix_fallbacks = s->s->engine().bucket_fallbacks();
+    });
+}
+
+int g2_sim_walk_slices(g2_sim* s, unsigned* heavy_groups, unsigned* slices) {
+    return guarded([&] {
+        uint32_t q[16];
+        s->s->engine().read_qstate(q);
+        *slices = q[7];
+        *heavy_groups = q[9] ? q[7] / q[9] : 0u;
     });
 }
 

@@ -107,7 +107,7 @@ Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), devic
     n_sinks_.reserve(1);
     n_groups_.reserve(1);
     events_.reserve(3);
-    qstate_.reserve(8);
+    qstate_.reserve(16);
     queue_cap_ = 1u << 20;  // ring size of the walk's donated-task queue (walk.cu kRing)
     queue_.reserve(queue_cap_);
     batch_.reserve(size_t(queue_cap_) * 32);
@@ -135,7 +135,9 @@ void Engine::reserve(size_t n) {
         tgt_rank_.reserve(n);
     amag_s_.reserve(n), ax_s_.reserve(n), ay_s_.reserve(n), az_s_.reserve(n), pot_s_.reserve(n), out_.reserve(3 * n);
     sinks_.reserve(n), sinks_alt_.reserve(n);
-    groups_.reserve(n), accum_.reserve(n), group_inter_.reserve(n), rel_.reserve(n), leaf_of_.reserve(n);
+    groups_.reserve(n), accum_.reserve(walk_slice_base(n) + walk_slice_slots()), group_inter_.reserve(n),
+        rel_.reserve(n), leaf_of_.reserve(n);
+    heavy_.reserve(walk_heavy_words()), sliced_.reserve(n);
     ensure_cells(std::max<size_t>(n + 64, 1024));
     cap_ = n;
     ensure_task_pool(std::max<size_t>(size_t(1) << 16, n / 8));  // no allocation inside a timed walk
@@ -442,7 +444,8 @@ void Engine::events_host(EventsH& ev) const {
 
 
 EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, const double* amag_s,
-                     bool with_pot, bool sync_events, uint32_t group_lo, uint32_t group_hi, bool finalize) {
+                     bool with_pot, bool sync_events, uint32_t group_lo, uint32_t group_hi, bool finalize,
+                     int slice_rank, int slice_world, bool combine) {
     EventsH ev;
     if (c_.list_capacity < 1) throw Error(kDataError, "InteractionList: capacity must be >= 1");
     G2_CUDA(cudaMemsetAsync(events_.p, 0, 3 * sizeof(unsigned long long), s_));
@@ -504,6 +507,10 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
         G2_CUDA(cudaMemsetAsync(trace_n_.p, 0, 4, s_));
         b.trace = trace_.p, b.trace_n = trace_n_.p, b.trace_cap = 1u << 23;
     }
+    b.heavy = heavy_.p, b.sliced = sliced_.p;
+    b.slice_base = uint32_t(walk_slice_base(n_));
+    b.slice_world = std::max(1, slice_world), b.slice_rank = slice_rank;
+    G2_CUDA(cudaMemsetAsync(heavy_.p, 0, sizeof(uint32_t), s_));
     G2_CUDA(cudaMemsetAsync(group_inter_.p, 0, size_t(ng_cap) * 8, s_));
     launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
     WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
@@ -527,6 +534,9 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
         G2_COUNT(1), frontier_check_kernel<<<gridn(size_t(ng_cap) * (kMaxDepth + 1)), kB, 0, s_>>>(
             level_count_.p, size_t(ng_cap) * (kMaxDepth + 1), uint32_t(std::min<size_t>(cap, 0xffffffffu)),
             flags_.p);
+    last_walk_ = b;
+    walk_G_ = p_.G;
+    if (combine) combine_slices(slice_region(), 0, 1);
     if (finalize) launch_walk_finalize(b, n_sinks_cap, ax_s_.p, ay_s_.p, az_s_.p, with_pot ? pot_s_.p : nullptr, s_);
     if (trace_path) {
         uint32_t nt = 0;
@@ -542,6 +552,19 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     }
     if (sync_events) read_events(ev);
     return ev;
+}
+
+void Engine::combine_slices(const float4* src, size_t stride, int world) {
+    TreeView tv{xyzm_s_.p, nodes_.p, uint32_t(n_), nodes32_.p, rel_.p, leaf_of_.p};
+    WalkBuffers b = last_walk_;
+    b.accum = accum();
+    uint32_t* cost = peer_world_ > 1 && peer_cost_[peer_self_] ? peer_cost_[peer_self_] : nullptr;
+    launch_walk_combine(b, tv, src, stride, world, walk_G_, cost, s_);
+}
+
+void Exchange::slice_source(Simulation& sim, const float4*& src, size_t& stride) {
+    src = sim.engine().slice_region();
+    stride = 0;
 }
 
 EventsH Engine::evaluate(size_t n, const double* mass, const double* pos, const double* acc_old_mag,
@@ -867,9 +890,16 @@ StepResultH Simulation::step() {
     shard_lo_ = lo, shard_hi_ = hi;
     const bool sharded = exchange_ != nullptr;  // a mesh (a one-rank NCCL mesh included)
     if (sharded) exchange_->before_walk(*this);
-    eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false, lo, hi, false);
+    eng_.walk(sinks_.p, n_active_.p, uint32_t(n), amag_.p, false, false, lo, hi, false, sharded ? rank_ : 0,
+              sharded ? world_ : 1, !sharded);
     G2_CUDA(cudaEventRecord(ev_[4], s));
-    if (sharded) exchange_->allgather_acc(*this);  // every rank receives every group's accelerations
+    if (sharded) {
+        exchange_->allgather_acc(*this);  // every rank receives every group's accelerations
+        const float4* src = nullptr;      // and every slice of the whole-system groups
+        size_t stride = 0;
+        exchange_->slice_source(*this, src, stride);
+        eng_.combine_slices(src, stride, world_);
+    }
     G2_CUDA(cudaEventRecord(ev_[5], s));
     launch_correct(st, sinks_.p, n_active_.p, uint32_t(n), eng_.accum(), t_next_.p, now_, tick_, sd, s);
     if (sharded) eng_.set_peer_push(1, 0, nullptr, nullptr);  // other walks (init, evaluate) stay local

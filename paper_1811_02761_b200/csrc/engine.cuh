@@ -77,6 +77,10 @@ public:
     bool take_bucket_overflow();  // true (and clears) if the last rebuild's bucket sort overflowed (ditto)
     // rebuild sorts so far: by the bucket sort, and by its radix fallback (an overflowed bucket)
     unsigned long long bucket_sorts() const { return bucket_sorts_; }
+    void read_qstate(uint32_t* q16) {  // the last walk's queue state (diagnostics; synchronises)
+        G2_CUDA(cudaMemcpyAsync(q16, qstate_.p, 16 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
+        G2_CUDA(cudaStreamSynchronize(s_));
+    }
     unsigned long long bucket_fallbacks() const { return bucket_fallbacks_; }
     // boundary read-backs: enqueue copies into the pinned staging block, one sync, then inspect
     HostSync* host_sync() { return hs_; }
@@ -95,9 +99,14 @@ public:
     void calc_nodes();
     // walk sinks (sorted positions) with acc_old_mag (sorted); results into
     // ax_s/ay_s/az_s/pot_s at the sinks' sorted positions.
+    // slice_rank/slice_world: the ranks the whole-system groups' slices are dealt to; combine: form
+    // the sliced groups' results now (false: the caller calls combine_slices after the exchange)
     EventsH walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, const double* amag_s,
                  bool with_pot, bool sync_events, uint32_t group_lo = 0, uint32_t group_hi = ~0u,
-                 bool finalize = true);
+                 bool finalize = true, int slice_rank = 0, int slice_world = 1, bool combine = true);
+    // the last walk's sliced groups from the slice partials (slice j at src + (j % world) * stride + 32 j)
+    void combine_slices(const float4* src, size_t stride, int world);
+    const float4* slice_region() { return accum() + walk_slice_base(n_); }
     // accum slots -> FP64 accelerations at the sinks' sorted positions
     int device() const { return device_; }
     float4* accum() { return accum_ext_ ? accum_ext_ : accum_.p; }
@@ -168,6 +177,10 @@ private:
     uint32_t ls_host_[kMaxDepth + 3] = {};  // host copy of level_start of the current topology
     DBuf<float4> rel_;
     DBuf<uint32_t> leaf_of_;
+    DBuf<uint32_t> heavy_;
+    DBuf<uint8_t> sliced_;
+    WalkBuffers last_walk_{};  // the last walk's buffers (combine_slices)
+    double walk_G_ = 1.0;
     DBuf<uint4> int_list_;                  // internal cells per depth (launch_tree_topology)
     DBuf<uint32_t> int_count_;
     DBuf<uint32_t> level_start_, tile_counters_;
@@ -262,6 +275,8 @@ struct Exchange {
     virtual void before_walk(class Simulation&) {}  // e.g. point the walk at this step's exchange buffers
     virtual bool device_shards() const { return false; }  // the walk splits the groups on the device
     virtual void allgather_acc(class Simulation& sim) = 0;
+    // where every rank's slice partials are after allgather_acc (default: pushed into this rank's region)
+    virtual void slice_source(class Simulation& sim, const float4*& src, size_t& stride);
     // make the rebuild tuner's inputs identical on every rank (the rebuild decision reorders all state,
     // and the exchange addresses accumulators by slot): walk := sum (modelled time: each rank's share of
     // the walk work; the sum is the single-rank value) or max (measured) over ranks; build := max

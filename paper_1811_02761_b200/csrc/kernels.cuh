@@ -120,8 +120,9 @@ struct WalkBuffers {
                               // order_scratch is given; nullable: group index order
     uint32_t* order_scratch;  // [walk_order_scratch_words()] bucket counters of the ordering sort
     uint32_t queue_cap;
-    uint32_t* qstate;         // [8]: init claimed, donated reserved, pending, n_init, donated consumed, shard lo,
-                              //      task records used
+    uint32_t* qstate;         // [16]: init claimed, donated reserved, pending, n_init, donated consumed,
+                              //      shard lo, task records used, slices (all ranks), slices of this rank,
+                              //      slices per heavy group, groups of the shard
     uint32_t* spill;          // per-warp stack spill
     uint32_t* level_count;    // [n_groups * 22] frontier-cap check (nullable)
     uint64_t* group_inter;    // [n_groups] per-group interactions (nullable)
@@ -148,7 +149,22 @@ struct WalkBuffers {
     const uint32_t* ng_prev;            // groups behind cost_prev
     uint32_t* ng_cur;                   // groups of this step (written by the shard kernel)
     uint32_t* shard;                    // [2] device lo, hi (group indices) when cost-balanced
+    // whole-system groups: a group whose sphere radius reaches kHeavyFrac of the root's
+    // extent is cut into one slice per root child, the same slices for any rank count; slice j runs
+    // on rank j % world and its partial goes to slot j of every rank's slice region (accum +
+    // walk_slice_base(n)); walk_combine_slices then sums each group's slices in slice order
+    uint32_t* heavy;                    // [kMaxHeavy + 1]: candidates' count, then the heavy groups (sorted)
+    uint8_t* sliced;                    // [n_groups] 1: the group runs as slices (not an initial task)
+    uint32_t slice_base;                // accumulator slot of slice 0 (walk_slice_base(n))
+    int slice_world, slice_rank;        // the ranks the slices are dealt to (1, 0: all here)
 };
+size_t walk_slice_base(size_t n);      // first slice slot after n sinks
+size_t walk_slice_slots();             // slice-region slots (kMaxHeavy x 8 slices x 32 sinks)
+size_t walk_heavy_words();
+// every heavy group's accumulators = G x the sum of its slices in slice order (slice j read from
+// slices + (j % world) * rank_stride + 32 j); zero cost for heavy groups in cost (nullable)
+void launch_walk_combine(const WalkBuffers& b, const TreeView& t, const float4* slices, size_t rank_stride, int world,
+                         double G, uint32_t* cost, cudaStream_t s);
 size_t walk_spill_words();
 size_t walk_order_scratch_words();
 size_t walk_resident_warps();

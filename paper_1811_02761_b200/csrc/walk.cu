@@ -81,6 +81,17 @@ constexpr uint32_t kRing = 1u << kRingBits;
 constexpr uint64_t kGenMask = (1ull << 26) - 1;  // generation tag of a slot (ticket >> kRingBits)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kFirst = 1, kLast = 2;  // buffer header flags: first / last buffer of a task
+// whole-system groups run as slices (one per root child), the same slices for any rank count
+constexpr uint32_t kMaxHeavy = 128;         // heavy groups per walk (more candidates: no slicing)
+constexpr uint32_t kSlicesPer = 8;          // slice slots per heavy group (<= root children)
+#ifndef G2_HEAVY_FRAC
+#define G2_HEAVY_FRAC 0.25
+#endif
+#ifndef G2_SLICE_CONSUMER
+#define G2_SLICE_CONSUMER 1  // (A/B: 0 drops the slice path from the consumer -- wrong results with slices)
+#endif
+constexpr double kHeavyFrac = G2_HEAVY_FRAC;  // heavy: sphere radius >= kHeavyFrac x the root's extent
+constexpr uint32_t kSliceTag = 0xC0000000u; // task-record parent tag of a slice's root record (| slice index)
 constexpr uint32_t kStop = ~0u;            // header group id that retires the consumer
 
 // Interaction list in pair-interleaved layout so the flush runs on packed
@@ -478,6 +489,15 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                         done = true;
                         break;
                     }
+                    if (G2_SLICE_CONSUMER && R.x >= kSliceTag) {  // a slice's root: its partial to slot j of every rank
+                        const size_t sl = size_t(b.slice_base) + size_t(R.x - kSliceTag) * 32 + lane;
+                        if (has_sink) {
+                            b.accum[sl] = acc;
+                            for (int q = 0; q < b.world; ++q)
+                                if (q != b.self) b.peer_accum[q][sl] = acc;
+                        }
+                        break;  // done stays false: walk_combine_slices forms the group's result
+                    }
                     if (has_sink) __stcg(&b.tacc[size_t(r) * 32 + lane], acc);
                     __threadfence();
                     __syncwarp();
@@ -519,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
     uint32_t* q_dtail = b.qstate + 1;  // donated slots reserved
     uint32_t* q_pending = b.qstate + 2;
     uint32_t* q_dhead = b.qstate + 4;  // donated slots claimed
-    const uint32_t ng = b.qstate[3];   // initial tasks (written by walk_init)
+    const uint32_t ng = b.qstate[3];   // initial tasks (written by walk_init / the ordering)
     const uint32_t glo = b.qstate[5];  // first group of this launch's shard (walk_init)
     // donation trigger: list entries written since the task's last donation (work done, not time),
     // scaled with the groups per producer warp of a full grid (a constant: identical on every rank)
@@ -588,8 +608,8 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         if (e == kEmpty) break;
         slot = __shfl_sync(kFull, slot, 0);
         const uint32_t grp = uint32_t(e >> 32), nbatch = uint32_t(e) & 63u;
-        // task record (lane 0): a donated task was given one by its donor; a group's initial task
-        // allocates one at its first donation
+        // task record (lane 0): a donated task was given one by its donor (a whole-system group's slice:
+        // its reserved slice record); a group's initial task allocates one at its first donation
         uint32_t rec = nbatch ? b.batch_rec[slot] : kNone, last_child = kNone;
 
         // ---------------- group
@@ -668,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             // ---- rejected internal cells: children onto the stack (cooperative)
             if (ctot) {
                 if (kCheck) {
-                    uint32_t* lc = &b.level_count[size_t(grp - glo) * (kMaxDepth + 1) + 1u];
+                    uint32_t* lc = &b.level_count[size_t(grp) * (kMaxDepth + 1) + 1u];
                     if (nchild0) atomicAdd(lc + ((s0.info >> 8) & 31u), nchild0);
                     if (nchild1) atomicAdd(lc + ((s1.info >> 8) & 31u), nchild1);
                 }
@@ -982,8 +1002,18 @@ __global__ void __launch_bounds__(256) groups_kernel(TreeView t, const double* _
 #pragma unroll
         for (int o = kGroupLanes / 2; o > 0; o >>= 1) r2 = smax(r2, __shfl_xor_sync(kFull, r2, o));
         if (gon && sub == 0) {
-            b.groups[g] = GroupRec{cx, cy, cz, dsqrt(r2), am, first, cnt};
+            const double radius = dsqrt(r2);
+            b.groups[g] = GroupRec{cx, cy, cz, radius, am, first, cnt};
+            b.sliced[g] = 0;
             if (b.world > 1) b.gcost[g] = 0u;
+            // whole-system group (sphere reaching a quarter of the root's extent): sliced when the
+            // root is internal; candidates beyond kMaxHeavy switch slicing off for this walk
+            const bool heavy = !(t.nodes32[0].info & kLeafBit) && (t.nodes32[0].info & 0xffu) >= 2u &&
+                               radius >= kHeavyFrac * t.nodes[0].extent;
+            if (heavy) {
+                const uint32_t h = atomicAdd(&b.heavy[0], 1u);
+                if (h < kMaxHeavy) b.heavy[1 + h] = g;
+            }
         }
     }
 }
@@ -1039,19 +1069,102 @@ __global__ void __launch_bounds__(kShardThreads) shard_kernel(const uint32_t* __
     }
 }
 
-__global__ void walk_init_kernel(WalkBuffers b) {
+// One block of kMaxHeavy threads: the queue state, and the whole-system groups' slices.  The heavy
+// candidates (group setup) are sorted by index (their discovery order is a race; the slice numbering
+// must not be); a candidate whose root MAC accepts (a single entry) stays a plain group.  Slice j
+// (group j / nk, root child j % nk) belongs to rank j % world; this rank's slices are published as
+// donated tasks of one cell (the root child) with the reserved record j, so the walk takes them
+// first and runs them with no change to its task code; the root's MAC evaluation is counted once,
+// by the owner of the group's slice 0.  The initial-task ordering leaves the sliced groups out.
+__global__ void __launch_bounds__(kMaxHeavy) walk_init_kernel(WalkBuffers b, TreeView t, WalkParams p, int sworld,
+                                                              int sself, int ordered) {
+    __shared__ uint32_t sorted[kMaxHeavy];
+    __shared__ uint32_t wsum[kMaxHeavy / 32 + 1];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const uint32_t cand = b.heavy[0];
+    const uint32_t rinfo = t.nodes32[0].info;
+    const uint32_t nc = (rinfo & kLeafBit) ? 0u : (rinfo & 0xffu);
+    const uint32_t nh0 = (ordered && cand <= kMaxHeavy && nc >= 2u) ? cand : 0u;
+    uint32_t v = 0;
+    if (threadIdx.x < nh0) {
+        v = b.heavy[1 + threadIdx.x];
+        uint32_t r = 0;
+        for (uint32_t q = 0; q < nh0; ++q) r += b.heavy[1 + q] < v;
+        sorted[r] = v;
+    }
+    __syncthreads();
+    // the root MAC of each candidate in index order (exact, traversal.cpp:40-56): rejected -> sliced
+    bool keep = false;
+    if (threadIdx.x < nh0) {
+        v = sorted[threadIdx.x];
+        const GroupRec g = b.groups[v];
+        const bool geom = p.force_geometric || g.a_min <= 0.0;
+        keep = !mac_exact(t.nodes[0], g, p, dmul(p.dacc, g.a_min), geom);
+    }
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wsum[w] = __popc(m);
+    __syncthreads();
+    uint32_t before = 0, nh = 0;
+    for (int q = 0; q < kMaxHeavy / 32; ++q) before += q < w ? wsum[q] : 0u, nh += wsum[q];
+    const uint32_t h_of = before + __popc(m & ((1u << lane) - 1u));
+    __syncthreads();
+    if (keep) {
+        b.heavy[1 + h_of] = v;
+        b.sliced[v] = 1;
+    }
+    const uint32_t nk = min(nc, kSlicesPer), nsl = nh * nk;
+    const uint32_t mine = nsl > uint32_t(sself) ? (nsl - uint32_t(sself) + uint32_t(sworld) - 1) / uint32_t(sworld) : 0u;
+    __syncthreads();  // the final heavy list
+    for (uint32_t i = threadIdx.x; i < mine; i += blockDim.x) {
+        const uint32_t j = uint32_t(sself) + i * uint32_t(sworld);
+        const uint32_t grp = b.heavy[1 + j / nk], k = j % nk;
+        b.trec[j] = make_uint4(kSliceTag | j, 1u, kNone, kNone);
+        b.batch[size_t(i) * 32] = t.nodes32[0].link + k;  // root child k
+        b.batch_rec[i] = j;
+        b.queue[i] = (uint64_t(grp) << 32) | 1u;  // ticket i: generation 0, one cell
+        if (k == 0 && p.count_ops) atomicAdd(&b.events[1], 1ull);  // the root's MAC evaluation
+    }
     if (threadIdx.x == 0) {
         const uint32_t n_groups = *b.n_groups;
         const uint32_t lo = b.shard ? b.shard[0] : b.group_lo;
         const uint32_t hi = min(b.shard ? b.shard[1] : b.group_hi, n_groups);
         const uint32_t ng = hi > lo ? hi - lo : 0u;
         b.qstate[5] = lo;
-        b.qstate[0] = 0;   // initial tasks claimed
-        b.qstate[1] = 0;   // donated slots reserved
-        b.qstate[2] = ng;  // tasks pending
-        b.qstate[3] = ng;  // initial tasks
-        b.qstate[4] = 0;   // donated slots consumed
-        b.qstate[6] = 0;   // task records used
+        b.qstate[0] = 0;          // initial tasks claimed
+        b.qstate[1] = mine;       // donated slots reserved (this rank's slices)
+        b.qstate[2] = ng + mine;  // tasks pending (the ordering subtracts the sliced groups)
+        b.qstate[3] = ng;         // initial tasks (likewise)
+        b.qstate[4] = 0;          // donated slots consumed
+        b.qstate[6] = nsl;        // task records used (slice records 0 .. nsl-1 reserved)
+        b.qstate[7] = nsl;        // slices of all ranks
+        b.qstate[8] = mine;       // this rank's slices
+        b.qstate[9] = nk;         // slices per heavy group
+        b.qstate[10] = ng;        // the shard's groups
+    }
+}
+
+// every heavy group: G x (slice 0 + slice 1 + ...) in slice order, one warp per group
+__global__ void __launch_bounds__(256) combine_slices_kernel(WalkBuffers b, const float4* __restrict__ slices,
+                                                             size_t rank_stride, int world, float G,
+                                                             uint32_t* cost) {
+    const uint32_t nsl = b.qstate[7], nk = b.qstate[9];
+    const uint32_t nh = nk ? nsl / nk : 0u;
+    const int lane = threadIdx.x & 31;
+    for (uint32_t h = blockIdx.x * 8 + (threadIdx.x >> 5); h < nh; h += gridDim.x * 8) {
+        const uint32_t g = b.heavy[1 + h];
+        const GroupRec gr = b.groups[g];
+        if (lane == 0 && cost) cost[g] = 0u;  // sliced groups are not in the contiguous shards' balance
+        if (uint32_t(lane) >= gr.count) continue;
+        float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (uint32_t k = 0; k < nk; ++k) {
+            const uint32_t j = h * nk + k;
+            const float4 v = slices[size_t(j % uint32_t(world)) * rank_stride + size_t(j) * 32 + lane];
+            if (k == 0)
+                tot = v;
+            else
+                tot.x += v.x, tot.y += v.y, tot.z += v.z, tot.w += v.w;
+        }
+        b.accum[gr.first + lane] = make_float4(G * tot.x, G * tot.y, G * tot.z, G * tot.w);
     }
 }
 
@@ -1065,18 +1178,18 @@ __device__ __forceinline__ uint32_t order_bucket(double radius) {
     return uint32_t(kOrderBuckets - 1) - min(__float_as_uint(float(radius)) >> 20, uint32_t(kOrderBuckets - 1));
 }
 __global__ void __launch_bounds__(256) order_hist_kernel(const GroupRec* __restrict__ groups, const uint32_t* qstate,
-                                                         uint32_t* hist) {
+                                                         const uint8_t* __restrict__ sliced, uint32_t* hist) {
     __shared__ uint32_t h[kOrderBuckets];
     for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x) h[i] = 0;
     __syncthreads();
     const uint32_t lo = qstate[5], ng = qstate[3];
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x)
-        atomicAdd(&h[order_bucket(groups[lo + i].radius)], 1u);
+        if (!sliced[lo + i]) atomicAdd(&h[order_bucket(groups[lo + i].radius)], 1u);
     __syncthreads();
     for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x)
         if (h[i]) atomicAdd(&hist[i], h[i]);
 }
-__global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist) {
+__global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist, uint32_t* qstate) {
     __shared__ uint32_t part[1024];
     const uint32_t a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
     part[threadIdx.x] = a + c;
@@ -1089,12 +1202,17 @@ __global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist) {
     }
     const uint32_t ex = part[threadIdx.x] - (a + c);
     hist[2 * threadIdx.x] = ex, hist[2 * threadIdx.x + 1] = ex + a;
+    if (threadIdx.x == 1023) {  // the initial tasks: the shard's groups less the sliced ones
+        qstate[2] -= qstate[3] - part[1023];
+        qstate[3] = part[1023];
+    }
 }
 __global__ void __launch_bounds__(256) order_scatter_kernel(const GroupRec* __restrict__ groups, const uint32_t* qstate,
-                                                            uint32_t* off, uint32_t* order) {
-    const uint32_t lo = qstate[5], ng = qstate[3];
+                                                            const uint8_t* __restrict__ sliced, uint32_t* off,
+                                                            uint32_t* order) {
+    const uint32_t lo = qstate[5], ng = qstate[10];  // the shard's groups (walk_init)
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x)
-        order[atomicAdd(&off[order_bucket(groups[lo + i].radius)], 1u)] = i;
+        if (!sliced[lo + i]) order[atomicAdd(&off[order_bucket(groups[lo + i].radius)], 1u)] = i;
 }
 
 // zero the accumulator slots this launch accumulates into: all sinks, or with a peer exchange
@@ -1150,6 +1268,16 @@ void walk_launch_t(const TreeView& t, const WalkParams& p, const WalkBuffers& b,
 }  // namespace
 
 size_t walk_spill_words() { return kSpillWords; }
+size_t walk_slice_base(size_t n) { return (n + 31) / 32 * 32 + 64 * 32; }
+size_t walk_slice_slots() { return size_t(kMaxHeavy) * kSlicesPer * 32; }
+size_t walk_heavy_words() { return kMaxHeavy + 1; }
+
+void launch_walk_combine(const WalkBuffers& b, const TreeView&, const float4* slices, size_t rank_stride, int world,
+                         double G, uint32_t* cost, cudaStream_t s) {
+    G2_COUNT(1), combine_slices_kernel<<<(kMaxHeavy + 7) / 8, 256, 0, s>>>(b, slices, rank_stride, std::max(1, world),
+                                                                            float(G), cost);
+    G2_CUDA(cudaGetLastError());
+}
 size_t walk_order_scratch_words() { return kOrderBuckets; }
 size_t walk_resident_warps() {
     // producer warps (one spill stack each) of the largest grid walk_launch_t can use
@@ -1178,13 +1306,14 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
         G2_CUDA(cudaGetLastError());
     }
     G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi, b.shard, gs);
-    G2_COUNT(1), walk_init_kernel<<<1, 32, 0, s>>>(b);
+    G2_COUNT(1), walk_init_kernel<<<1, kMaxHeavy, 0, s>>>(b, t, p, b.slice_world, b.slice_rank,
+                                                          b.order_scratch != nullptr);
     if (b.order_scratch) {
         const unsigned ob = std::max(1u, std::min<unsigned>(ceil_div(ceil_div(n_sinks_cap, gs), 256), kNumSMs * 4));
         G2_CUDA(cudaMemsetAsync(b.order_scratch, 0, kOrderBuckets * sizeof(uint32_t), s));
-        G2_COUNT(1), order_hist_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.order_scratch);
-        G2_COUNT(1), order_scan_kernel<<<1, 1024, 0, s>>>(b.order_scratch);
-        G2_COUNT(1), order_scatter_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.order_scratch,
+        G2_COUNT(1), order_hist_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.sliced, b.order_scratch);
+        G2_COUNT(1), order_scan_kernel<<<1, 1024, 0, s>>>(b.order_scratch, b.qstate);
+        G2_COUNT(1), order_scatter_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.sliced, b.order_scratch,
                                                              const_cast<uint32_t*>(b.order));
     }
     // the guarded flush whenever eps^2 is not a normal FP32 number (eps == 0 included): with eps^2

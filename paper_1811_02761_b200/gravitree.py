@@ -422,6 +422,12 @@ class Simulation:
         _chk(_lib.g2_sim_sort_stats(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
 
+    def walk_slices(self) -> tuple:
+        """(whole-system groups cut into slices, slices over all ranks) of the last step's walk."""
+        a, b = C.c_uint(), C.c_uint()
+        _chk(_lib.g2_sim_walk_slices(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def system(self) -> ParticleSystem:
         n = self._n
         pos, vel, acc = np.empty((n, 3)), np.empty((n, 3)), np.empty((n, 3))

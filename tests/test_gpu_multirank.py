@@ -54,6 +54,11 @@ def test_sharded_steps_match_single_rank(world, mesh):
         assert sum(o.events.interactions for o in out) == r0.events.interactions
         assert sum(o.events.mac_evals for o in out) == r0.events.mac_evals
         assert all(o.active == r0.active for o in out)
+    # whole-system groups were cut into slices, dealt round-robin to the ranks: the same
+    # slices for any rank count, summed in slice order -- hence still bit-identical
+    heavy, slices = ref.walk_slices()
+    assert heavy > 0 and slices >= 2 * heavy, (heavy, slices)
+    assert all(s.walk_slices() == (heavy, slices) for s in sims)
     a = ref.system()
     for s in sims:
         b = s.system()
