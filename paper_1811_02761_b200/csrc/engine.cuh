@@ -104,7 +104,7 @@ public:
     EventsH walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_t n_sinks_cap, const double* amag_s,
                  bool with_pot, bool sync_events, uint32_t group_lo = 0, uint32_t group_hi = ~0u,
                  bool finalize = true, int slice_rank = 0, int slice_world = 1, bool combine = true);
-    // the last walk's sliced groups from the slice partials (slice j at src + (j % world) * stride + 32 j)
+    // the last walk's sliced groups from the slice partials (slice j at src + owner(j) * stride + 32 j)
     void combine_slices(const float4* src, size_t stride, int world);
     const float4* slice_region() { return accum() + walk_slice_base(n_); }
     // accum slots -> FP64 accelerations at the sinks' sorted positions

@@ -151,7 +151,7 @@ struct WalkBuffers {
     uint32_t* shard;                    // [2] device lo, hi (group indices) when cost-balanced
     // whole-system groups: a group whose sphere radius reaches kHeavyFrac of the root's
     // extent is cut into one slice per root child, the same slices for any rank count; slice j runs
-    // on rank j % world and its partial goes to slot j of every rank's slice region (accum +
+    // on rank owner(j) (dealt by expected cost) and its partial goes to slot j of every rank's slice region (accum +
     // walk_slice_base(n)); walk_combine_slices then sums each group's slices in slice order
     uint32_t* heavy;                    // [kMaxHeavy + 1]: candidates' count, then the heavy groups (sorted)
     uint8_t* sliced;                    // [n_groups] 1: the group runs as slices (not an initial task)
@@ -162,7 +162,7 @@ size_t walk_slice_base(size_t n);      // first slice slot after n sinks
 size_t walk_slice_slots();             // slice-region slots (kMaxHeavy x 8 slices x 32 sinks)
 size_t walk_heavy_words();
 // every heavy group's accumulators = G x the sum of its slices in slice order (slice j read from
-// slices + (j % world) * rank_stride + 32 j); zero cost for heavy groups in cost (nullable)
+// slices + owner(j) * rank_stride + 32 j); zero cost for heavy groups in cost (nullable)
 void launch_walk_combine(const WalkBuffers& b, const TreeView& t, const float4* slices, size_t rank_stride, int world,
                          double G, uint32_t* cost, cudaStream_t s);
 size_t walk_spill_words();

