@@ -61,15 +61,36 @@ __global__ void __launch_bounds__(kBlock) norm3_kernel(const double* ax, const d
 __device__ __forceinline__ uint64_t level_ticks(int level) { return 1ull << (kMaxBlockLevel - level); }
 
 // ---- t_next = min_i last_update + ticks(level) (integrator.cpp:103-105) -------
+// 16 particles per thread and step (one 16-byte load of levels, eight of update times), one atomic
+// per block (a same-address atomic per warp serialised at L2)
 __global__ void __launch_bounds__(kBlock) tnext_kernel(const uint8_t* __restrict__ level,
                                                        const uint64_t* __restrict__ last, size_t n,
                                                        unsigned long long* t_next) {
     unsigned long long m = ~0ull;
-    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
+    const size_t n16 = n / 16;
+    for (size_t i = blockIdx.x * size_t(kBlock) + threadIdx.x; i < n16; i += size_t(gridDim.x) * kBlock) {
+        const uint4 lv = reinterpret_cast<const uint4*>(level)[i];
+        const uint32_t lw[4] = {lv.x, lv.y, lv.z, lv.w};
+        const ulonglong2* lp = reinterpret_cast<const ulonglong2*>(last) + 8 * i;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const ulonglong2 t = lp[q];
+            const uint32_t w = lw[q >> 1], sh = 16 * (q & 1);
+            m = min(m, (unsigned long long)(t.x + level_ticks(uint8_t(w >> sh))));
+            m = min(m, (unsigned long long)(t.y + level_ticks(uint8_t(w >> (sh + 8)))));
+        }
+    }
+    for (size_t i = 16 * n16 + blockIdx.x * size_t(kBlock) + threadIdx.x; i < n; i += size_t(gridDim.x) * kBlock)
         m = min(m, (unsigned long long)(last[i] + level_ticks(level[i])));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if ((threadIdx.x & 31) == 0 && m != ~0ull) atomicMin(t_next, m);
+    __shared__ unsigned long long wm[kBlock / 32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int q = 1; q < kBlock / 32; ++q) m = min(m, wm[q]);
+        if (m != ~0ull) atomicMin(t_next, m);
+    }
 }
 
 // ---- predict (integrator.cpp:40-45) on ALL particles + active flags (:107-110), two particles per
@@ -435,7 +456,8 @@ void launch_norm3(const double* ax, const double* ay, const double* az, double* 
 
 void launch_tnext(const StepState& st, size_t n, unsigned long long* t_next, cudaStream_t s) {
     G2_CUDA(cudaMemsetAsync(t_next, 0xff, sizeof(unsigned long long), s));
-    G2_COUNT(1), tnext_kernel<<<grid_for(n), kBlock, 0, s>>>(st.level, st.last_update, n, t_next);
+    G2_COUNT(1), tnext_kernel<<<std::max(1u, std::min<unsigned>(ceil_div(n, size_t(kBlock) * 16), kNumSMs * 8)), kBlock, 0,
+                                 s>>>(st.level, st.last_update, n, t_next);
 }
 
 unsigned predict_blocks(size_t n) { return grid_for(n / 2 + 1); }
