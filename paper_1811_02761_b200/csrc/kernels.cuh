@@ -103,7 +103,7 @@ struct WalkParams {
     // a task donates half of its pending cells after writing D list entries since its last donation,
     // D = clamp(donate_scale x groups per producer warp, donate_few, donate_pushes): small walks
     // (block steps) split their groups finer; deterministic: D depends on the TOTAL group count only
-    uint32_t donate_pushes = 2048, donate_few = 512, donate_scale = 256;  // paper-protocol sweep, profiles/r2_donation_sweep.md
+    uint32_t donate_pushes = 4096, donate_few = 512, donate_scale = 256;  // sweeps: profiles/r2_donation_sweep.md
     double mass_max = 0.0;    // largest particle mass (host-known): guards the FP32 self-pair factor
 };
 constexpr int kMaxPeers = 8;

@@ -640,19 +640,23 @@ __global__ void __launch_bounds__(kLeafThreads) calc_leaf_kernel(const double4* 
 }
 
 #if G2_CALC_LEAF_CELLS
-// (A/B) leaves in cell order, one thread per cell
-// a leaf of at most 8 particles, same operation order as the general loop below
+// leaves in cell order, one thread per cell
+#ifndef G2_LEAF_SMALL
+#define G2_LEAF_SMALL 8
+#endif
+constexpr int kLeafSmall = G2_LEAF_SMALL;  // leaves held in registers (larger: two passes over L1)
+// a leaf of at most kLeafSmall particles, same operation order as the general loop below
 __device__ __forceinline__ void leaf_small(const double4* __restrict__ xyzm, uint32_t f, uint32_t cnt, uint32_t c,
                                            WNode* __restrict__ nodes, WNode32* __restrict__ nodes32,
                                            float4* __restrict__ rel) {
-    double4 p[8];
+    double4 p[kLeafSmall];
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < kLeafSmall; ++j)
         if (j < int(cnt)) p[j] = xyzm[f + j];
     WNode nd;
     double m = 0.0, wx = 0.0, wy = 0.0, wz = 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < kLeafSmall; ++j)
         if (j < int(cnt)) {
             m = dadd(m, p[j].w);
             wx = dadd(wx, dmul(p[j].w, p[j].x));
@@ -664,7 +668,7 @@ __device__ __forceinline__ void leaf_small(const double4* __restrict__ xyzm, uin
     const double c32x = double(float(nd.cx)), c32y = double(float(nd.cy)), c32z = double(float(nd.cz));
     double e2 = 0.0;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
+    for (int j = 0; j < kLeafSmall; ++j)
         if (j < int(cnt)) {
             e2 = smax(e2, norm2(dsub(p[j].x, nd.cx), dsub(p[j].y, nd.cy), dsub(p[j].z, nd.cz)));
             rel[f + j] = make_float4(float(dsub(p[j].x, c32x)), float(dsub(p[j].y, c32y)), float(dsub(p[j].z, c32z)),
@@ -688,7 +692,7 @@ __global__ void __launch_bounds__(kBlock, G2_CALC_MINB) calc_leaf_cells_kernel(c
     for (uint32_t c = blockIdx.x * kBlock + threadIdx.x; c < total; c += gridDim.x * kBlock) {
         if (child_count[c]) continue;
         const uint32_t f = first[c], k1 = f + count[c];
-        if (k1 - f <= 8) {  // the usual leaf: every particle loaded up front, one memory round trip
+        if (k1 - f <= uint32_t(kLeafSmall)) {  // the usual leaf: every particle loaded up front, one memory round trip
             leaf_small(xyzm, f, k1 - f, c, nodes, nodes32, rel);
             continue;
         }
