@@ -141,7 +141,7 @@ void Engine::reserve(size_t n) {
     ensure_cells(std::max<size_t>(n + 64, 1024));
     cap_ = n;
     ensure_task_pool(std::max<size_t>(size_t(1) << 16, n / 8));  // no allocation inside a timed walk
-    order_.reserve(n + 1), order_scratch_.reserve(walk_order_scratch_words());
+    order_.reserve(n + 1), order_scratch_.reserve(walk_order_scratch_words(n));
 }
 
 void Engine::ensure_task_pool(size_t want) {
@@ -498,6 +498,7 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     static const bool no_order = std::getenv("G2_NO_ORDER") != nullptr;  // development A/B
     if (!no_order) {
         order_.reserve(ng_cap + 1);  // no-op unless targets with duplicates outnumber the particles
+        order_scratch_.reserve(walk_order_scratch_words(ng_cap));
         b.order = order_.p, b.order_scratch = order_scratch_.p;
     }
     static const char* trace_path = std::getenv("G2_WALK_TRACE");  // development: per-task timeline

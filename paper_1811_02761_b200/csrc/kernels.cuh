@@ -118,7 +118,7 @@ struct WalkBuffers {
     uint32_t* batch;          // [queue_cap * 32] cells of each donated slot
     const uint32_t* order;    // [n_groups] initial-task order (heaviest first), written by the launcher when
                               // order_scratch is given; nullable: group index order
-    uint32_t* order_scratch;  // [walk_order_scratch_words()] bucket counters of the ordering sort
+    uint32_t* order_scratch;  // [walk_order_scratch_words(n)] bucket counters + tile counts of the ordering
     uint32_t queue_cap;
     uint32_t* qstate;         // [16]: init claimed, donated reserved, pending, n_init, donated consumed,
                               //      shard lo, task records used, slices (all ranks), slices of this rank,
@@ -166,7 +166,7 @@ size_t walk_heavy_words();
 void launch_walk_combine(const WalkBuffers& b, const TreeView& t, const float4* slices, size_t rank_stride, int world,
                          double G, uint32_t* cost, cudaStream_t s);
 size_t walk_spill_words();
-size_t walk_order_scratch_words();
+size_t walk_order_scratch_words(size_t n_groups);
 size_t walk_resident_warps();
 void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffers& b, uint32_t group_size,
                    uint32_t n_sinks_cap, cudaStream_t s);

@@ -1128,6 +1128,8 @@ __global__ void __launch_bounds__(kMaxHeavy) walk_init_kernel(WalkBuffers b, Tre
     if (keep) {
         b.heavy[1 + h_of] = v;
         b.sliced[v] = 1;
+        // the root's expansion, which no slice task performs, in the frontier-cap counters
+        if (b.level_count) atomicAdd(&b.level_count[size_t(v) * (kMaxDepth + 1) + 1u + ((rinfo >> 8) & 31u)], nc);
     }
     const uint32_t nk = min(nc, kSlicesPer), nsl = nh * nk;
     // slices to ranks: classes of equal expected cost (root child k: cost ~ its mass) dealt heaviest
@@ -1199,6 +1201,10 @@ __global__ void __launch_bounds__(256) combine_slices_kernel(WalkBuffers b, Tree
 // of the FP32 radius, 2048 buckets).  The order only schedules: every group's task tree, and hence its
 // result, is the same in any order.
 constexpr int kOrderBuckets = 2048;
+#ifndef G2_ORDER_HEAVY
+#define G2_ORDER_HEAVY 1.0
+#endif
+constexpr float kOrderHeavy = G2_ORDER_HEAVY;  // fraction of the groups ordered largest sphere first
 __device__ __forceinline__ uint32_t order_bucket(double radius) {
     return uint32_t(kOrderBuckets - 1) - min(__float_as_uint(float(radius)) >> 20, uint32_t(kOrderBuckets - 1));
 }
@@ -1214,7 +1220,7 @@ __global__ void __launch_bounds__(256) order_hist_kernel(const GroupRec* __restr
     for (int i = threadIdx.x; i < kOrderBuckets; i += blockDim.x)
         if (h[i]) atomicAdd(&hist[i], h[i]);
 }
-__global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist, uint32_t* qstate) {
+__global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist, uint32_t* qstate, float heavy) {
     __shared__ uint32_t part[1024];
     const uint32_t a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
     part[threadIdx.x] = a + c;
@@ -1227,17 +1233,79 @@ __global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist, uint32
     }
     const uint32_t ex = part[threadIdx.x] - (a + c);
     hist[2 * threadIdx.x] = ex, hist[2 * threadIdx.x + 1] = ex + a;
-    if (threadIdx.x == 1023) {  // the initial tasks: the shard's groups less the sliced ones
-        qstate[2] -= qstate[3] - part[1023];
-        qstate[3] = part[1023];
+    // the heavy class: the largest spheres up to a fraction `heavy` of the groups, whole buckets; the
+    // rest keeps index (Morton) order, so concurrently walked groups share tree nodes in L2
+    __shared__ uint32_t cut;
+    if (threadIdx.x == 0) cut = heavy <= 0.f ? 0u : kOrderBuckets;
+    __syncthreads();
+    const uint32_t total = part[1023];
+    const uint32_t lim = uint32_t(ceilf(heavy * float(total)));
+    if (heavy > 0.f && heavy < 1.f) {
+        if (ex < lim && ex + a >= lim) atomicMin(&cut, 2 * threadIdx.x + 1);
+        if (ex + a < lim && ex + a + c >= lim) atomicMin(&cut, 2 * threadIdx.x + 2);
     }
+    __syncthreads();
+    if (threadIdx.x == 1023) {  // the initial tasks: the shard's groups less the sliced ones
+        qstate[2] -= qstate[3] - total;
+        qstate[3] = total;
+        qstate[12] = cut;
+    }
+    if (cut < kOrderBuckets && threadIdx.x == cut / 2) qstate[13] = (cut & 1) ? ex + a : ex;  // heavy count
+    if (cut >= kOrderBuckets && threadIdx.x == 1023) qstate[13] = total;
 }
 __global__ void __launch_bounds__(256) order_scatter_kernel(const GroupRec* __restrict__ groups, const uint32_t* qstate,
                                                             const uint8_t* __restrict__ sliced, uint32_t* off,
                                                             uint32_t* order) {
     const uint32_t lo = qstate[5], ng = qstate[10];  // the shard's groups (walk_init)
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x)
-        if (!sliced[lo + i]) order[atomicAdd(&off[order_bucket(groups[lo + i].radius)], 1u)] = i;
+    const uint32_t cut = qstate[12];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
+        if (sliced[lo + i]) continue;
+        const uint32_t bk = order_bucket(groups[lo + i].radius);
+        if (bk < cut) order[atomicAdd(&off[bk], 1u)] = i;
+    }
+}
+
+// the light class in index order after the heavy one: per-tile counts, then an ordered scatter
+constexpr int kOrderTile = 1024;
+__device__ __forceinline__ bool order_light(const GroupRec* __restrict__ groups, const uint8_t* __restrict__ sliced,
+                                            uint32_t lo, uint32_t ng, uint32_t cut, uint32_t i) {
+    return i < ng && !sliced[lo + i] && order_bucket(groups[lo + i].radius) >= cut;
+}
+__global__ void __launch_bounds__(kOrderTile) order_light_count_kernel(const GroupRec* __restrict__ groups,
+                                                                       const uint32_t* qstate,
+                                                                       const uint8_t* __restrict__ sliced,
+                                                                       uint32_t* tile_count) {
+    const uint32_t lo = qstate[5], ng = qstate[10], cut = qstate[12];
+    const uint32_t i = blockIdx.x * kOrderTile + threadIdx.x;
+    const uint32_t m = __ballot_sync(0xffffffffu, order_light(groups, sliced, lo, ng, cut, i));
+    __shared__ uint32_t c;
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0 && m) atomicAdd(&c, uint32_t(__popc(m)));
+    __syncthreads();
+    if (threadIdx.x == 0) tile_count[blockIdx.x] = c;
+}
+__global__ void __launch_bounds__(kOrderTile) order_light_scatter_kernel(const GroupRec* __restrict__ groups,
+                                                                         const uint32_t* qstate,
+                                                                         const uint8_t* __restrict__ sliced,
+                                                                         const uint32_t* __restrict__ tile_count,
+                                                                         uint32_t* order) {
+    const uint32_t lo = qstate[5], ng = qstate[10], cut = qstate[12];
+    const uint32_t i = blockIdx.x * kOrderTile + threadIdx.x;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __shared__ uint32_t wsum[kOrderTile / 32], base;
+    if (threadIdx.x == 0) {
+        uint32_t b = qstate[13];  // after the heavy class
+        for (uint32_t t = 0; t < blockIdx.x; ++t) b += tile_count[t];
+        base = b;
+    }
+    const bool light = order_light(groups, sliced, lo, ng, cut, i);
+    const uint32_t m = __ballot_sync(0xffffffffu, light);
+    if (lane == 0) wsum[w] = __popc(m);
+    __syncthreads();
+    uint32_t before = base;
+    for (int q = 0; q < w; ++q) before += wsum[q];
+    if (light) order[before + __popc(m & ((1u << lane) - 1u))] = i;
 }
 
 // zero the accumulator slots this launch accumulates into: all sinks, or with a peer exchange
@@ -1303,7 +1371,7 @@ void launch_walk_combine(const WalkBuffers& b, const TreeView& t, const float4* 
                                                                             std::max(1, world), float(G), cost);
     G2_CUDA(cudaGetLastError());
 }
-size_t walk_order_scratch_words() { return kOrderBuckets; }
+size_t walk_order_scratch_words(size_t n_groups) { return kOrderBuckets + n_groups / kOrderTile + 1; }
 size_t walk_resident_warps() {
     // producer warps (one spill stack each) of the largest grid walk_launch_t can use
     return size_t(kNumSMs) * kMaxBlocksPerSM * kPairs;
@@ -1337,9 +1405,18 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
         const unsigned ob = std::max(1u, std::min<unsigned>(ceil_div(ceil_div(n_sinks_cap, gs), 256), kNumSMs * 4));
         G2_CUDA(cudaMemsetAsync(b.order_scratch, 0, kOrderBuckets * sizeof(uint32_t), s));
         G2_COUNT(1), order_hist_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.sliced, b.order_scratch);
-        G2_COUNT(1), order_scan_kernel<<<1, 1024, 0, s>>>(b.order_scratch, b.qstate);
+        static const char* hf = std::getenv("G2_ORDER_HEAVY");  // development: heavy-class fraction sweeps
+        const float heavy = hf ? float(std::atof(hf)) : kOrderHeavy;
+        G2_COUNT(1), order_scan_kernel<<<1, 1024, 0, s>>>(b.order_scratch, b.qstate, heavy);
         G2_COUNT(1), order_scatter_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.sliced, b.order_scratch,
                                                              const_cast<uint32_t*>(b.order));
+        if (heavy < 1.0f) {  // the order scan set the cut; the light class follows the heavy one
+            const unsigned tiles = unsigned(std::max<size_t>(1, ceil_div(ceil_div(n_sinks_cap, gs), kOrderTile)));
+            uint32_t* tile_count = b.order_scratch + kOrderBuckets;
+            G2_COUNT(1), order_light_count_kernel<<<tiles, kOrderTile, 0, s>>>(b.groups, b.qstate, b.sliced, tile_count);
+            G2_COUNT(1), order_light_scatter_kernel<<<tiles, kOrderTile, 0, s>>>(b.groups, b.qstate, b.sliced, tile_count,
+                                                                                 const_cast<uint32_t*>(b.order));
+        }
     }
     // the guarded flush whenever eps^2 is not a normal FP32 number (eps == 0 included): with eps^2
     // flushed to zero the self pair would otherwise meet rsqrt(0) = inf and 0 * inf = NaN.  Likewise
