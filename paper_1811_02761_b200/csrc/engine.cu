@@ -155,7 +155,7 @@ void Engine::ensure_cells(size_t cap) {
     if (cap <= cell_cap_) return;
     first_child_.reserve(cap), child_count_.reserve(cap), first_.reserve(cap), count_.reserve(cap);
     depth_.reserve(cap), nodes_.reserve(cap), nodes32_.reserve(cap), int_list_.reserve(cap);
-    int_count_.reserve(kMaxDepth + 1);
+    int_count_.reserve(kMaxDepth + 1), calc_sync_.reserve(calc_sync_words());
     split_status_.reserve(cap / 32 + 64);
     cell_cap_ = cap;
 }
@@ -420,8 +420,8 @@ void Engine::split_and_nodes(bool with_nodes) {
 }
 
 void Engine::calc_nodes() {
-    launch_calc_node(xyzm_s_.p, n_, child_count_.p, first_.p, count_.p, level_start_.p, ls_host_, leaf_of_.p, int_list_.p, int_count_.p,
-                     nodes_.p, nodes32_.p, rel_.p, s_);
+    launch_calc_node(xyzm_s_.p, n_, child_count_.p, first_.p, count_.p, level_start_.p, ls_host_, leaf_of_.p, int_list_.p,
+                     int_count_.p, calc_sync_.p, nodes_.p, nodes32_.p, rel_.p, s_);
 }
 
 void Engine::refresh(size_t n, const double* mass, const double* pos) {

@@ -182,7 +182,7 @@ private:
     WalkBuffers last_walk_{};  // the last walk's buffers (combine_slices)
     double walk_G_ = 1.0;
     DBuf<uint4> int_list_;                  // internal cells per depth (launch_tree_topology)
-    DBuf<uint32_t> int_count_;
+    DBuf<uint32_t> int_count_, calc_sync_;
     DBuf<uint32_t> level_start_, tile_counters_;
     DBuf<uint64_t> split_status_;
     DBuf<uint32_t> split_tiles_;

@@ -73,7 +73,9 @@ void launch_tree_topology(const uint32_t* first_child, const uint32_t* child_cou
 void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count, const uint32_t* first,
                       const uint32_t* count, const uint32_t* level_start,
                       const uint32_t* level_start_host, const uint32_t* leaf_of, const uint4* int_list,
-                      const uint32_t* int_count, WNode* nodes, WNode32* nodes32, float4* rel, cudaStream_t s);
+                      const uint32_t* int_count, uint32_t* sync, WNode* nodes, WNode32* nodes32, float4* rel,
+                      cudaStream_t s);
+size_t calc_sync_words();  // device scratch words of launch_calc_node's `sync`
 // leaf-relative offsets of the CURRENT positions against the existing nodes (GravityEngine::evaluate
 // walks fresh positions with the node attributes of the last build/refresh, engine.cpp:31-81)
 void launch_leaf_rel(const double4* xyzm, const uint32_t* child_count, const uint32_t* first, const uint32_t* count,

@@ -14,6 +14,9 @@ constexpr int kBlock = 256;
 #ifndef G2_CALC_LEAF_CELLS
 #define G2_CALC_LEAF_CELLS 1  // leaves in cell order (1) or warp-synchronous particle chunks (0): 4.55 vs 4.58 ms paper step
 #endif
+#ifndef G2_CALC_FUSED
+#define G2_CALC_FUSED 0  // 1: internal levels in one dependency-ordered launch (measured: 0.342 vs 0.337 ms per calc)
+#endif
 #ifndef G2_CALC_GROUP8
 #define G2_CALC_GROUP8 0  // 8 lanes per internal cell (A/B): 170 vs 146 us per calc at 2^23
 #endif
@@ -726,13 +729,14 @@ __global__ void __launch_bounds__(kBlock, G2_CALC_MINB) calc_leaf_cells_kernel(c
 
 // internal cell from its (at most 8) children in order (octree.cpp:145-162).  All children
 // are loaded up front: one memory round trip per cell instead of two dependent chains of cc.
+template <bool kL2 = false>  // kL2: children read through L2 (written by other blocks of the same launch)
 __device__ __forceinline__ WNode internal_node(const WNode* nodes, uint32_t f, uint32_t cc, uint8_t dep) {
     double qx[8], qy[8], qz[8], qm[8], qe[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j)
         if (j < int(cc)) {
             const double2* q = reinterpret_cast<const double2*>(nodes + f + j);
-            const double2 a = q[0], b = q[1], e = q[2];
+            const double2 a = kL2 ? __ldcg(q) : q[0], b = kL2 ? __ldcg(q + 1) : q[1], e = kL2 ? __ldcg(q + 2) : q[2];
             qx[j] = a.x, qy[j] = a.y, qz[j] = b.x, qm[j] = b.y, qe[j] = e.x;
         }
     WNode nd;
@@ -841,6 +845,76 @@ __global__ void __launch_bounds__(kLevelsThreads, 1) calc_levels_kernel(const ui
     for (int d = d_hi; d >= d_lo; --d) {
         internal_level(int_list, level_start[d], int_count[d], threadIdx.x >> 5, kLevelsThreads / 32, nodes, nodes32);
         __syncthreads();  // level d complete (and visible to the block) before level d - 1 reads it
+    }
+}
+
+// All internal levels in ONE launch, as a dependency-ordered work list: units are handed out by an
+// atomic ticket in stage order (stage = one wide level in chunks of kFuseCells cells, or one run of
+// narrow levels done by a single block with __syncthreads between its levels), and a unit starts once
+// every unit of the previous stage has completed.  Tickets are taken in order, so the units a waiting
+// block depends on are all held by running blocks: no co-residency assumption, no deadlock.
+constexpr int kFuseThreads = 256;
+constexpr uint32_t kFuseCells = kFuseThreads;  // one internal cell per thread
+constexpr int kMaxStages = kMaxDepth + 1;
+struct CalcStages {
+    int n;                                   // stages, deepest first
+    int8_t hi[kMaxStages], lo[kMaxStages];   // depth range of each stage
+    int8_t narrow[kMaxStages];               // 1: one unit, one block
+};
+__global__ void __launch_bounds__(kFuseThreads, 2) calc_internal_fused_kernel(const uint4* __restrict__ int_list,
+                                                                              const uint32_t* __restrict__ int_count,
+                                                                              const uint32_t* __restrict__ level_start,
+                                                                              WNode* nodes, WNode32* __restrict__ nodes32,
+                                                                              CalcStages st, uint32_t* sync) {
+    __shared__ uint32_t stage_end[kMaxStages];
+    __shared__ uint32_t unit_s;
+    __shared__ int ready;  // the last stage this block has seen complete
+    if (threadIdx.x == 0) {
+        uint32_t e = 0;
+        for (int k = 0; k < st.n; ++k) {
+            e += st.narrow[k] ? 1u : max(1u, (int_count[st.hi[k]] + kFuseCells - 1) / kFuseCells);
+            stage_end[k] = e;
+        }
+        ready = -1;
+    }
+    __syncthreads();
+    const uint32_t total = st.n ? stage_end[st.n - 1] : 0u;
+    uint32_t* ticket = sync;
+    uint32_t* done = sync + 1;
+    while (true) {
+        if (threadIdx.x == 0) unit_s = atomicAdd(ticket, 1u);
+        __syncthreads();
+        const uint32_t u = unit_s;
+        if (u >= total) return;
+        int k = 0;
+        while (u >= stage_end[k]) ++k;
+        if (threadIdx.x == 0 && k > 0 && ready < k - 1) {
+            const uint32_t need = stage_end[k - 1] - (k >= 2 ? stage_end[k - 2] : 0u);
+            uint32_t v;
+            while (true) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(done + k - 1) : "memory");
+                if (v >= need) break;
+                __nanosleep(32);
+            }
+            ready = k - 1;
+        }
+        __syncthreads();  // the previous stage's records are complete (read through L2); unit_s is free
+        // one wide level's chunk, or every level of a narrow run (one call site of internal_node)
+        const bool narrow = st.narrow[k];
+        const uint32_t c0 = narrow ? 0u : (u - (k ? stage_end[k - 1] : 0u)) * kFuseCells;
+        for (int d = st.hi[k]; d >= st.lo[k]; --d) {
+            const uint32_t b = level_start[d], cnt = int_count[d];
+            const uint32_t c1 = narrow ? cnt : min(cnt, c0 + kFuseCells);
+            for (uint32_t i = c0 + threadIdx.x; i < c1; i += kFuseThreads) {
+                const uint4 E = int_list[b + i];
+                store_node(nodes, nodes32, E.x, internal_node<true>(nodes, E.y, E.z, uint8_t(E.w)));
+            }
+            __syncthreads();  // level d complete (and visible to the block) before level d - 1
+        }
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(&done[k], 1u);
+        }
     }
 }
 
@@ -1020,7 +1094,8 @@ void launch_tree_topology(const uint32_t* first_child, const uint32_t* child_cou
 void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count, const uint32_t* first,
                       const uint32_t* count, const uint32_t* level_start,
                       const uint32_t* level_start_host, const uint32_t* leaf_of, const uint4* int_list,
-                      const uint32_t* int_count, WNode* nodes, WNode32* nodes32, float4* rel, cudaStream_t s) {
+                      const uint32_t* int_count, uint32_t* sync, WNode* nodes, WNode32* nodes32, float4* rel,
+                      cudaStream_t s) {
 #if G2_CALC_LEAF_CELLS
     G2_COUNT(1), calc_leaf_cells_kernel<<<grid_for(level_start_host[kMaxDepth + 1]), kBlock, 0, s>>>(
         xyzm, child_count, first, count, level_start, nodes, nodes32, rel);
@@ -1035,6 +1110,30 @@ void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count
     auto bound = [&](int d) {
         return std::min(level_start_host[d + 1] - level_start_host[d], level_start_host[d + 2] - level_start_host[d + 1]);
     };
+#if G2_CALC_FUSED
+    CalcStages st{};
+    for (int d = deepest; d >= 0;) {
+        const bool narrow = bound(d) <= kNarrowCells;
+        int lo = d;
+        if (narrow)
+            while (lo > 0 && bound(lo - 1) <= kNarrowCells) --lo;
+        st.hi[st.n] = int8_t(d), st.lo[st.n] = int8_t(lo), st.narrow[st.n] = narrow ? 1 : 0;
+        ++st.n;
+        d = lo - 1;
+    }
+    if (st.n) {
+        static int per_sm = 0;
+        if (!per_sm) {
+            G2_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, calc_internal_fused_kernel, kFuseThreads, 0));
+            per_sm = std::max(1, per_sm);
+        }
+        G2_CUDA(cudaMemsetAsync(sync, 0, (kMaxStages + 1) * sizeof(uint32_t), s));
+        G2_COUNT(1), calc_internal_fused_kernel<<<unsigned(per_sm * kNumSMs), kFuseThreads, 0, s>>>(
+            int_list, int_count, level_start, nodes, nodes32, st, sync);
+    }
+    G2_CUDA(cudaGetLastError());
+    return;
+#endif
     for (int d = deepest; d >= 0;) {
         if (bound(d) <= kNarrowCells) {  // a run of narrow levels: one block
             int lo = d;
@@ -1082,5 +1181,7 @@ void launch_pack_identity(const double* pos3, const double* mass, double4* xyzm,
     G2_COUNT(1), pack_kernel<<<grid_for(n), kBlock, 0, s>>>(pos3, mass, nullptr, xyzm, n);
 }
 void launch_iota(uint32_t* out, size_t n, cudaStream_t s) { G2_COUNT(1), iota_kernel<<<grid_for(n), kBlock, 0, s>>>(out, n); }
+
+size_t calc_sync_words() { return kMaxStages + 1; }
 
 }  // namespace g2
