@@ -176,6 +176,14 @@ int g2_sim_sort_stats(g2_sim* s, unsigned long long* bucket_sorts, unsigned long
 /* extension (diagnostics): the last step walk's whole-system groups cut into slices (one per root
  * child) and the number of slices over all ranks; synchronises the simulation's stream */
 int g2_sim_walk_slices(g2_sim* s, unsigned* heavy_groups, unsigned* slices);
+/* mesh arithmetic (host code, callable without a GPU): the contiguous equal shard [lo, hi)
+ * of n_groups for a rank (copy / NCCL meshes), the fixed per-rank window of accumulator slots those
+ * meshes gather, and the rank that walks slice `slice` of the whole-system groups (root children
+ * masses root_child_mass[n_children], n_heavy sliced groups) */
+void g2_mesh_shard(unsigned n_groups, int rank, int world, unsigned* lo, unsigned* hi);
+size_t g2_mesh_window(size_t n, size_t group_size, int world);
+unsigned g2_slice_owner(const float* root_child_mass, unsigned n_children, unsigned slice, unsigned n_heavy,
+                        int world);
 /* extension: the rebuild tuner's clock (RebuildTuner::record_walk/record_build, rebuild_tuner.hpp:18-31).
  * flop_rate <= 0: CUDA-event phase times (default).  flop_rate > 0: a deterministic model -- walk
  * seconds = (27 interactions + 5 MAC evaluations) / flop_rate (op_counters.hpp:50-63), build seconds =

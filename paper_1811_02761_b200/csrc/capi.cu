@@ -106,8 +106,9 @@ __global__ void unpack_kernel(const float4* __restrict__ gathered, float4* __res
     const uint32_t na = *n_active;
     const uint32_t ng = (na + gs - 1) / gs;
     for (uint32_t r = 0; r < world; ++r) {
-        const uint32_t lo = uint32_t(uint64_t(ng) * r / world) * gs;
-        const uint32_t hi = min(uint32_t(uint64_t(ng) * (r + 1) / world) * gs, na);
+        uint32_t lo, hi;
+        g2::equal_shard(ng, int(r), int(world), lo, hi);
+        lo *= gs, hi = min(hi * gs, na);
         for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; lo + j < hi; j += gridDim.x * blockDim.x)
             accum[lo + j] = gathered[size_t(r) * per_rank + j];
     }
@@ -121,10 +122,7 @@ __global__ void unpack_kernel(const float4* __restrict__ gathered, float4* __res
 struct ShardExchange : g2::Exchange {
     int world = 1;
     g2::DBuf<float4> gathered;
-    static size_t window(const g2::Simulation& sim, int world) {
-        const size_t gs = sim.group_size(), ng_max = (sim.n() + gs - 1) / gs;
-        return ((ng_max + world - 1) / world) * gs;
-    }
+    static size_t window(const g2::Simulation& sim, int world) { return g2::shard_window(sim.n(), sim.group_size(), world); }
     g2::DBuf<float4> gathered_slices;  // [world][walk_slice_slots()] every rank's slice region
     void prepare(g2::Simulation& sim) {  // before the first step: the accumulator must not move later
         sim.engine().reserve_accum(std::max(2 * sim.n() + 64 * sim.group_size(),
@@ -700,6 +698,19 @@ int g2_sim_sort_stats(g2_sim* s, unsigned long long* bucket_sorts, unsigned long
         *bucket_sorts = s->s->engine().bucket_sorts();
         *radix_fallbacks = s->s->engine().bucket_fallbacks();
     });
+}
+
+void g2_mesh_shard(unsigned n_groups, int rank, int world, unsigned* lo, unsigned* hi) {
+    uint32_t a = 0, b = 0;
+    if (world >= 1 && rank >= 0 && rank < world) g2::equal_shard(n_groups, rank, world, a, b);
+    *lo = a, *hi = b;
+}
+size_t g2_mesh_window(size_t n, size_t group_size, int world) {
+    return world >= 1 && group_size >= 1 ? g2::shard_window(n, group_size, world) : 0;
+}
+unsigned g2_slice_owner(const float* root_child_mass, unsigned n_children, unsigned slice, unsigned n_heavy,
+                        int world) {
+    return g2::slice_owner_of(root_child_mass, n_children, slice, n_heavy, unsigned(std::max(1, world)));
 }
 
 int g2_sim_walk_slices(g2_sim* s, unsigned* heavy_groups, unsigned* slices) {

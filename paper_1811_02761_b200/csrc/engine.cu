@@ -885,8 +885,7 @@ StepResultH Simulation::step() {
         }
         const uint32_t gs = uint32_t(eng_.config().group_size);
         const uint32_t ng = (na + gs - 1) / gs;
-        lo = uint32_t(uint64_t(ng) * rank_ / world_);
-        hi = uint32_t(uint64_t(ng) * (rank_ + 1) / world_);
+        equal_shard(ng, rank_, world_, lo, hi);
     }
     shard_lo_ = lo, shard_hi_ = hi;
     const bool sharded = exchange_ != nullptr;  // a mesh (a one-rank NCCL mesh included)

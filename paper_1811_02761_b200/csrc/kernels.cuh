@@ -161,6 +161,18 @@ struct WalkBuffers {
     int slice_world, slice_rank;        // the ranks the slices are dealt to (1, 0: all here)
 };
 size_t walk_slice_base(size_t n);      // first slice slot after n sinks
+// the rank that walks slice j (nk root children of masses w, nh sliced groups, world ranks)
+__host__ __device__ uint32_t slice_owner_of(const float* w, uint32_t nk, uint32_t j, uint32_t nh, uint32_t world);
+// contiguous equal shard [lo, hi) of ng groups for rank of world (the copy / NCCL meshes)
+__host__ __device__ inline void equal_shard(uint32_t ng, int rank, int world, uint32_t& lo, uint32_t& hi) {
+    lo = uint32_t(uint64_t(ng) * uint32_t(rank) / uint32_t(world));
+    hi = uint32_t(uint64_t(ng) * uint32_t(rank + 1) / uint32_t(world));
+}
+// the fixed per-rank window of accumulator slots every rank contributes to the copy / NCCL gather
+inline size_t shard_window(size_t n, size_t gs, int world) {
+    const size_t ng_max = (n + gs - 1) / gs;
+    return ((ng_max + size_t(world) - 1) / size_t(world)) * gs;
+}
 size_t walk_slice_slots();             // slice-region slots (kMaxHeavy x 8 slices x 32 sinks)
 size_t walk_heavy_words();
 // every heavy group's accumulators = G x the sum of its slices in slice order (slice j read from

@@ -1070,20 +1070,24 @@ __global__ void __launch_bounds__(kShardThreads) shard_kernel(const uint32_t* __
 }
 
 // the rank of slice j (group j / nk, root child k = j % nk): classes of equal expected cost (root
-// child k: cost ~ its mass) dealt heaviest class first, round-robin with alternating direction
+// child k: cost ~ its mass w[k]) dealt heaviest class first, round-robin with alternating direction
 // (snake), so every rank gets a near-equal share.  It only schedules: slice j's result and its place
-// in the group's sum do not depend on it.
-__device__ __forceinline__ uint32_t slice_owner(const TreeView& t, uint32_t j, uint32_t nh, uint32_t nk,
-                                                uint32_t world) {
-    const uint32_t h = j / nk, k = j % nk, c0 = t.nodes32[0].link;
-    const float wk = t.nodes32[c0 + k].m;
+// in the group's sum do not depend on it.  Host-callable (g2_slice_owner, tests).
+}  // namespace
+__host__ __device__ uint32_t slice_owner_of(const float* w, uint32_t nk, uint32_t j, uint32_t nh, uint32_t world) {
+    const uint32_t h = j / nk, k = j % nk;
     uint32_t cls = 0;
-    for (uint32_t q = 0; q < nk; ++q) {
-        const float wq = t.nodes32[c0 + q].m;
-        cls += wq > wk || (wq == wk && q < k);
-    }
+    for (uint32_t q = 0; q < nk; ++q) cls += w[q] > w[k] || (w[q] == w[k] && q < k);
     const uint32_t seq = cls * nh + h, r = seq % world;
     return ((seq / world) & 1u) ? world - 1u - r : r;
+}
+namespace {
+__device__ __forceinline__ uint32_t slice_owner(const TreeView& t, uint32_t j, uint32_t nh, uint32_t nk,
+                                                uint32_t world) {
+    float w[kSlicesPer];
+    const uint32_t c0 = t.nodes32[0].link;
+    for (uint32_t q = 0; q < nk; ++q) w[q] = t.nodes32[c0 + q].m;
+    return slice_owner_of(w, nk, j, nh, world);
 }
 
 // One block of kMaxHeavy threads: the queue state, and the whole-system groups' slices.  The heavy
