@@ -137,6 +137,9 @@ __global__ void __launch_bounds__(256) scatter_kernel(const double4* __restrict_
     const KeyFrame f(*cube);
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
+    // predicted bucket of storage position i: i nb / n, by a multiply (only a starting guess: the
+    // splitters check it) instead of a 64-bit division per key
+    const double pred = double(nb) / double(n);
     __syncthreads();
     // warp-uniform loop over kScatterRows x 32 consecutive storage positions
     constexpr uint32_t kSpan = 32u * kScatterRows;
@@ -152,13 +155,15 @@ __global__ void __launch_bounds__(256) scatter_kernel(const double4* __restrict_
                 const double4 p = xyzm[i];
                 bad |= !f.inside(p);
                 key[r] = f.key(p, st);
-                b[r] = find_bucket(split, nb, key[r], uint32_t((uint64_t(i) * nb) / n));
+                b[r] = find_bucket(split, nb, key[r], min(uint32_t(double(i) * pred), nb - 1));
             }
         }
         if (bad) flags->data_error = 2;
 #pragma unroll
         for (int r = 0; r < kScatterRows; ++r) {
-            const uint32_t m = __match_any_sync(kFull, b[r]);
+            // nearly sorted input: a row of 32 consecutive positions usually shares one bucket
+            const uint32_t b0 = __shfl_sync(kFull, b[r], 0);
+            const uint32_t m = __all_sync(kFull, b[r] == b0) ? kFull : __match_any_sync(kFull, b[r]);
             const int leader = __ffs(m) - 1;
             slot[r] = 0;
             if (lane == leader && b[r] != ~0u) slot[r] = atomicAdd(&cursor[b[r]], uint32_t(__popc(m)));
