@@ -126,7 +126,10 @@ __device__ __forceinline__ uint32_t find_bucket(const uint64_t* __restrict__ spl
     return lo ? lo - 1 : 0;
 }
 
-constexpr int kScatterRows = 4;  // rows of 32 consecutive positions per warp and step: independent chains
+#ifndef G2_SCATTER_ROWS
+#define G2_SCATTER_ROWS 4
+#endif
+constexpr int kScatterRows = G2_SCATTER_ROWS;  // rows of 32 consecutive positions per warp and step: independent chains
 __global__ void __launch_bounds__(256) scatter_kernel(const double4* __restrict__ xyzm, uint32_t n,
                                                       const Cube* __restrict__ cube, uint32_t nb,
                                                       const uint64_t* __restrict__ split, uint32_t* cursor,
