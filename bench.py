@@ -303,11 +303,12 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world, tuner_c
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         rs = []
-        e0.record(stream)
-        for _ in range(args.paper_steps):
-            rs.append(sim.step())
-        e1.record(stream)
-        e1.synchronize()
+        with ClockSampler(local) as clk:  # the block steps run long after the headline region: clocks too
+            e0.record(stream)
+            for _ in range(args.paper_steps):
+                rs.append(sim.step())
+            e1.record(stream)
+            e1.synchronize()
         s_per_step = e0.elapsed_time(e1) / 1e3 / args.paper_steps
         flops = float(np.mean([g2.walk_flops(r.events) for r in rs]))
         if world > 1:
@@ -321,6 +322,7 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world, tuner_c
         out[label] = {"steps": args.paper_steps, "dt_max": dt_max, "s_per_step": s_per_step,
                       "mean_active_fraction": float(np.mean([r.active for r in rs])) / args.n,
                       "rebuilds": int(sum(r.rebuilt for r in rs)), "walk_flop_per_step": flops,
+                      "clocks": clk.summary(),
                       "speedup_vs_paper_v100": PAPER_V100_S_PER_STEP / s_per_step if s_per_step > 0 else None,
                       "s_per_1e11_walk_flop": s_per_step / (flops / 1e11) if flops > 0 else None}
         del sim

@@ -176,6 +176,9 @@ int g2_sim_sort_stats(g2_sim* s, unsigned long long* bucket_sorts, unsigned long
 /* extension (diagnostics): the last step walk's whole-system groups cut into slices (one per root
  * child) and the number of slices over all ranks; synchronises the simulation's stream */
 int g2_sim_walk_slices(g2_sim* s, unsigned* heavy_groups, unsigned* slices);
+/* extension (diagnostics): task records the last step's walk used (split groups' ordered combination)
+ * and the pool's capacity; synchronises the simulation's stream */
+int g2_sim_walk_records(g2_sim* s, unsigned* used, size_t* capacity);
 /* mesh arithmetic (host code, callable without a GPU): the contiguous equal shard [lo, hi)
  * of n_groups for a rank (copy / NCCL meshes), the fixed per-rank window of accumulator slots those
  * meshes gather, and the rank that walks slice `slice` of the whole-system groups (root children

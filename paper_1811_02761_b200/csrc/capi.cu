@@ -713,6 +713,15 @@ unsigned g2_slice_owner(const float* root_child_mass, unsigned n_children, unsig
     return g2::slice_owner_of(root_child_mass, n_children, slice, n_heavy, unsigned(std::max(1, world)));
 }
 
+int g2_sim_walk_records(g2_sim* s, unsigned* used, size_t* capacity) {
+    return guarded([&] {
+        uint32_t q[16];
+        s->s->engine().read_qstate(q);
+        *used = q[6];
+        *capacity = s->s->engine().task_pool_capacity();
+    });
+}
+
 int g2_sim_walk_slices(g2_sim* s, unsigned* heavy_groups, unsigned* slices) {
     return guarded([&] {
         uint32_t q[16];

@@ -108,11 +108,7 @@ Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), devic
     n_groups_.reserve(1);
     events_.reserve(3);
     qstate_.reserve(16);
-    queue_cap_ = 1u << 20;  // ring size of the walk's donated-task queue (walk.cu kRing)
-    queue_.reserve(queue_cap_);
-    batch_.reserve(size_t(queue_cap_) * 32);
-    batch_rec_.reserve(queue_cap_);
-    G2_CUDA(cudaMemsetAsync(queue_.p, 0xff, size_t(queue_cap_) * sizeof(uint64_t), s_));
+    ensure_queue(size_t(1) << 20);
     spill_.reserve(walk_resident_warps() * walk_spill_words());
     G2_CUDA(cudaMallocHost(&hs_, sizeof(HostSync)));
     *hs_ = HostSync{};
@@ -140,7 +136,7 @@ void Engine::reserve(size_t n) {
     heavy_.reserve(walk_heavy_words()), sliced_.reserve(n);
     ensure_cells(std::max<size_t>(n + 64, 1024));
     cap_ = n;
-    ensure_task_pool(std::max<size_t>(size_t(1) << 16, n / 8));  // no allocation inside a timed walk
+    ensure_task_pool(std::max<size_t>(size_t(1) << 16, n / 4));  // no allocation inside a timed walk
     order_.reserve(n + 1), order_scratch_.reserve(walk_order_scratch_words(n));
 }
 
@@ -149,6 +145,21 @@ void Engine::ensure_task_pool(size_t want) {
     G2_CUDA(cudaStreamSynchronize(s_));
     trec_.reserve(want), tacc_.reserve(want * 32);
     rec_cap_ = want;
+    ensure_queue(want);
+}
+
+// The donated-task ring holds at least as many slots as the task pool has records: a walk's tickets
+// (one per donated task, each with its own record) then never wrap, so a donor never waits for a slot.
+void Engine::ensure_queue(size_t records) {
+    uint32_t bits = 20;
+    while (bits < 31 && (size_t(1) << bits) < records) ++bits;
+    if ((size_t(1) << bits) <= queue_cap_) return;
+    if (queue_cap_) G2_CUDA(cudaStreamSynchronize(s_));
+    queue_cap_ = uint32_t(1u << bits), ring_bits_ = bits;
+    queue_.reserve(queue_cap_);
+    batch_.reserve(size_t(queue_cap_) * 32);
+    batch_rec_.reserve(queue_cap_);
+    G2_CUDA(cudaMemsetAsync(queue_.p, 0xff, size_t(queue_cap_) * sizeof(uint64_t), s_));
 }
 
 void Engine::ensure_cells(size_t cap) {
@@ -485,6 +496,7 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     b.queue = queue_.p;
     b.batch = batch_.p;
     b.queue_cap = queue_cap_;
+    b.ring_bits = ring_bits_;
     b.qstate = qstate_.p;
     b.spill = spill_.p;
     b.group_lo = group_lo;

@@ -77,6 +77,7 @@ public:
     bool take_bucket_overflow();  // true (and clears) if the last rebuild's bucket sort overflowed (ditto)
     // rebuild sorts so far: by the bucket sort, and by its radix fallback (an overflowed bucket)
     unsigned long long bucket_sorts() const { return bucket_sorts_; }
+    size_t task_pool_capacity() const { return rec_cap_; }
     void read_qstate(uint32_t* q16) {  // the last walk's queue state (diagnostics; synchronises)
         G2_CUDA(cudaMemcpyAsync(q16, qstate_.p, 16 * sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
         G2_CUDA(cudaStreamSynchronize(s_));
@@ -151,6 +152,7 @@ public:
 private:
     void ensure_cells(size_t cap);
     void ensure_task_pool(size_t records);
+    void ensure_queue(size_t records);
     void sort_keys_identity_payload(size_t n);  // keys in keys_a_ by original id -> perm_, keys sorted
     void upload_orig(size_t n, const double* mass, const double* pos);
 
@@ -200,6 +202,7 @@ private:
     DBuf<float4> tacc_;         // [rec_cap * 32] their accumulators
     DBuf<uint32_t> batch_rec_;  // [queue_cap] record of each donated slot
     size_t rec_cap_ = 0;
+    uint32_t queue_cap_ = 0, ring_bits_ = 20;
     bool grow_pool_ = false;    // a walk ran out of task records: double the pool before the next
     uint32_t* peer_cost_[kMaxPeers] = {};
     const uint32_t* cost_prev_ = nullptr;
@@ -217,7 +220,6 @@ private:
     DBuf<uint32_t> trace_n_;
     DBuf<DevFlags> flags_;
     SortScratch sort_;
-    uint32_t queue_cap_ = 0;
 };
 
 // ---- rebuild auto-tuner: host restatement of rebuild_tuner.{hpp,cpp} ------------

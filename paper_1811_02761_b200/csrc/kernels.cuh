@@ -121,7 +121,8 @@ struct WalkBuffers {
     const uint32_t* order;    // [n_groups] initial-task order (heaviest first), written by the launcher when
                               // order_scratch is given; nullable: group index order
     uint32_t* order_scratch;  // [walk_order_scratch_words(n)] bucket counters + tile counts of the ordering
-    uint32_t queue_cap;
+    uint32_t queue_cap;       // ring slots (1 << ring_bits, >= the task pool: tickets never wrap in a walk)
+    uint32_t ring_bits;
     uint32_t* qstate;         // [16]: init claimed, donated reserved, pending, n_init, donated consumed,
                               //      shard lo, task records used, slices (all ranks), slices of this rank,
                               //      slices per heavy group, groups of the shard

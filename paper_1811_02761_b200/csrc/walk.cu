@@ -76,9 +76,7 @@ constexpr int kDonateMinLive = G2_DONATE_MIN_LIVE;  // pending cells a task need
 constexpr int kMaxBatches = G2_DONATE_BATCHES;       // donated batches (tasks) of 32 cells per donation
 constexpr uint32_t kNone = ~0u;             // no task record / no child / no parent
 constexpr uint64_t kEmpty = ~0ull;
-constexpr int kRingBits = 20;              // donated-task ring: 2^20 slots, reused
-constexpr uint32_t kRing = 1u << kRingBits;
-constexpr uint64_t kGenMask = (1ull << 26) - 1;  // generation tag of a slot (ticket >> kRingBits)
+constexpr uint64_t kGenMask = (1ull << 26) - 1;  // generation tag of a slot (ticket >> ring bits)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr uint32_t kFirst = 1, kLast = 2;  // buffer header flags: first / last buffer of a task
 // whole-system groups run as slices (one per root child), the same slices for any rank count
@@ -574,9 +572,9 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             while (true) {
                 if (owed >= 0) {
                     {  // ring slot of ticket `owed`; the generation tag tells a stale occupant apart
-                        const uint32_t sl = uint32_t(owed) & (kRing - 1);
+                        const uint32_t sl = uint32_t(owed) & (b.queue_cap - 1);
                         const uint64_t v = ld_acq64(&b.queue[sl]);
-                        if (v != kEmpty && ((v >> 6) & kGenMask) == ((uint64_t(owed) >> kRingBits) & kGenMask)) {
+                        if (v != kEmpty && ((v >> 6) & kGenMask) == ((uint64_t(owed) >> b.ring_bits) & kGenMask)) {
                             e = v;  // the slot is released after the batch has been copied
                             slot = sl;
                             owed = -1;
@@ -870,7 +868,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                         atomicAdd(q_pending, uint32_t(nb));
                         for (int j = 0; j < nb; ++j) {
                             // wait for the slot's previous occupant to be consumed (ring of 2^20)
-                            const uint32_t sl = (ds + uint32_t(j)) & (kRing - 1);
+                            const uint32_t sl = (ds + uint32_t(j)) & (b.queue_cap - 1);
                             while (ld_vol64(&b.queue[sl]) != kEmpty) __nanosleep(64);
                             b.batch_rec[sl] = child0 + uint32_t(j);
                         }
@@ -882,7 +880,7 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                 if (ok) {
                     ndon += uint32_t(nb);
                     for (int j = 0; j < nb; ++j) {
-                        const uint32_t sl = (ds + uint32_t(j)) & (kRing - 1);
+                        const uint32_t sl = (ds + uint32_t(j)) & (b.queue_cap - 1);
                         const int i = 32 * j + lane;
                         if (i < give) b.batch[size_t(sl) * 32 + lane] = from_spill ? spill[gbase + i] : sm.stack[i];
                     }
@@ -891,8 +889,8 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
                     if (lane < nb) {
                         const uint32_t t = ds + uint32_t(lane);
                         const uint32_t k = uint32_t(min(32, give - 32 * lane));
-                        st_rel64(&b.queue[t & (kRing - 1)],
-                                 (uint64_t(grp) << 32) | ((uint64_t(t >> kRingBits) & kGenMask) << 6) | k);
+                        st_rel64(&b.queue[t & (b.queue_cap - 1)],
+                                 (uint64_t(grp) << 32) | ((uint64_t(t >> b.ring_bits) & kGenMask) << 6) | k);
                     }
                     if (from_spill) {
                         gbase += give;
