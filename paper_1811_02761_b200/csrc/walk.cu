@@ -70,6 +70,9 @@ constexpr uint32_t kSpillWords = 16384;    // global stack entries per producer
 #define G2_DONATE_MIN_LIVE 2
 #endif
 constexpr int kDonateMinLive = G2_DONATE_MIN_LIVE;  // pending cells a task needs before it donates half
+#ifndef G2_DONATE_BACKOFF
+#define G2_DONATE_BACKOFF 0  // > 0: the interval between a task's donations doubles every that many donations
+#endif
 #ifndef G2_DONATE_BATCHES
 #define G2_DONATE_BATCHES 2
 #endif
@@ -626,6 +629,9 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
         // absolute screen-error term from the FP32 rounding of node centres (|c| <= |g| + D)
         const float tolc = 5e-7f * (fabsf(gxh) + fabsf(gyh) + fabsf(gzh));
         uint32_t macs = 0, pushes = 0, tflags = kFirst, ndon = 0, maxlive = 0;  // ndon/maxlive: trace only
+#if G2_DONATE_BACKOFF
+        uint32_t dsteps = 0;  // donations by this task
+#endif
         // logical LIFO = spill[gbase, gtop) (bottom, global) ++ sm.stack[0, ssize) (top, shared)
         int ssize, gbase = 0, gtop = 0, lsize = 0;
         uint32_t last_donation = 0;  // `pushes` at the last donation
@@ -832,7 +838,13 @@ __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t
             // subtrees) every kDonateEvery rounds of a long task, or when warps wait idle
             const int live = ssize + gtop - gbase;
             if (b.trace) maxlive = max(maxlive, uint32_t(live));
+#if G2_DONATE_BACKOFF
+            // a task's k-th donation waits for D x 2^(k / backoff) entries (a function of its own progress)
+            if (live >= kDonateMinLive && pushes - last_donation >= (donate_pushes << min(dsteps / G2_DONATE_BACKOFF, 8u))) {
+                ++dsteps;
+#else
             if (live >= kDonateMinLive && pushes - last_donation >= donate_pushes) {
+#endif
                 // deterministic: the decision depends on this task's own progress only.  Half of the
                 // pending cells (from the logical bottom: shallowest = largest subtrees) leave as up to
                 // kMaxBatches batches of 32, one task (record) each, children in batch order.
