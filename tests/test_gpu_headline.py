@@ -7,7 +7,8 @@
 * config 5 (dacc sweep at 2^23): on every 512th group (16384 sinks), the reference's own error and the
   B200's error against FP64 direct summation (g2_direct_sum_targets) at the SAME N and sinks; the B200
   meets SURVEY §8c's bar, median and p99 <= max(1.05 x reference, reference + 2e-6);
-* config 4 (M31 25 x 2^20, the paper's largest V100 run): the tree equals build_tree bit for bit.
+* config 4 (M31 25 x 2^20, the paper's largest V100 run): the tree equals build_tree bit for bit;
+* potentials at config 3 on every 128th group against the reference's.
 """
 import numpy as np
 import pytest
@@ -81,6 +82,29 @@ def test_config5_dacc_sweep_same_n(g2, ref, m31_23, e):
     eg, er = g2.force_error(acc, direct), g2.force_error(acc_r, direct)
     for q in ("median", "p99"):
         assert eg[q] <= max(1.05 * er[q], er[q] + 2e-6), (q, eg, er)
+
+
+def test_config3_potentials_vs_reference(g2, ref, m31_23):
+    """Potentials (flush_list<true>, traversal.cpp:61-84, self term excluded only for |d|^2 == 0,
+    :78) at the headline N on every 128th whole group: events exact, potentials within the FP32 bar,
+    accelerations unchanged by the potential path."""
+    m, p, amag = m31_23
+    rt = ref.build_tree(m, p, with_nodes=False)
+    tg = group_targets(rt.perm, 128)
+    e = ref.engine(eps=EPS, dacc=2.0 ** -9, threads=0)
+    e.build(m, p)
+    acc_r, pot_r, ev_r = e.evaluate(m, p, amag, targets=tg, with_potential=True)
+    s = g2.ParticleSystem(m, p, acc_old_mag=amag)
+    eng = g2.GravityEngine(g2.GravParams(1.0, EPS, 2.0 ** -9))
+    eng.build(s)
+    pot = np.zeros(N23)
+    ev = eng.evaluate(s, targets=tg, pot_out=pot)
+    assert (ev.interactions, ev.mac_evals, ev.list_pushes) == (ev_r["interactions"], ev_r["mac_evals"],
+                                                               ev_r["list_pushes"])
+    rel = np.abs(pot[tg] - pot_r[tg]) / np.abs(pot_r[tg])
+    assert np.median(rel) <= MED_TOL and np.quantile(rel, 0.99) <= P99_TOL, (np.median(rel), np.quantile(rel, 0.99))
+    err = g2.force_error(s.acc[tg], acc_r[tg])
+    assert err["median"] <= MED_TOL and err["p99"] <= P99_TOL, err
 
 
 def test_config4_tree_bitexact_25x2e20(g2, ref):
