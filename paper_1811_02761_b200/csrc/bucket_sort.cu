@@ -29,8 +29,9 @@ namespace {
 constexpr uint32_t kSampleChunk = 1024;  // samples per sorting CTA
 constexpr uint32_t kOversample = 4;      // samples per bucket
 constexpr int kLsItems = 8;                        // keys per thread of a local sort
-constexpr int kLsSmall = 512, kLsBig = 1024;       // threads of the two local-sort instances
-constexpr uint32_t kSmallCap = kLsSmall * kLsItems;  // 4096
+constexpr int kLsSmall = 256, kLsMid = 512, kLsBig = 1024;  // threads of the three local-sort instances
+constexpr uint32_t kSmallCap = kLsSmall * kLsItems;  // 2048: most buckets (mean 2048)
+constexpr uint32_t kMidCap = kLsMid * kLsItems;      // 4096
 constexpr uint32_t kMaxBig = 64;                   // buckets the large instance takes per sort
 static_assert(kLsBig * kLsItems == int(kBucketCap), "the large local sort holds a full bucket region");
 constexpr unsigned kFull = 0xffffffffu;
@@ -186,14 +187,15 @@ __global__ void __launch_bounds__(256) scatter_kernel(const double4* __restrict_
 }
 
 // ---- 3. bucket offsets --------------------------------------------------------------------------
-// buckets above the small local sort's capacity go to a list for the large one (at most kMaxBig);
-// more of them, or a bucket above the large capacity, open the gate
+// buckets above the small local sort's capacity go to a list for the mid-size one, those above its
+// capacity to a list for the large one (at most kMaxBig); more of them, or a bucket above the large
+// capacity, open the gate
 __global__ void __launch_bounds__(1024) offsets_kernel(const uint32_t* __restrict__ cursor, uint32_t nb,
                                                        uint32_t* __restrict__ offset, uint32_t* __restrict__ big,
-                                                       int* gate) {
+                                                       uint32_t* __restrict__ mid, int* gate) {
     __shared__ uint32_t wsum[32];
-    __shared__ uint32_t nbig;
-    if (threadIdx.x == 0) nbig = 0;
+    __shared__ uint32_t nbig, nmid;
+    if (threadIdx.x == 0) nbig = 0, nmid = 0;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const uint32_t per = (nb + 1023) / 1024;  // <= 8
     const uint32_t j0 = threadIdx.x * per;
@@ -225,16 +227,18 @@ __global__ void __launch_bounds__(1024) offsets_kernel(const uint32_t* __restric
             const uint32_t c = cursor[j0 + q];
             offset[j0 + q] = run;
             run += c;
-            if (c > kSmallCap) {
+            if (c > kMidCap) {
                 const uint32_t k = atomicAdd(&nbig, 1u);
                 if (k < kMaxBig && c <= kBucketCap)
                     big[1 + k] = j0 + q;
                 else
                     *gate = 1;
+            } else if (c > kSmallCap) {
+                mid[1 + atomicAdd(&nmid, 1u)] = j0 + q;
             }
         }
     __syncthreads();
-    if (threadIdx.x == 0) big[0] = nbig;
+    if (threadIdx.x == 0) big[0] = nbig, mid[0] = nmid;
 }
 
 // ---- 4. local sort -------------------------------------------------------------------------------
@@ -258,13 +262,13 @@ struct LsSmem {
 };
 
 #ifndef G2_LS_MINB
-#define G2_LS_MINB 2
+#define G2_LS_MINB 4  // resident 256-thread local sorts per SM (64 registers)
 #endif
 #ifndef G2_LS_MASKS_FIRST
 #define G2_LS_MASKS_FIRST 0
 #endif
-template <int kThreads, bool kBig>
-__global__ void __launch_bounds__(kThreads, kBig ? 1 : G2_LS_MINB) local_sort_kernel(const uint64_t* __restrict__ rkeys,
+template <int kThreads, int kKind>  // kKind 0: every bucket up to its capacity; 1 / 2: the mid / big list
+__global__ void __launch_bounds__(kThreads, kKind == 2 ? 1 : (kKind == 1 ? 2 : G2_LS_MINB)) local_sort_kernel(const uint64_t* __restrict__ rkeys,
                                                                           const uint32_t* __restrict__ rvals,
                                                                           const uint32_t* __restrict__ cursor,
                                                                           const uint32_t* __restrict__ offset,
@@ -278,21 +282,21 @@ __global__ void __launch_bounds__(kThreads, kBig ? 1 : G2_LS_MINB) local_sort_ke
     LsSmem<kThreads>& S = *reinterpret_cast<LsSmem<kThreads>*>(ls_raw);
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     uint32_t bkt = blockIdx.x;
-    if (kBig) {
+    if (kKind) {
         if (*gate || blockIdx.x >= big[0]) return;
         bkt = big[1 + blockIdx.x];
     }
     const uint32_t cnt = cursor[bkt];
     if (cnt == 0) return;
     const uint32_t off = offset[bkt];
-    if (!kBig) {
+    if (!kKind) {
         if (*gate) {
             // the bucket sort failed (a bucket over capacity): the output is the identity order (the
             // caller's state stays as it is) and the host redoes the ordering with the id-order sort
             for (uint32_t q = tid; q < cnt; q += kThreads) keys_out[off + q] = 0, vals_out[off + q] = off + q;
             return;
         }
-        if (cnt > kCap) return;  // the large instance sorts it
+        if (cnt > kCap) return;  // the mid-size or large instance sorts it
     }
     const uint64_t* rk = rkeys + size_t(bkt) * kBucketCap;
     const uint32_t* rv = rvals + size_t(bkt) * kBucketCap;
@@ -494,9 +498,11 @@ bool launch_bucket_sort(const double4* xyzm, size_t n, const Cube* cube, BucketS
     sc.rkeys.reserve(size_t(nb) * kBucketCap), sc.rvals.reserve(size_t(nb) * kBucketCap);
     static bool attr = false;
     if (!attr) {
-        G2_CUDA(cudaFuncSetAttribute(local_sort_kernel<kLsSmall, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        G2_CUDA(cudaFuncSetAttribute(local_sort_kernel<kLsSmall, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(LsSmem<kLsSmall>))));
-        G2_CUDA(cudaFuncSetAttribute(local_sort_kernel<kLsBig, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        G2_CUDA(cudaFuncSetAttribute(local_sort_kernel<kLsMid, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(sizeof(LsSmem<kLsMid>))));
+        G2_CUDA(cudaFuncSetAttribute(local_sort_kernel<kLsBig, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(sizeof(LsSmem<kLsBig>))));
         G2_CUDA(cudaFuncSetAttribute(splitter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSplitSmem)));
         attr = true;
@@ -505,13 +511,14 @@ bool launch_bucket_sort(const double4* xyzm, size_t n, const Cube* cube, BucketS
     const uint32_t chunk = std::min(ns, kSampleChunk);
     sc.samples.reserve(ns);
     sc.big.reserve(kMaxBig + 1);
+    sc.mid.reserve(nb + 1);
     G2_COUNT(1), sample_sort_kernel<<<ns / chunk, chunk, 0, s>>>(xyzm, n32, cube, ns, sc.samples.p);
     G2_COUNT(1), splitter_kernel<<<ns / chunk, chunk, ns * sizeof(uint64_t), s>>>(sc.samples.p, ns, nb, sc.split.p,
                                                                                    sc.cursor.p, sc.gate.p);
     const unsigned grid = std::max(1u, std::min<unsigned>(ceil_div(n, 256), kNumSMs * 8));
     G2_COUNT(1), scatter_kernel<<<grid, 256, 0, s>>>(xyzm, n32, cube, nb, sc.split.p, sc.cursor.p, sc.rkeys.p,
                                                       sc.rvals.p, sc.gate.p, flags);
-    G2_COUNT(1), offsets_kernel<<<1, 1024, 0, s>>>(sc.cursor.p, nb, sc.offset.p, sc.big.p, sc.gate.p);
+    G2_COUNT(1), offsets_kernel<<<1, 1024, 0, s>>>(sc.cursor.p, nb, sc.offset.p, sc.big.p, sc.mid.p, sc.gate.p);
     static const bool dbg = std::getenv("G2_BUCKET_DEBUG") != nullptr;  // development: bucket sizes
     if (dbg) {
         std::vector<uint32_t> c(nb);
@@ -527,9 +534,11 @@ bool launch_bucket_sort(const double4* xyzm, size_t n, const Cube* cube, BucketS
                 std::fprintf(stderr, "  bucket %u size %u split %016llx next %016llx\n", j, c[j],
                              (unsigned long long)sp[j], (unsigned long long)(j + 1 < nb ? sp[j + 1] : ~0ull));
     }
-    G2_COUNT(1), local_sort_kernel<kLsSmall, false><<<nb, kLsSmall, sizeof(LsSmem<kLsSmall>), s>>>(
+    G2_COUNT(1), local_sort_kernel<kLsSmall, 0><<<nb, kLsSmall, sizeof(LsSmem<kLsSmall>), s>>>(
         sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.big.p, sc.gate.p, keys_out, vals_out);
-    G2_COUNT(1), local_sort_kernel<kLsBig, true><<<kMaxBig, kLsBig, sizeof(LsSmem<kLsBig>), s>>>(
+    G2_COUNT(1), local_sort_kernel<kLsMid, 1><<<nb, kLsMid, sizeof(LsSmem<kLsMid>), s>>>(
+        sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.mid.p, sc.gate.p, keys_out, vals_out);
+    G2_COUNT(1), local_sort_kernel<kLsBig, 2><<<kMaxBig, kLsBig, sizeof(LsSmem<kLsBig>), s>>>(
         sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.big.p, sc.gate.p, keys_out, vals_out);
     G2_CUDA(cudaGetLastError());
     return true;

@@ -16,7 +16,8 @@ struct BucketScratch {
     DBuf<uint64_t> split;   // [nb] sorted splitter keys
     DBuf<uint32_t> cursor;  // [nb] keys claimed per bucket
     DBuf<uint32_t> offset;  // [nb] output offset per bucket
-    DBuf<uint32_t> big;     // [1 + kMaxBig] count, then the buckets above the small local sort's capacity
+    DBuf<uint32_t> big;     // [1 + kMaxBig] count, then the buckets above the mid-size local sort's capacity
+    DBuf<uint32_t> mid;     // [1 + nb] count, then the buckets above the small local sort's capacity
     DBuf<int> gate;         // 1: some bucket overflowed (the output is the identity order)
     DBuf<uint64_t> rkeys;   // [nb * kBucketCap] bucket regions
     DBuf<uint32_t> rvals;
