@@ -127,11 +127,17 @@ __device__ __forceinline__ uint32_t find_bucket(const uint64_t* __restrict__ spl
     return lo ? lo - 1 : 0;
 }
 
+#ifndef G2_LS_CONCURRENT
+#define G2_LS_CONCURRENT 1
+#endif
+#ifndef G2_SCATTER_MINB
+#define G2_SCATTER_MINB 8  // 32 registers: 8 resident 256-thread CTAs per SM (one wave); 1.13 -> 1.07 ms makeTree
+#endif
 #ifndef G2_SCATTER_ROWS
-#define G2_SCATTER_ROWS 4
+#define G2_SCATTER_ROWS 2
 #endif
 constexpr int kScatterRows = G2_SCATTER_ROWS;  // rows of 32 consecutive positions per warp and step: independent chains
-__global__ void __launch_bounds__(256) scatter_kernel(const double4* __restrict__ xyzm, uint32_t n,
+__global__ void __launch_bounds__(256, G2_SCATTER_MINB) scatter_kernel(const double4* __restrict__ xyzm, uint32_t n,
                                                       const Cube* __restrict__ cube, uint32_t nb,
                                                       const uint64_t* __restrict__ split, uint32_t* cursor,
                                                       uint64_t* __restrict__ rkeys, uint32_t* __restrict__ rvals,
@@ -534,12 +540,32 @@ bool launch_bucket_sort(const double4* xyzm, size_t n, const Cube* cube, BucketS
                 std::fprintf(stderr, "  bucket %u size %u split %016llx next %016llx\n", j, c[j],
                              (unsigned long long)sp[j], (unsigned long long)(j + 1 < nb ? sp[j + 1] : ~0ull));
     }
+    // the instances touch disjoint buckets: the few large buckets (one SM each) and the mid-size ones
+    // run beside the bulk of small ones instead of as serial tails
+    cudaStream_t s_mid = s, s_big = s;
+    if (G2_LS_CONCURRENT) {
+        if (!sc.fork) {
+            G2_CUDA(cudaEventCreateWithFlags(&sc.fork, cudaEventDisableTiming));
+            for (int k = 0; k < 2; ++k) {
+                G2_CUDA(cudaStreamCreateWithFlags(&sc.side[k], cudaStreamNonBlocking));
+                G2_CUDA(cudaEventCreateWithFlags(&sc.join[k], cudaEventDisableTiming));
+            }
+        }
+        G2_CUDA(cudaEventRecord(sc.fork, s));
+        for (auto x : sc.side) G2_CUDA(cudaStreamWaitEvent(x, sc.fork, 0));
+        s_big = sc.side[0], s_mid = sc.side[1];
+    }
+    G2_COUNT(1), local_sort_kernel<kLsBig, 2><<<kMaxBig, kLsBig, sizeof(LsSmem<kLsBig>), s_big>>>(
+        sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.big.p, sc.gate.p, keys_out, vals_out);
+    G2_COUNT(1), local_sort_kernel<kLsMid, 1><<<nb, kLsMid, sizeof(LsSmem<kLsMid>), s_mid>>>(
+        sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.mid.p, sc.gate.p, keys_out, vals_out);
     G2_COUNT(1), local_sort_kernel<kLsSmall, 0><<<nb, kLsSmall, sizeof(LsSmem<kLsSmall>), s>>>(
         sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.big.p, sc.gate.p, keys_out, vals_out);
-    G2_COUNT(1), local_sort_kernel<kLsMid, 1><<<nb, kLsMid, sizeof(LsSmem<kLsMid>), s>>>(
-        sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.mid.p, sc.gate.p, keys_out, vals_out);
-    G2_COUNT(1), local_sort_kernel<kLsBig, 2><<<kMaxBig, kLsBig, sizeof(LsSmem<kLsBig>), s>>>(
-        sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.big.p, sc.gate.p, keys_out, vals_out);
+    if (G2_LS_CONCURRENT)
+        for (int k = 0; k < 2; ++k) {
+            G2_CUDA(cudaEventRecord(sc.join[k], sc.side[k]));
+            G2_CUDA(cudaStreamWaitEvent(s, sc.join[k], 0));
+        }
     G2_CUDA(cudaGetLastError());
     return true;
 }

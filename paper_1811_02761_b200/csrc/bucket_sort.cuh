@@ -21,6 +21,19 @@ struct BucketScratch {
     DBuf<int> gate;         // 1: some bucket overflowed (the output is the identity order)
     DBuf<uint64_t> rkeys;   // [nb * kBucketCap] bucket regions
     DBuf<uint32_t> rvals;
+    // the three local-sort instances run concurrently (forked from the caller's stream and joined)
+    cudaStream_t side[2] = {nullptr, nullptr};
+    cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+    BucketScratch() = default;
+    BucketScratch(const BucketScratch&) = delete;
+    BucketScratch& operator=(const BucketScratch&) = delete;
+    ~BucketScratch() {
+        for (auto& x : side)
+            if (x) cudaStreamDestroy(x);
+        for (auto& e : join)
+            if (e) cudaEventDestroy(e);
+        if (fork) cudaEventDestroy(fork);
+    }
 };
 
 // number of buckets for n keys (a power of two), 0 when n is outside the supported range

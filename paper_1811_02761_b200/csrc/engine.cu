@@ -63,6 +63,9 @@ struct ReorderArgs {
     uint8_t *lout, *aout;
     const uint64_t* tin;
     uint64_t* tout;
+    const uint32_t* iin;  // original ids by position
+    uint32_t* iout;
+    uint32_t* iout2;      // nullable: a second copy of the new ids (the engine's perm)
 };
 __global__ void __launch_bounds__(kB) reorder_kernel(ReorderArgs r, const uint32_t* __restrict__ src, size_t n) {
     for (size_t i = blockIdx.x * size_t(kB) + threadIdx.x; i < n; i += size_t(gridDim.x) * kB) {
@@ -73,6 +76,9 @@ __global__ void __launch_bounds__(kB) reorder_kernel(ReorderArgs r, const uint32
         r.lout[i] = r.lin[j];
         r.aout[i] = r.ain[j];
         r.tout[i] = r.tin[j];
+        const uint32_t id = r.iin[j];
+        r.iout[i] = id;
+        if (r.iout2) r.iout2[i] = id;
     }
 }
 __global__ void fill_u8_kernel(uint8_t* p, uint8_t v, size_t n) {
@@ -315,7 +321,8 @@ static void dbg_mark(int i, cudaStream_t s) {
     cudaEventRecord(dbg_ev[i], s);
 }
 
-const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur, bool cube_partials) {
+const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur, bool cube_partials,
+                                       bool defer_perm) {
     const size_t n = n_;
     dbg_mark(0, s_);
     if (cube_partials)
@@ -344,8 +351,11 @@ const uint32_t* Engine::rebuild_sorted(const uint32_t* ids, const uint32_t* rank
         uint32_t* src = alt ? vals_b_.p : vals_a_.p;
         launch_fix_ties(keys_a_.p, src, ids, n, flags_.p, s_);
         if (phase_debug()) debug_displacement(src, n, s_);
-        G2_CUDA(cudaMemcpyAsync(src_.p, src, n * 4, cudaMemcpyDeviceToDevice, s_));
-        launch_gather_u32(ids, src_.p, perm_.p, n, s_);  // perm[k] = original id at new position k
+        DBuf<uint32_t>& v = alt ? vals_b_ : vals_a_;  // the sort's output becomes src_ (no copy)
+        std::swap(src_.p, v.p);
+        std::swap(src_.cap, v.cap);
+        // perm[k] = original id at new position k (a deferring caller writes it in its state gather)
+        if (!defer_perm) launch_gather_u32(ids, src_.p, perm_.p, n, s_);
         rank_valid_ = false;
     } else {
         launch_keys(xyzm_s_.p, ids, n, cube_.p, keys_a_.p, flags_.p, s_);  // keys by original id
@@ -775,7 +785,7 @@ StepState Simulation::state() {
     return StepState{eng_.xyzm_s(), vx_.p, vy_.p, vz_.p, ax_.p, ay_.p, az_.p, amag_.p, level_.p, last_.p};
 }
 
-void Simulation::reorder(const uint32_t* src) {
+void Simulation::reorder(const uint32_t* src, uint32_t* perm_out) {
     cudaStream_t s = eng_.stream();
     const size_t n = n_;
     DBuf<double>* pairs[][2] = {{&vx_, &vx2_}, {&vy_, &vy2_}, {&vz_, &vz2_}, {&ax_, &ax2_},
@@ -784,13 +794,14 @@ void Simulation::reorder(const uint32_t* src) {
     r.xin = eng_.xyzm_s(), r.xout = eng_.xyzm_alt();
     for (int k = 0; k < 7; ++k) r.in[k] = pairs[k][0]->p, r.out[k] = pairs[k][1]->p;
     r.lin = level_.p, r.lout = level2_.p, r.ain = active_.p, r.aout = active2_.p, r.tin = last_.p, r.tout = last2_.p;
+    r.iin = ids_.p, r.iout = ids2_.p, r.iout2 = perm_out;  // ids[src[k]] == the engine's perm[k]
     G2_COUNT(1), reorder_kernel<<<gridn(n), kB, 0, s>>>(r, src, n);  // one pass over the index for all state
     for (auto& pr : pairs) std::swap(pr[0]->p, pr[1]->p);
     eng_.swap_xyzm();
     std::swap(level_.p, level2_.p);
     std::swap(active_.p, active2_.p);
     std::swap(last_.p, last2_.p);
-    G2_CUDA(cudaMemcpyAsync(ids_.p, eng_.perm(), n * 4, cudaMemcpyDeviceToDevice, s));
+    std::swap(ids_.p, ids2_.p);
     rank_cur_valid_ = false;  // original id -> position: rebuilt on demand (API boundary only)
 }
 
@@ -803,8 +814,8 @@ const uint32_t* Simulation::rank_cur() {
 }
 
 void Simulation::rebuild_order(bool cube_partials) {
-    const uint32_t* src = eng_.rebuild_sorted(ids_.p, nullptr, cube_partials);
-    reorder(src);
+    const uint32_t* src = eng_.rebuild_sorted(ids_.p, nullptr, cube_partials, true);
+    reorder(src, eng_.perm());
     eng_.split_and_nodes(false);  // syncs once to size the levels
     // a bucket over capacity (its output was the identity order: the state is unchanged) or a long
     // run of equal keys: redo the ordering with the (key, original id) sort

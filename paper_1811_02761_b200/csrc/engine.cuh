@@ -70,7 +70,9 @@ public:
     // storage-order sort + tie repair (rank_ left stale); else the (key, id) sort via key_by_id.
     // cube_partials: the bbox partials of the current positions are already in bbox_partials() (the
     // predict kernel wrote them), only the final reduction runs
-    const uint32_t* rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur, bool cube_partials = false);
+    // defer_perm: the caller writes perm (= ids gathered by the returned order) itself
+    const uint32_t* rebuild_sorted(const uint32_t* ids, const uint32_t* rank_cur, bool cube_partials = false,
+                                   bool defer_perm = false);
     double* bbox_partials() { return bbox_part_.p; }
     DevFlags* dev_flags() { return flags_.p; }
     bool take_tie_overflow();  // true (and clears) if a tie run was too long for the repair (staged by split)
@@ -326,7 +328,7 @@ public:
 
 private:
     StepState state();
-    void reorder(const uint32_t* src);
+    void reorder(const uint32_t* src, uint32_t* perm_out = nullptr);
     void rebuild_order(bool cube_partials = false);          // new Morton order + topology of the resident state
     const uint32_t* rank_cur();    // original id -> current position (computed on demand)
     double elapsed(cudaEvent_t a, cudaEvent_t b);
