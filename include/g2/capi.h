@@ -169,6 +169,9 @@ int g2_sim_create_from_snapshot(const char* path, double dacc, const g2_step_sch
 int g2_sim_write_snapshot(g2_sim* s, const char* path);
 /* extension: rebuild the tree every step (the all-active "full step" benchmark) */
 int g2_sim_set_rebuild_every_step(g2_sim* s, int on);
+/* extension: run calc_node's internal levels beside the next walk's compaction and group spheres
+ * (default on; off times calc_node alone) */
+int g2_sim_set_calc_overlap(g2_sim* s, int on);
 int g2_sim_tuner_interval(g2_sim* s, size_t* interval);
 /* extension (diagnostics): how the Simulation's rebuilds sorted so far -- by the bucket sort of the
  * nearly sorted storage order, and by its onesweep radix fallback (a bucket over capacity) */
@@ -179,6 +182,9 @@ int g2_sim_walk_slices(g2_sim* s, unsigned* heavy_groups, unsigned* slices);
 /* extension (diagnostics): task records the last step's walk used (split groups' ordered combination)
  * and the pool's capacity; synchronises the simulation's stream */
 int g2_sim_walk_records(g2_sim* s, unsigned* used, size_t* capacity);
+/* extension (measurement): device seconds of the last walk kernel alone (CUDA events around its launch,
+ * on its stream; the step's walk_tree phase also holds the group set-up kernels) */
+int g2_sim_walk_kernel_seconds(g2_sim* s, double* seconds);
 /* mesh arithmetic (host code, callable without a GPU): the contiguous equal shard [lo, hi)
  * of n_groups for a rank (copy / NCCL meshes), the fixed per-rank window of accumulator slots those
  * meshes gather, and the rank that walks slice `slice` of the whole-system groups (root children

@@ -679,6 +679,9 @@ int g2_sim_get_state(g2_sim* s, double* pos, double* vel, double* acc, double* a
 int g2_sim_set_state(g2_sim* s, const double* pos, const double* vel) {
     return guarded([&] { s->s->set_state(pos, vel); });
 }
+int g2_sim_set_calc_overlap(g2_sim* s, int on) {
+    return guarded([&] { s->s->set_calc_overlap(on != 0); });
+}
 int g2_sim_set_rebuild_every_step(g2_sim* s, int on) {
     return guarded([&] { s->s->set_rebuild_every_step(on != 0); });
 }
@@ -720,6 +723,10 @@ int g2_sim_walk_records(g2_sim* s, unsigned* used, size_t* capacity) {
         *used = q[6];
         *capacity = s->s->engine().task_pool_capacity();
     });
+}
+
+int g2_sim_walk_kernel_seconds(g2_sim* s, double* seconds) {
+    return guarded([&] { *seconds = s->s->engine().last_walk_kernel_seconds(); });
 }
 
 int g2_sim_walk_slices(g2_sim* s, unsigned* heavy_groups, unsigned* slices) {

@@ -121,6 +121,14 @@ Engine::Engine(GravParamsH p, EngineConfigH c, int device) : p_(p), c_(c), devic
 }
 
 Engine::~Engine() {
+    for (auto e : walk_ev_)
+        if (e) cudaEventDestroy(e);
+    if (side_) {
+        cudaStreamSynchronize(side_);
+        cudaStreamDestroy(side_);
+        cudaEventDestroy(calc_fork_);
+        cudaEventDestroy(calc_join_);
+    }
     if (s_) {
         cudaStreamSynchronize(s_);
         cudaStreamDestroy(s_);
@@ -186,7 +194,10 @@ void Engine::enqueue_events() {
     G2_CUDA(cudaMemcpyAsync(hs_->events, events_.p, sizeof hs_->events, cudaMemcpyDeviceToHost, s_));
     G2_CUDA(cudaMemcpyAsync(&hs_->recs, qstate_.p + 6, sizeof(uint32_t), cudaMemcpyDeviceToHost, s_));
 }
-void Engine::sync() { G2_CUDA(cudaStreamSynchronize(s_)); }
+void Engine::sync() {
+    join_calc();
+    G2_CUDA(cudaStreamSynchronize(s_));
+}
 
 void Engine::check_flags() {
     enqueue_flags();
@@ -440,9 +451,34 @@ void Engine::split_and_nodes(bool with_nodes) {
     if (with_nodes) calc_nodes();
 }
 
-void Engine::calc_nodes() {
+void Engine::calc_nodes(bool overlap) {
+    join_calc();
+    if (overlap && !side_) {
+        G2_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+        G2_CUDA(cudaEventCreateWithFlags(&calc_fork_, cudaEventDisableTiming));
+        G2_CUDA(cudaEventCreateWithFlags(&calc_join_, cudaEventDisableTiming));
+    }
     launch_calc_node(xyzm_s_.p, n_, child_count_.p, first_.p, count_.p, level_start_.p, ls_host_, leaf_of_.p, int_list_.p,
-                     int_count_.p, calc_sync_.p, nodes_.p, nodes32_.p, rel_.p, s_);
+                     int_count_.p, calc_sync_.p, nodes_.p, nodes32_.p, rel_.p, s_, overlap ? side_ : nullptr,
+                     calc_fork_);
+    if (overlap) {
+        G2_CUDA(cudaEventRecord(calc_join_, side_));
+        calc_join_pending_ = true;
+    }
+}
+
+double Engine::last_walk_kernel_seconds() {
+    if (!walk_ev_valid_) return 0.0;
+    G2_CUDA(cudaEventSynchronize(walk_ev_[1]));
+    float ms = 0.f;
+    G2_CUDA(cudaEventElapsedTime(&ms, walk_ev_[0], walk_ev_[1]));
+    return ms * 1e-3;
+}
+
+void Engine::join_calc() {
+    if (!calc_join_pending_) return;
+    G2_CUDA(cudaStreamWaitEvent(s_, calc_join_, 0));
+    calc_join_pending_ = false;
 }
 
 void Engine::refresh(size_t n, const double* mass, const double* pos) {
@@ -535,7 +571,8 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     b.slice_world = std::max(1, slice_world), b.slice_rank = slice_rank;
     G2_CUDA(cudaMemsetAsync(heavy_.p, 0, sizeof(uint32_t), s_));
     G2_CUDA(cudaMemsetAsync(group_inter_.p, 0, size_t(ng_cap) * 8, s_));
-    launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
+    launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);  // reads no node: may overlap calc_node's internal levels
+    join_calc();
     WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
                   c_.count_ops ? 1 : 0, 0};
     wp.mass_max = mass_max_;
@@ -552,7 +589,10 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     if (df) wp.donate_few = uint32_t(std::max(1, std::atoi(df)));
     static const char* dsc = std::getenv("G2_DONATE_SCALE");
     if (dsc) wp.donate_scale = uint32_t(std::max(1, std::atoi(dsc)));
-    launch_walk(tv, wp, b, with_pot, n_sinks_cap, gs, flags_.p, s_);
+    if (!walk_ev_[0])
+        for (auto& e : walk_ev_) G2_CUDA(cudaEventCreate(&e));
+    launch_walk(tv, wp, b, with_pot, n_sinks_cap, gs, flags_.p, s_, walk_ev_);
+    walk_ev_valid_ = true;
     if (check)
         G2_COUNT(1), frontier_check_kernel<<<gridn(size_t(ng_cap) * (kMaxDepth + 1)), kB, 0, s_>>>(
             level_count_.p, size_t(ng_cap) * (kMaxDepth + 1), uint32_t(std::min<size_t>(cap, 0xffffffffu)),
@@ -886,12 +926,12 @@ StepResultH Simulation::step() {
             tuner_.reset_cycle();
         rebuild_order(true);
         G2_CUDA(cudaEventRecord(ev_[2], s));
-        eng_.calc_nodes();
-        G2_CUDA(cudaEventRecord(ev_[3], s));
+        eng_.calc_nodes(calc_overlap_);
+        G2_CUDA(cudaEventRecord(ev_[3], eng_.calc_tail_stream()));
     } else {
         G2_CUDA(cudaEventRecord(ev_[2], s));
-        eng_.calc_nodes();
-        G2_CUDA(cudaEventRecord(ev_[3], s));
+        eng_.calc_nodes(calc_overlap_);  // internal levels beside the compaction and the group spheres
+        G2_CUDA(cudaEventRecord(ev_[3], eng_.calc_tail_stream()));
     }
     st = state();
     // active set in (new) Morton order == reference's rank-sorted targets (engine.cpp:39-41)

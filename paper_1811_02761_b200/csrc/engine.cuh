@@ -99,7 +99,12 @@ public:
     void events_host(EventsH& ev) const;
     void ensure_rank();        // rank_ = inverse of perm_ if a storage-order rebuild left it stale
     void split_and_nodes(bool with_nodes);
-    void calc_nodes();
+    // overlap: the internal levels run on a side stream, joined by the next walk (after its group
+    // spheres) or the next calc_nodes; calc_tail_stream() is where they end
+    void calc_nodes(bool overlap = false);
+    void join_calc();
+    double last_walk_kernel_seconds();  // device time of the last walk kernel (CUDA events on its stream)
+    cudaStream_t calc_tail_stream() const { return calc_join_pending_ ? side_ : s_; }
     // walk sinks (sorted positions) with acc_old_mag (sorted); results into
     // ax_s/ay_s/az_s/pot_s at the sinks' sorted positions.
     // slice_rank/slice_world: the ranks the whole-system groups' slices are dealt to; combine: form
@@ -162,6 +167,11 @@ private:
     EngineConfigH c_;
     int device_;
     cudaStream_t s_ = nullptr;
+    cudaStream_t side_ = nullptr;  // calc_node's internal levels (calc_nodes(true))
+    cudaEvent_t calc_fork_ = nullptr, calc_join_ = nullptr;
+    bool calc_join_pending_ = false;
+    cudaEvent_t walk_ev_[2] = {nullptr, nullptr};  // around the walk kernel launch
+    bool walk_ev_valid_ = false;
     size_t n_ = 0, cap_ = 0, ncells_ = 0, cell_cap_ = 0;
     HostSync* hs_ = nullptr;  // pinned
     bool has_tree_ = false;
@@ -308,6 +318,7 @@ public:
     bool initialized() const { return initialized_; }
     size_t n() const { return n_; }
     void set_rebuild_every_step(bool v) { rebuild_every_step_ = v; }
+    void set_calc_overlap(bool v) { calc_overlap_ = v; }
     // the rebuild tuner's clock: CUDA-event phase times (flop_rate <= 0, the default), or a
     // deterministic model -- walk = walk Flop (27 I + 5 M, op_counters.hpp:50-63) / flop_rate, build =
     // build_s_per_particle x n -- which makes the rebuild schedule, hence the trajectory, reproducible
@@ -339,6 +350,7 @@ private:
     RebuildTuner tuner_;
     size_t n_;
     bool initialized_ = false, autotune_ = true, rebuild_every_step_ = false;
+    bool calc_overlap_ = true;  // calc_node's internal levels beside the compaction and group spheres
     double model_rate_ = 0.0, model_build_ = 0.0;
     uint64_t now_ = 0;
     double tick_ = 0.0, time_ = 0.0;

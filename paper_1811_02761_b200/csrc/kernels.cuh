@@ -69,12 +69,13 @@ void launch_tree_topology(const uint32_t* first_child, const uint32_t* child_cou
 // calc_node over the whole tree (octree.cpp:108-162): the leaves (warps over particle chunks), then
 // the internal levels deepest first from the per-depth lists (one launch per wide level, one block
 // per run of narrow levels); also writes the compact walk records and the leaf-relative particle
-// offsets.  level_start_host: the host copy of level_start (level widths).
+// offsets.  level_start_host: the host copy of level_start (level widths).  s_internal (nullable):
+// the internal levels go to that stream, forked from s after the leaves through `fork`.
 void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count, const uint32_t* first,
                       const uint32_t* count, const uint32_t* level_start,
                       const uint32_t* level_start_host, const uint32_t* leaf_of, const uint4* int_list,
                       const uint32_t* int_count, uint32_t* sync, WNode* nodes, WNode32* nodes32, float4* rel,
-                      cudaStream_t s);
+                      cudaStream_t s, cudaStream_t s_internal = nullptr, cudaEvent_t fork = nullptr);
 size_t calc_sync_words();  // device scratch words of launch_calc_node's `sync`
 // leaf-relative offsets of the CURRENT positions against the existing nodes (GravityEngine::evaluate
 // walks fresh positions with the node attributes of the last build/refresh, engine.cpp:31-81)
@@ -185,8 +186,9 @@ size_t walk_order_scratch_words(size_t n_groups);
 size_t walk_resident_warps();
 void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffers& b, uint32_t group_size,
                    uint32_t n_sinks_cap, cudaStream_t s);
+// kernel_ev (nullable): two events recorded around the walk kernel itself
 void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
-                 uint32_t group_size, DevFlags* flags, cudaStream_t s);
+                 uint32_t group_size, DevFlags* flags, cudaStream_t s, const cudaEvent_t* kernel_ev = nullptr);
 // acc_out/pot_out in sorted order for the sinks (FP64)
 void launch_walk_finalize(const WalkBuffers& b, uint32_t n_sinks_cap, double* ax, double* ay, double* az,
                           double* pot, cudaStream_t s);

@@ -1095,7 +1095,7 @@ void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count
                       const uint32_t* count, const uint32_t* level_start,
                       const uint32_t* level_start_host, const uint32_t* leaf_of, const uint4* int_list,
                       const uint32_t* int_count, uint32_t* sync, WNode* nodes, WNode32* nodes32, float4* rel,
-                      cudaStream_t s) {
+                      cudaStream_t s, cudaStream_t s_internal, cudaEvent_t fork) {
 #if G2_CALC_LEAF_CELLS
     G2_COUNT(1), calc_leaf_cells_kernel<<<grid_for(level_start_host[kMaxDepth + 1]), kBlock, 0, s>>>(
         xyzm, child_count, first, count, level_start, nodes, nodes32, rel);
@@ -1103,6 +1103,11 @@ void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count
     G2_COUNT(1), calc_leaf_kernel<<<unsigned(std::min<size_t>(ceil_div(n, kLeafThreads), size_t(kNumSMs) * 8)),
                                     kLeafThreads, 0, s>>>(xyzm, leaf_of, count, uint32_t(n), nodes, nodes32, rel);
 #endif
+    if (s_internal) {  // the internal levels on their own stream, after the leaves
+        G2_CUDA(cudaEventRecord(fork, s));
+        G2_CUDA(cudaStreamWaitEvent(s_internal, fork, 0));
+        s = s_internal;
+    }
     int deepest = -1;  // the deepest internal level (the deepest non-empty level holds leaves only)
     for (int d = 0; d <= kMaxDepth; ++d)
         if (level_start_host[d + 1] > level_start_host[d]) deepest = d - 1;

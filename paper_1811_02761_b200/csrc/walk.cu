@@ -1016,16 +1016,24 @@ __global__ void __launch_bounds__(256) groups_kernel(TreeView t, const double* _
             b.groups[g] = GroupRec{cx, cy, cz, radius, am, first, cnt};
             b.sliced[g] = 0;
             if (b.world > 1) b.gcost[g] = 0u;
-            // whole-system group (sphere reaching a quarter of the root's extent): sliced when the
-            // root is internal; candidates beyond kMaxHeavy switch slicing off for this walk
-            const bool heavy = !(t.nodes32[0].info & kLeafBit) && (t.nodes32[0].info & 0xffu) >= 2u &&
-                               radius >= kHeavyFrac * t.nodes[0].extent;
-            if (heavy) {
-                const uint32_t h = atomicAdd(&b.heavy[0], 1u);
-                if (h < kMaxHeavy) b.heavy[1 + h] = g;
-            }
         }
     }
+}
+
+// whole-system groups (sphere reaching a quarter of the root's extent): slicing candidates when the
+// root is internal; candidates beyond kMaxHeavy switch slicing off for this walk.  Apart from
+// groups_kernel, which reads no node, so the spheres can be formed while calc_node's internal levels
+// still run (Engine::calc_nodes(true)).
+__global__ void __launch_bounds__(256) heavy_select_kernel(TreeView t, WalkBuffers b) {
+    const uint32_t ng = *b.n_groups;
+    const uint32_t info = t.nodes32[0].info;
+    if ((info & kLeafBit) || (info & 0xffu) < 2u) return;
+    const double cut = kHeavyFrac * t.nodes[0].extent;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x)
+        if (b.groups[g].radius >= cut) {
+            const uint32_t h = atomicAdd(&b.heavy[0], 1u);
+            if (h < kMaxHeavy) b.heavy[1 + h] = g;
+        }
 }
 
 // Cost-balanced contiguous shards of the groups: rank r walks groups
@@ -1400,7 +1408,7 @@ void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffe
 }
 
 void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
-                 uint32_t gs, DevFlags* flags, cudaStream_t s) {
+                 uint32_t gs, DevFlags* flags, cudaStream_t s, const cudaEvent_t* kernel_ev) {
     const unsigned zb = std::max(1u, std::min<unsigned>(ceil_div(n_sinks_cap, 256), kNumSMs * 8));
     uint32_t zlo = 0, zhi = ~0u;
     if (b.world > 1) {
@@ -1413,6 +1421,10 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
         G2_CUDA(cudaGetLastError());
     }
     G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi, b.shard, gs);
+    {
+        const unsigned hb = std::max(1u, std::min<unsigned>(ceil_div(ceil_div(n_sinks_cap, gs), 256), kNumSMs * 4));
+        G2_COUNT(1), heavy_select_kernel<<<hb, 256, 0, s>>>(t, b);
+    }
     G2_COUNT(1), walk_init_kernel<<<1, kMaxHeavy, 0, s>>>(b, t, p, b.slice_world, b.slice_rank,
                                                           b.order_scratch != nullptr);
     if (b.order_scratch) {
@@ -1438,6 +1450,7 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
     const bool eps0 = !(float(p.eps * p.eps) >= FLT_MIN) ||
                       !(p.mass_max / (p.eps * p.eps * p.eps) < 1e30);
     const bool check = b.level_count != nullptr;
+    if (kernel_ev) G2_CUDA(cudaEventRecord(kernel_ev[0], s));
     if (check) {
         if (with_pot)
             eps0 ? walk_launch_t<true, true, true>(t, p, b, flags, s) : walk_launch_t<true, false, true>(t, p, b, flags, s);
@@ -1452,6 +1465,7 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
             eps0 ? walk_launch_t<false, true, false>(t, p, b, flags, s)
                  : walk_launch_t<false, false, false>(t, p, b, flags, s);
     }
+    if (kernel_ev) G2_CUDA(cudaEventRecord(kernel_ev[1], s));
     G2_CUDA(cudaGetLastError());
 }
 

@@ -406,6 +406,10 @@ class Simulation:
     def set_rebuild_every_step(self, on: bool = True):
         _chk(_lib.g2_sim_set_rebuild_every_step(self._h, C.c_int(int(on))))
 
+    def set_calc_overlap(self, on: bool = True):
+        """calc_node's internal levels beside the walk's compaction and group spheres (default on)."""
+        _chk(_lib.g2_sim_set_calc_overlap(self._h, C.c_int(int(on))))
+
     def set_tuner_model(self, flop_rate: float, build_seconds_per_particle: float = 0.0):
         """The rebuild tuner's clock: CUDA-event times (flop_rate <= 0) or the deterministic model
         walk = (27 I + 5 M) / flop_rate, build = build_seconds_per_particle x n (reproducible schedule)."""
@@ -421,6 +425,12 @@ class Simulation:
         a, b = C.c_ulonglong(), C.c_ulonglong()
         _chk(_lib.g2_sim_sort_stats(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def walk_kernel_seconds(self) -> float:
+        """Device seconds of the last step's walk kernel alone (CUDA events around its launch)."""
+        t = C.c_double()
+        _chk(_lib.g2_sim_walk_kernel_seconds(self._h, C.byref(t)))
+        return t.value
 
     def walk_slices(self) -> tuple:
         """(whole-system groups cut into slices, slices over all ranks) of the last step's walk."""
