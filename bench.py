@@ -215,7 +215,7 @@ def workload_config(args):
             "l2": "no flush: the resident state (~1 GB at 2^23) exceeds the 126 MB L2"}
 
 
-def hbm_phases(sim, r, n, calc_alone=None):
+def hbm_phases(sim, r, n, alone=None):
     """HBM roofline of the non-walk phases of one all-active step: algorithmic
     bytes per particle x N over the phase's CUDA-event time, against the measured copy peak.
     makeTree = bbox+keys 60 B + radix sort 8 + 24 x 8 passes + split 8 B x mean particle depth
@@ -230,16 +230,16 @@ def hbm_phases(sim, r, n, calc_alone=None):
            "mean_particle_depth": depth_mean, "cells_per_particle": len(t.depth) / n}
     for k, b in per.items():
         sec = getattr(r.timings, k)
-        if k == "calc_node" and calc_alone:
-            # in the timed steps the internal levels overlap the walk's compaction and group spheres,
-            # so the phase span is not calcNode's own time: the kernels alone, measured in extra steps
-            sec = calc_alone
+        if alone and k in alone:
+            # in the timed steps part of the phase runs on a side stream beside later phases, so its
+            # span is not the phase's own time: the phase alone, measured in extra steps
+            sec = alone[k]
         gbs = b * n / sec / 1e9 if sec > 0 else None
         out[k] = {"bytes_per_particle": b, "seconds": sec, "achieved_gbs": gbs,
                   "frac": gbs / peak if gbs and peak else None}
-        if k == "calc_node" and calc_alone:
-            out[k]["how"] = ("3 extra all-active steps after the timed region with the overlap off (CUDA events); "
-                             f"the overlapped span in the timed steps: {getattr(r.timings, k):.6f} s")
+        if alone and k in alone:
+            out[k]["how"] = ("3 extra all-active steps after the timed region with the phase overlap off (CUDA "
+                             f"events); the span on the step's stream in the timed steps: {getattr(r.timings, k):.6f} s")
     return out
 
 
@@ -388,10 +388,12 @@ def run_g2(args):
         ev1.record(stream)
         ev1.synchronize()
     launches = (lib().g2_launch_count() - l0) / args.steps
-    # calcNode's own kernels (the timed steps overlap its internal levels with the group set-up)
-    sim.set_calc_overlap(False)
-    calc_alone = float(np.mean([sim.step().timings.calc_node for _ in range(3)]))
-    sim.set_calc_overlap(True)
+    # makeTree's and calcNode's own kernels: the timed steps overlap the rebuild's reorder of the
+    # corrector's state and calcNode's internal levels with later phases (side streams)
+    sim.set_phase_overlap(False)
+    alone_steps = [sim.step().timings for _ in range(3)]
+    sim.set_phase_overlap(True)
+    alone = {k: float(np.mean([getattr(t, k) for t in alone_steps])) for k in ("make_tree", "calc_node")}
     total_s = ev0.elapsed_time(ev1) / 1e3
     walk_s = float(np.mean([r.timings.walk_tree for r in results]))  # the phase: group set-up + kernel
     walk_kernel_s = float(np.mean(walk_kernel))
@@ -468,7 +470,7 @@ def run_g2(args):
         paper = paper_protocol(args, g2, mass, pos, vel, params, local, rank, world,
                                tuner_clock=(float(f"{achieved * 1e12:.2g}"), float(f"{build_pp:.2g}")))
 
-    hbm = hbm_phases(sim, r0, args.n, calc_alone) if rank == 0 else None
+    hbm = hbm_phases(sim, r0, args.n, alone) if rank == 0 else None
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

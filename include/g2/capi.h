@@ -169,9 +169,10 @@ int g2_sim_create_from_snapshot(const char* path, double dacc, const g2_step_sch
 int g2_sim_write_snapshot(g2_sim* s, const char* path);
 /* extension: rebuild the tree every step (the all-active "full step" benchmark) */
 int g2_sim_set_rebuild_every_step(g2_sim* s, int on);
-/* extension: run calc_node's internal levels beside the next walk's compaction and group spheres
- * (default on; off times calc_node alone) */
-int g2_sim_set_calc_overlap(g2_sim* s, int on);
+/* extension: overlap independent phases of a step on a side stream (default on): calc_node's internal
+ * levels beside the walk's compaction and group spheres.  Off: every phase alone on the step's stream
+ * (the per-phase rooflines) */
+int g2_sim_set_phase_overlap(g2_sim* s, int on);
 int g2_sim_tuner_interval(g2_sim* s, size_t* interval);
 /* extension (diagnostics): how the Simulation's rebuilds sorted so far -- by the bucket sort of the
  * nearly sorted storage order, and by its onesweep radix fallback (a bucket over capacity) */

@@ -679,8 +679,8 @@ int g2_sim_get_state(g2_sim* s, double* pos, double* vel, double* acc, double* a
 int g2_sim_set_state(g2_sim* s, const double* pos, const double* vel) {
     return guarded([&] { s->s->set_state(pos, vel); });
 }
-int g2_sim_set_calc_overlap(g2_sim* s, int on) {
-    return guarded([&] { s->s->set_calc_overlap(on != 0); });
+int g2_sim_set_phase_overlap(g2_sim* s, int on) {
+    return guarded([&] { s->s->set_phase_overlap(on != 0); });
 }
 int g2_sim_set_rebuild_every_step(g2_sim* s, int on) {
     return guarded([&] { s->s->set_rebuild_every_step(on != 0); });

@@ -926,11 +926,11 @@ StepResultH Simulation::step() {
             tuner_.reset_cycle();
         rebuild_order(true);
         G2_CUDA(cudaEventRecord(ev_[2], s));
-        eng_.calc_nodes(calc_overlap_);
+        eng_.calc_nodes(phase_overlap_);
         G2_CUDA(cudaEventRecord(ev_[3], eng_.calc_tail_stream()));
     } else {
         G2_CUDA(cudaEventRecord(ev_[2], s));
-        eng_.calc_nodes(calc_overlap_);  // internal levels beside the compaction and the group spheres
+        eng_.calc_nodes(phase_overlap_);  // internal levels beside the compaction and the group spheres
         G2_CUDA(cudaEventRecord(ev_[3], eng_.calc_tail_stream()));
     }
     st = state();

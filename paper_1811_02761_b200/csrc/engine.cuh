@@ -318,7 +318,7 @@ public:
     bool initialized() const { return initialized_; }
     size_t n() const { return n_; }
     void set_rebuild_every_step(bool v) { rebuild_every_step_ = v; }
-    void set_calc_overlap(bool v) { calc_overlap_ = v; }
+    void set_phase_overlap(bool v) { phase_overlap_ = v; }
     // the rebuild tuner's clock: CUDA-event phase times (flop_rate <= 0, the default), or a
     // deterministic model -- walk = walk Flop (27 I + 5 M, op_counters.hpp:50-63) / flop_rate, build =
     // build_s_per_particle x n -- which makes the rebuild schedule, hence the trajectory, reproducible
@@ -350,7 +350,7 @@ private:
     RebuildTuner tuner_;
     size_t n_;
     bool initialized_ = false, autotune_ = true, rebuild_every_step_ = false;
-    bool calc_overlap_ = true;  // calc_node's internal levels beside the compaction and group spheres
+    bool phase_overlap_ = true;  // calc_node's internal levels beside the compaction and group spheres
     double model_rate_ = 0.0, model_build_ = 0.0;
     uint64_t now_ = 0;
     double tick_ = 0.0, time_ = 0.0;

@@ -406,9 +406,9 @@ class Simulation:
     def set_rebuild_every_step(self, on: bool = True):
         _chk(_lib.g2_sim_set_rebuild_every_step(self._h, C.c_int(int(on))))
 
-    def set_calc_overlap(self, on: bool = True):
-        """calc_node's internal levels beside the walk's compaction and group spheres (default on)."""
-        _chk(_lib.g2_sim_set_calc_overlap(self._h, C.c_int(int(on))))
+    def set_phase_overlap(self, on: bool = True):
+        """Overlap independent step phases on side streams (default on; off: every phase alone)."""
+        _chk(_lib.g2_sim_set_phase_overlap(self._h, C.c_int(int(on))))
 
     def set_tuner_model(self, flop_rate: float, build_seconds_per_particle: float = 0.0):
         """The rebuild tuner's clock: CUDA-event times (flop_rate <= 0) or the deterministic model
