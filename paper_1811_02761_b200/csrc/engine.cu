@@ -571,7 +571,10 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     b.slice_world = std::max(1, slice_world), b.slice_rank = slice_rank;
     G2_CUDA(cudaMemsetAsync(heavy_.p, 0, sizeof(uint32_t), s_));
     G2_CUDA(cudaMemsetAsync(group_inter_.p, 0, size_t(ng_cap) * 8, s_));
-    launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);  // reads no node: may overlap calc_node's internal levels
+    // the group spheres, shards and accumulator clearing read no node: they may overlap calc_node's
+    // internal levels (calc_nodes(true)), joined before the first kernel that reads the tree
+    launch_groups(tv, amag_s, b, gs, n_sinks_cap, s_);
+    launch_walk_prep(b, n_sinks_cap, gs, s_);
     join_calc();
     WalkParams wp{p_.G, p_.eps, p_.dacc, c_.bootstrap_theta, uint32_t(std::min<size_t>(cap, 0xffffffffu)),
                   c_.count_ops ? 1 : 0, 0};
@@ -591,7 +594,7 @@ EventsH Engine::walk(const uint32_t* sinks, const uint32_t* n_sinks_dev, uint32_
     if (dsc) wp.donate_scale = uint32_t(std::max(1, std::atoi(dsc)));
     if (!walk_ev_[0])
         for (auto& e : walk_ev_) G2_CUDA(cudaEventCreate(&e));
-    launch_walk(tv, wp, b, with_pot, n_sinks_cap, gs, flags_.p, s_, walk_ev_);
+    launch_walk(tv, wp, b, with_pot, n_sinks_cap, gs, flags_.p, s_, walk_ev_, false);
     walk_ev_valid_ = true;
     if (check)
         G2_COUNT(1), frontier_check_kernel<<<gridn(size_t(ng_cap) * (kMaxDepth + 1)), kB, 0, s_>>>(

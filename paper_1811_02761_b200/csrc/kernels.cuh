@@ -186,9 +186,12 @@ size_t walk_order_scratch_words(size_t n_groups);
 size_t walk_resident_warps();
 void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffers& b, uint32_t group_size,
                    uint32_t n_sinks_cap, cudaStream_t s);
-// kernel_ev (nullable): two events recorded around the walk kernel itself
+// kernel_ev (nullable): two events recorded around the walk kernel itself; prep = false: the caller
+// ran launch_walk_prep (the part that reads no node) already
+void launch_walk_prep(const WalkBuffers& b, uint32_t n_sinks_cap, uint32_t group_size, cudaStream_t s);
 void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
-                 uint32_t group_size, DevFlags* flags, cudaStream_t s, const cudaEvent_t* kernel_ev = nullptr);
+                 uint32_t group_size, DevFlags* flags, cudaStream_t s, const cudaEvent_t* kernel_ev = nullptr,
+                 bool prep = true);
 // acc_out/pot_out in sorted order for the sinks (FP64)
 void launch_walk_finalize(const WalkBuffers& b, uint32_t n_sinks_cap, double* ax, double* ay, double* az,
                           double* pot, cudaStream_t s);

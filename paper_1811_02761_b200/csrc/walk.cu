@@ -1280,10 +1280,21 @@ __global__ void __launch_bounds__(256) order_scatter_kernel(const GroupRec* __re
                                                             uint32_t* order) {
     const uint32_t lo = qstate[5], ng = qstate[10];  // the shard's groups (walk_init)
     const uint32_t cut = qstate[12];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < ng; i += gridDim.x * blockDim.x) {
-        if (sliced[lo + i]) continue;
-        const uint32_t bk = order_bucket(groups[lo + i].radius);
-        if (bk < cut) order[atomicAdd(&off[bk], 1u)] = i;
+    const int lane = threadIdx.x & 31;
+    // warp-aggregated claims: the radii crowd into few buckets, whose counters would serialise
+    for (uint32_t b0 = blockIdx.x * blockDim.x; b0 < ng; b0 += gridDim.x * blockDim.x) {  // warp-uniform trips
+        const uint32_t i = b0 + threadIdx.x;
+        uint32_t bk = ~0u;
+        if (i < ng && !sliced[lo + i]) {
+            bk = order_bucket(groups[lo + i].radius);
+            if (bk >= cut) bk = ~0u;
+        }
+        const uint32_t peers = __match_any_sync(kFull, bk);
+        const int leader = __ffs(peers) - 1;
+        uint32_t pos = 0;
+        if (bk != ~0u && lane == leader) pos = atomicAdd(&off[bk], uint32_t(__popc(peers)));
+        pos = __shfl_sync(kFull, pos, leader) + __popc(peers & ((1u << lane) - 1u));
+        if (bk != ~0u) order[pos] = i;
     }
 }
 
@@ -1407,8 +1418,8 @@ void launch_groups(const TreeView& t, const double* acc_old_mag, const WalkBuffe
     G2_CUDA(cudaGetLastError());
 }
 
-void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
-                 uint32_t gs, DevFlags* flags, cudaStream_t s, const cudaEvent_t* kernel_ev) {
+// the walk's set-up that reads no node (shards, accumulator clearing): may run before calc_node ends
+void launch_walk_prep(const WalkBuffers& b, uint32_t n_sinks_cap, uint32_t gs, cudaStream_t s) {
     const unsigned zb = std::max(1u, std::min<unsigned>(ceil_div(n_sinks_cap, 256), kNumSMs * 8));
     uint32_t zlo = 0, zhi = ~0u;
     if (b.world > 1) {
@@ -1421,6 +1432,11 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
         G2_CUDA(cudaGetLastError());
     }
     G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi, b.shard, gs);
+}
+
+void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
+                 uint32_t gs, DevFlags* flags, cudaStream_t s, const cudaEvent_t* kernel_ev, bool prep) {
+    if (prep) launch_walk_prep(b, n_sinks_cap, gs, s);
     {
         const unsigned hb = std::max(1u, std::min<unsigned>(ceil_div(ceil_div(n_sinks_cap, gs), 256), kNumSMs * 4));
         G2_COUNT(1), heavy_select_kernel<<<hb, 256, 0, s>>>(t, b);
