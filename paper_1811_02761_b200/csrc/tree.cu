@@ -324,9 +324,12 @@ __device__ __forceinline__ void split_chunk_counts(const int* lo, const int* hi,
     __syncthreads();
 }
 
+// per tile: the (depth, chunk) counts as bytes (<= 32 each), kept for the write pass
+constexpr int kChunkCountWords = ((kMaxDepth + 1) * kSplitChunks + 3) / 4;
 __global__ void __launch_bounds__(kSplitThreads) split_count_kernel(const uint64_t* __restrict__ keys, uint32_t n,
                                                                     uint32_t lc, uint32_t* __restrict__ tile_counts,
-                                                                    uint32_t ntiles, uint16_t* __restrict__ lohi) {
+                                                                    uint32_t ntiles, uint16_t* __restrict__ lohi,
+                                                                    uint32_t* __restrict__ chunk_counts) {
     __shared__ SplitWindow w;
     __shared__ uint32_t wcnt[kMaxDepth + 1][kSplitChunks];
     const uint32_t base = blockIdx.x * kSplitTile;
@@ -343,6 +346,11 @@ __global__ void __launch_bounds__(kSplitThreads) split_count_kernel(const uint64
         uint32_t c = 0;
         for (int q = 0; q < kSplitChunks; ++q) c += wcnt[threadIdx.x][q];
         tile_counts[size_t(threadIdx.x) * ntiles + blockIdx.x] = c;
+    }
+    static_assert(kSplitChunks % 4 == 0, "4 chunk counts per word");
+    for (int t = threadIdx.x; t < kChunkCountWords; t += kSplitThreads) {
+        const uint32_t* w = &wcnt[0][0] + 4 * t;
+        chunk_counts[size_t(blockIdx.x) * kChunkCountWords + t] = w[0] | (w[1] << 8) | (w[2] << 16) | (w[3] << 24);
     }
 }
 
@@ -390,7 +398,8 @@ __global__ void __launch_bounds__(1024) split_scan_kernel(uint32_t* __restrict__
 __global__ void __launch_bounds__(kSplitThreads) split_write_kernel(SplitArgs a, uint32_t n,
                                                                     const uint32_t* __restrict__ tile_offs,
                                                                     uint32_t ntiles, const uint32_t* __restrict__ totals,
-                                                                    const uint16_t* __restrict__ lohi) {
+                                                                    const uint16_t* __restrict__ lohi,
+                                                                    const uint32_t* __restrict__ chunk_counts) {
     __shared__ uint32_t wcnt[kMaxDepth + 1][kSplitChunks];
     __shared__ uint32_t lstart[kMaxDepth + 2];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -407,7 +416,12 @@ __global__ void __launch_bounds__(kSplitThreads) split_write_kernel(SplitArgs a,
         const uint32_t v = i < n ? lohi[i] : uint32_t(kMaxDepth + 1) | (uint32_t(kMaxDepth) << 8);
         lo[k] = int(v & 0xffu), hi[k] = int(v >> 8);
     }
-    split_chunk_counts(lo, hi, wcnt);
+    for (int t = threadIdx.x; t < kChunkCountWords; t += kSplitThreads) {  // the count pass's chunk counts
+        const uint32_t v = chunk_counts[size_t(blockIdx.x) * kChunkCountWords + t];
+        uint32_t* w = &wcnt[0][0] + 4 * t;
+        w[0] = v & 0xffu, w[1] = (v >> 8) & 0xffu, w[2] = (v >> 16) & 0xffu, w[3] = v >> 24;
+    }
+    __syncthreads();
     if (threadIdx.x <= kMaxDepth) {  // exclusive prefix over the tile's chunks, plus the tile offset
         uint32_t acc = lstart[threadIdx.x] + tile_offs[size_t(threadIdx.x) * ntiles + blockIdx.x];
         for (int q = 0; q < kSplitChunks; ++q) {
@@ -1040,7 +1054,10 @@ void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const
 }
 
 // per-depth tile counts + totals, then the per-particle (lo, hi) depth ranges (u16)
-size_t split_tile_words(size_t n) { return (kMaxDepth + 1) * (ceil_div(n, kSplitTile) + 1) + 32 + (n + 1) / 2 + 4; }
+size_t split_tile_words(size_t n) {
+    return (kMaxDepth + 1) * (ceil_div(n, kSplitTile) + 1) + 32 + (n + 1) / 2 + 4 +
+           size_t(kChunkCountWords) * ceil_div(n, kSplitTile);
+}
 
 bool launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
     if (a.leaf_cap <= kSplitMaxCap && a.tiles) {
@@ -1048,9 +1065,12 @@ bool launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
         const uint32_t ntiles = ceil_div(n, kSplitTile);
         uint32_t* totals = a.tiles + size_t(kMaxDepth + 1) * ntiles;
         uint16_t* lohi = reinterpret_cast<uint16_t*>(a.tiles + (kMaxDepth + 1) * (size_t(ntiles) + 1) + 32);
-        G2_COUNT(1), split_count_kernel<<<ntiles, kSplitThreads, 0, s>>>(a.keys, n, a.leaf_cap, a.tiles, ntiles, lohi);
+        uint32_t* chunk_counts = a.tiles + (kMaxDepth + 1) * (size_t(ntiles) + 1) + 32 + (size_t(n) + 1) / 2 + 4;
+        G2_COUNT(1), split_count_kernel<<<ntiles, kSplitThreads, 0, s>>>(a.keys, n, a.leaf_cap, a.tiles, ntiles, lohi,
+                                                                          chunk_counts);
         G2_COUNT(1), split_scan_kernel<<<kMaxDepth + 1, 1024, 0, s>>>(a.tiles, ntiles, totals);
-        G2_COUNT(1), split_write_kernel<<<ntiles, kSplitThreads, 0, s>>>(a, n, a.tiles, ntiles, totals, lohi);
+        G2_COUNT(1), split_write_kernel<<<ntiles, kSplitThreads, 0, s>>>(a, n, a.tiles, ntiles, totals, lohi,
+                                                                          chunk_counts);
         G2_COUNT(1), split_cells_kernel<<<grid_for(a.cell_cap), kBlock, 0, s>>>(a, n);
         G2_CUDA(cudaGetLastError());
         return a.leaf_of != nullptr;
