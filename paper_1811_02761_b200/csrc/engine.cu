@@ -1060,14 +1060,11 @@ void Simulation::set_state(const double* pos, const double* vel) {
     const size_t n = n_;
     io_.reserve(3 * n);
     io2_.reserve(3 * n);
-    if (pos) {
-        G2_CUDA(cudaMemcpyAsync(io_.p, pos, 3 * n * 8, cudaMemcpyHostToDevice, s));
-        G2_COUNT(1), set_pos_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), io_.p, ids_.p, n);
-    }
-    if (vel) {
-        G2_CUDA(cudaMemcpyAsync(io2_.p, vel, 3 * n * 8, cudaMemcpyHostToDevice, s));
-        G2_COUNT(1), deinterleave_kernel<<<gridn(n), kB, 0, s>>>(io2_.p, ids_.p, vx_.p, vy_.p, vz_.p, n);
-    }
+    // both uploads back to back (one copy direction: no kernel bubble between them), then the scatters
+    if (pos) G2_CUDA(cudaMemcpyAsync(io_.p, pos, 3 * n * 8, cudaMemcpyHostToDevice, s));
+    if (vel) G2_CUDA(cudaMemcpyAsync(io2_.p, vel, 3 * n * 8, cudaMemcpyHostToDevice, s));
+    if (pos) G2_COUNT(1), set_pos_kernel<<<gridn(n), kB, 0, s>>>(eng_.xyzm_s(), io_.p, ids_.p, n);
+    if (vel) G2_COUNT(1), deinterleave_kernel<<<gridn(n), kB, 0, s>>>(io2_.p, ids_.p, vx_.p, vy_.p, vz_.p, n);
     G2_CUDA(cudaStreamSynchronize(s));
 }
 
