@@ -233,6 +233,17 @@ def test_deterministic_accelerations():
         runs.append(sim.system())
     for k in ("acc", "pos", "vel", "level"):
         assert np.array_equal(getattr(runs[0], k), getattr(runs[1], k)), k
+    # the phase overlap (calcNode's internal levels beside the group set-up on a side stream) only
+    # schedules: the same run with every phase alone on the step's stream is bit-identical
+    sim = g2.Simulation(g2.ParticleSystem(m, p, v), params, g2.StepScheme(dt_max=1.0))
+    sim.set_phase_overlap(False)
+    sim.init()
+    sim.set_fixed_rebuild_interval(2)
+    for _ in range(6):
+        sim.step()
+    alone = sim.system()
+    for k in ("acc", "pos", "vel", "level"):
+        assert np.array_equal(getattr(runs[0], k), getattr(alone, k)), k
 
 
 def test_p2p_ipc_two_processes(tmp_path):
