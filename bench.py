@@ -317,6 +317,11 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world, tuner_c
             e1.record(stream)
             e1.synchronize()
         s_per_step = e0.elapsed_time(e1) / 1e3 / args.paper_steps
+        # the phases' own CUDA-event spans; the rest of the step span is device idle between the
+        # phases and between steps (host round trips, launch latency)
+        phase_s = float(np.mean([r.timings.total() for r in rs]))
+        phase_split = {k: float(np.mean([getattr(r.timings, k) for r in rs]))
+                       for k in ("predict", "make_tree", "calc_node", "walk_tree", "correct")}
         flops = float(np.mean([g2.walk_flops(r.events) for r in rs]))
         if world > 1:
             import torch.distributed as dist
@@ -329,7 +334,8 @@ def paper_protocol(args, g2, mass, pos, vel, params, local, rank, world, tuner_c
         out[label] = {"steps": args.paper_steps, "dt_max": dt_max, "s_per_step": s_per_step,
                       "mean_active_fraction": float(np.mean([r.active for r in rs])) / args.n,
                       "rebuilds": int(sum(r.rebuilt for r in rs)), "walk_flop_per_step": flops,
-                      "clocks": clk.summary(),
+                      "clocks": clk.summary(), "phases_s_per_step": phase_split,
+                      "outside_phases_s_per_step": s_per_step - phase_s,
                       "speedup_vs_paper_v100": PAPER_V100_S_PER_STEP / s_per_step if s_per_step > 0 else None,
                       "s_per_1e11_walk_flop": s_per_step / (flops / 1e11) if flops > 0 else None}
         del sim
