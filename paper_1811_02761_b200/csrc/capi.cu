@@ -4,6 +4,7 @@
 #include <nccl.h>
 
 #include <condition_variable>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -262,17 +263,42 @@ __global__ void peer_times_kernel(PeerTimes times, PeerFlags peers, int world, i
         asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peers.f[q] + self), "l"(epoch) : "memory");
 }
 
-__global__ void peer_wait_kernel(const uint64_t* flags, int world, uint64_t epoch) {
+// bounded: a rank that never arrives (crashed, hung, or a mismatched step count) turns into a
+// ResourceError at the end of the step instead of a GPU spinning forever
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__global__ void peer_wait_kernel(const uint64_t* flags, int world, uint64_t epoch, uint64_t timeout_ns,
+                                 g2::DevFlags* df) {
     const int q = threadIdx.x;
     if (q < world) {
-        uint64_t v;
-        do {
+        const uint64_t t0 = global_ns();
+        while (true) {
+            uint64_t v;
             asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + q) : "memory");
-            if (v < epoch) __nanosleep(200);
-        } while (v < epoch);
+            if (v >= epoch) break;
+            if (global_ns() - t0 > timeout_ns) {
+                atomicExch(&df->peer_timeout, 1);
+                break;
+            }
+            __nanosleep(200);
+        }
     }
     __syncwarp();
     __threadfence_system();
+}
+
+// the device-side exchange barrier's patience: G2_PEER_TIMEOUT_S seconds (default 120; ranks meet
+// at it once per step, so only a dead or diverged peer comes near it)
+uint64_t peer_timeout_ns() {
+    static const uint64_t ns = [] {
+        const char* e = std::getenv("G2_PEER_TIMEOUT_S");
+        const double sec = e ? std::atof(e) : 120.0;
+        return uint64_t((sec > 0.0 ? sec : 120.0) * 1e9);
+    }();
+    return ns;
 }
 
 struct PeerExchange final : g2::Exchange {
@@ -354,7 +380,8 @@ struct PeerExchange final : g2::Exchange {
         PeerFlags pf{};
         for (int q = 0; q < world; ++q) pf.f[q] = pflags[q];
         G2_COUNT(1), peer_signal_kernel<<<1, 32, 0, s>>>(pf, world, self, epoch);
-        G2_COUNT(1), peer_wait_kernel<<<1, 32, 0, s>>>(flags, world, epoch);
+        G2_COUNT(1), peer_wait_kernel<<<1, 32, 0, s>>>(flags, world, epoch, peer_timeout_ns(),
+                                                        sim.engine().dev_flags());
         G2_CUDA(cudaGetLastError());
     }
     void agree_times(g2::Simulation& sim, double& walk, double& build, bool sum_walk) override {
@@ -368,10 +395,12 @@ struct PeerExchange final : g2::Exchange {
         PeerFlags pf{};
         for (int q = 0; q < world; ++q) pt.t[q] = ptimes[q], pf.f[q] = ptflags[q];
         G2_COUNT(1), peer_times_kernel<<<1, 32, 0, s>>>(pt, pf, world, self, tepoch, walk, build);
-        G2_COUNT(1), peer_wait_kernel<<<1, 32, 0, s>>>(tflags, world, tepoch);
+        G2_COUNT(1), peer_wait_kernel<<<1, 32, 0, s>>>(tflags, world, tepoch, peer_timeout_ns(),
+                                                        sim.engine().dev_flags());
         G2_CUDA(cudaGetLastError());
         G2_CUDA(cudaMemcpyAsync(htimes, times, 2 * world * sizeof(double), cudaMemcpyDeviceToHost, s));
         G2_CUDA(cudaStreamSynchronize(s));
+        sim.engine().check_flags();  // a peer that never arrived: ResourceError now, not next step
         double w = sum_walk ? 0.0 : htimes[0], b = htimes[1];
         for (int q = 0; q < world; ++q) {
             w = sum_walk ? w + htimes[2 * q] : std::max(w, htimes[2 * q]);

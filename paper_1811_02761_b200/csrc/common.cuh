@@ -37,6 +37,7 @@ struct DevFlags {
     int queue_overflow;   // walk task queue exhausted (internal)
     int tie_run;          // a run of equal keys too long for the in-place tie repair (host re-sorts by id)
     int task_pool;        // walk task records exhausted: a donation was skipped (host grows the pool)
+    int peer_timeout;     // a peer rank did not arrive at the device-side exchange barrier in time
 };
 
 constexpr int kMaxDepth = 21;        // octree.hpp:47

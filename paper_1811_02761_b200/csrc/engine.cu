@@ -222,12 +222,15 @@ void Engine::raise_flags() {
         G2_CUDA(cudaMemsetAsync(&flags_.p->task_pool, 0, sizeof(int), s_));
     }
     const DevFlags f = hs_->flags;
-    if (f.data_error || f.resource_error || f.singularity || f.stack_overflow || f.queue_overflow) {
+    if (f.data_error || f.resource_error || f.singularity || f.stack_overflow || f.queue_overflow || f.peer_timeout) {
         G2_CUDA(cudaMemset(flags_.p, 0, sizeof(DevFlags)));
         if (f.singularity) throw Error(kSingularity, "direct_sum: coincident particles with zero softening");
         if (f.data_error == 1) throw Error(kDataError, "bounding_cube: non-finite position");
         if (f.data_error) throw Error(kDataError, "morton_key: position outside root cube");
         if (f.resource_error) throw Error(kResourceError, "walk_tree_group: frontier queue exhausted");
+        if (f.peer_timeout)
+            throw Error(kResourceError, "peer exchange: a rank did not reach the exchange barrier in time "
+                                        "(G2_PEER_TIMEOUT_S); this step's accelerations are incomplete");
         throw Error(kInternal, "walk: internal stack/queue overflow");
     }
 }

@@ -1,6 +1,7 @@
 """Worker for test_gpu_multirank.test_p2p_ipc_two_processes (launched by torch.distributed.run):
 each rank builds the same Simulation on cuda:0, exports its exchange buffers as CUDA IPC
-handles, all-gathers the handles over gloo, maps the peer's, and runs three sharded steps."""
+handles, all-gathers the handles over gloo, maps the peer's, and runs three sharded steps.
+With "stall" as the second argument only rank 0 steps (test_p2p_peer_timeout)."""
 import os
 import sys
 
@@ -22,6 +23,20 @@ handles = [None] * world
 dist.all_gather_object(handles, sim.p2p_export(rank, world))
 sim.set_mesh_p2p(rank, world, handles)
 sim.init()
+if len(sys.argv) > 2 and sys.argv[2] == "stall":
+    # rank 1 never steps: rank 0's exchange barrier must give up (G2_PEER_TIMEOUT_S) with a
+    # ResourceError instead of spinning on the GPU forever
+    if rank == 0:
+        try:
+            sim.step()
+            outcome = "no error"
+        except g2.ResourceError as e:
+            outcome = "ResourceError: " + str(e)
+        with open(os.path.join(out, "stall.txt"), "w") as f:
+            f.write(outcome)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0)
 inter = 0
 for _ in range(3):
     inter = sim.step().events.interactions

@@ -271,6 +271,19 @@ def test_p2p_ipc_two_processes(tmp_path):
         assert np.array_equal(g["acc"], a.acc) and np.array_equal(g["pos"], a.pos)
 
 
+def test_p2p_peer_timeout(tmp_path):
+    """A peer that never reaches the device-side exchange barrier (crashed, hung, diverged) makes
+    the waiting rank's step raise ResourceError after G2_PEER_TIMEOUT_S instead of hanging the GPU."""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", "--master-port=29617", os.path.join(root, "tests", "p2p_ranks.py"),
+           str(tmp_path), "stall"]
+    env = dict(os.environ, G2_PEER_TIMEOUT_S="2")
+    subprocess.run(cmd, check=True, cwd=root, env=env, timeout=600)
+    outcome = (tmp_path / "stall.txt").read_text()
+    assert outcome.startswith("ResourceError") and "exchange barrier" in outcome, outcome
+
+
 def test_bench_two_ranks_one_device(tmp_path):
     """bench.py's N > 1 path (torchrun, fused peer exchange, max over ranks) end to end, both ranks on
     cuda:0 through the bench's one-device test mode (gloo process group)."""
