@@ -843,6 +843,7 @@ __global__ void __launch_bounds__(kBlock) calc_internal_kernel(const uint4* __re
                                                                const uint32_t* __restrict__ int_count,
                                                                const uint32_t* __restrict__ level_start, WNode* nodes,
                                                                WNode32* __restrict__ nodes32, int d) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the previous level's records are complete
     internal_level(int_list, level_start[d], int_count[d], blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5),
                    gridDim.x * (kBlock / 32), nodes, nodes32);
 }
@@ -856,6 +857,7 @@ __global__ void __launch_bounds__(kLevelsThreads, 1) calc_levels_kernel(const ui
                                                                         const uint32_t* __restrict__ level_start,
                                                                         WNode* nodes, WNode32* __restrict__ nodes32,
                                                                         int d_hi, int d_lo) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the previous level's records are complete
     for (int d = d_hi; d >= d_lo; --d) {
         internal_level(int_list, level_start[d], int_count[d], threadIdx.x >> 5, kLevelsThreads / 32, nodes, nodes32);
         __syncthreads();  // level d complete (and visible to the block) before level d - 1 reads it
@@ -1159,18 +1161,34 @@ void launch_calc_node(const double4* xyzm, size_t n, const uint32_t* child_count
     G2_CUDA(cudaGetLastError());
     return;
 #endif
+    // the level chain as programmatic dependent launches: each level's grid is launched while the
+    // previous one drains and waits (griddepcontrol.wait) for its completion and memory flush, which
+    // takes the launch latency off the chain (the first launch follows the leaves normally)
+    static const bool no_pdl = std::getenv("G2_NO_PDL") != nullptr;  // development A/B
+    bool chain_first = true;
+    auto launch = [&](auto kernel, unsigned grid, unsigned block, auto... args) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid), cfg.blockDim = dim3(block), cfg.dynamicSmemBytes = 0, cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr, cfg.numAttrs = (chain_first || no_pdl) ? 0 : 1;
+        chain_first = false;
+        G2_COUNT(1);
+        G2_CUDA(cudaLaunchKernelEx(&cfg, kernel, args...));
+    };
     for (int d = deepest; d >= 0;) {
         if (bound(d) <= kNarrowCells) {  // a run of narrow levels: one block
             int lo = d;
             while (lo > 0 && bound(lo - 1) <= kNarrowCells) --lo;
-            G2_COUNT(1), calc_levels_kernel<<<1, kLevelsThreads, 0, s>>>(int_list, int_count, level_start, nodes,
-                                                                        nodes32, d, lo);
+            launch(calc_levels_kernel, 1u, unsigned(kLevelsThreads), int_list, int_count, level_start, nodes, nodes32,
+                   d, lo);
             d = lo - 1;
             continue;
         }
         const unsigned grid = unsigned(std::min<size_t>(ceil_div(size_t(bound(d)) * (G2_CALC_GROUP8 ? 8 : 1), kBlock),
                                                         size_t(kNumSMs) * 8));
-        G2_COUNT(1), calc_internal_kernel<<<grid, kBlock, 0, s>>>(int_list, int_count, level_start, nodes, nodes32, d);
+        launch(calc_internal_kernel, grid, unsigned(kBlock), int_list, int_count, level_start, nodes, nodes32, d);
         --d;
     }
     G2_CUDA(cudaGetLastError());
