@@ -51,6 +51,7 @@ constexpr uint32_t kMaxFixRun = 32;         // longest run of window-equal keys 
 __global__ void __launch_bounds__(kSampleChunk) sample_sort_kernel(const double4* __restrict__ xyzm, uint32_t n,
                                                                    const Cube* __restrict__ cube, uint32_t ns,
                                                                    uint64_t* __restrict__ samples) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     __shared__ uint64_t s[kSampleChunk];
     __shared__ SpreadTable st;
     spread_init(st);
@@ -78,6 +79,7 @@ constexpr uint32_t kSplitSmem = 128u * 1024u;
 __global__ void __launch_bounds__(kSampleChunk) splitter_kernel(const uint64_t* __restrict__ samples, uint32_t ns,
                                                                 uint32_t nb, uint64_t* __restrict__ split,
                                                                 uint32_t* __restrict__ cursor, int* gate) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     extern __shared__ uint64_t all[];
     const uint32_t chunk = blockDim.x, nchunks = ns / chunk;
     const uint32_t j = blockIdx.x * chunk + threadIdx.x;
@@ -142,6 +144,7 @@ __global__ void __launch_bounds__(256, G2_SCATTER_MINB) scatter_kernel(const dou
                                                       const uint64_t* __restrict__ split, uint32_t* cursor,
                                                       uint64_t* __restrict__ rkeys, uint32_t* __restrict__ rvals,
                                                       int* gate, DevFlags* flags) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     __shared__ SpreadTable st;
     spread_init(st);
     const KeyFrame f(*cube);
@@ -199,6 +202,7 @@ __global__ void __launch_bounds__(256, G2_SCATTER_MINB) scatter_kernel(const dou
 __global__ void __launch_bounds__(1024) offsets_kernel(const uint32_t* __restrict__ cursor, uint32_t nb,
                                                        uint32_t* __restrict__ offset, uint32_t* __restrict__ big,
                                                        uint32_t* __restrict__ mid, int* gate) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t nbig, nmid;
     if (threadIdx.x == 0) nbig = 0, nmid = 0;
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(kThreads, kKind == 2 ? 1 : (kKind == 1 ? 2 : G
                                                                           const int* gate,
                                                                           uint64_t* __restrict__ keys_out,
                                                                           uint32_t* __restrict__ vals_out) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     constexpr int kWarps = kThreads / 32;
     constexpr uint32_t kCap = uint32_t(kThreads) * kLsItems;
     extern __shared__ __align__(16) unsigned char ls_raw[];
@@ -518,13 +523,13 @@ bool launch_bucket_sort(const double4* xyzm, size_t n, const Cube* cube, BucketS
     sc.samples.reserve(ns);
     sc.big.reserve(kMaxBig + 1);
     sc.mid.reserve(nb + 1);
-    G2_COUNT(1), sample_sort_kernel<<<ns / chunk, chunk, 0, s>>>(xyzm, n32, cube, ns, sc.samples.p);
-    G2_COUNT(1), splitter_kernel<<<ns / chunk, chunk, ns * sizeof(uint64_t), s>>>(sc.samples.p, ns, nb, sc.split.p,
+    G2_COUNT(1), launch_pdl(sample_sort_kernel, dim3(ns / chunk), dim3(chunk), size_t(0), s, xyzm, n32, cube, ns, sc.samples.p);
+    G2_COUNT(1), launch_pdl(splitter_kernel, dim3(ns / chunk), dim3(chunk), size_t(ns * sizeof(uint64_t)), s, sc.samples.p, ns, nb, sc.split.p,
                                                                                    sc.cursor.p, sc.gate.p);
     const unsigned grid = std::max(1u, std::min<unsigned>(ceil_div(n, 256), kNumSMs * 8));
-    G2_COUNT(1), scatter_kernel<<<grid, 256, 0, s>>>(xyzm, n32, cube, nb, sc.split.p, sc.cursor.p, sc.rkeys.p,
+    G2_COUNT(1), launch_pdl(scatter_kernel, dim3(grid), dim3(256), size_t(0), s, xyzm, n32, cube, nb, sc.split.p, sc.cursor.p, sc.rkeys.p,
                                                       sc.rvals.p, sc.gate.p, flags);
-    G2_COUNT(1), offsets_kernel<<<1, 1024, 0, s>>>(sc.cursor.p, nb, sc.offset.p, sc.big.p, sc.mid.p, sc.gate.p);
+    G2_COUNT(1), launch_pdl(offsets_kernel, dim3(1), dim3(1024), size_t(0), s, sc.cursor.p, nb, sc.offset.p, sc.big.p, sc.mid.p, sc.gate.p);
     static const bool dbg = std::getenv("G2_BUCKET_DEBUG") != nullptr;  // development: bucket sizes
     if (dbg) {
         std::vector<uint32_t> c(nb);
@@ -559,7 +564,7 @@ bool launch_bucket_sort(const double4* xyzm, size_t n, const Cube* cube, BucketS
         sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.big.p, sc.gate.p, keys_out, vals_out);
     G2_COUNT(1), local_sort_kernel<kLsMid, 1><<<nb, kLsMid, sizeof(LsSmem<kLsMid>), s_mid>>>(
         sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.mid.p, sc.gate.p, keys_out, vals_out);
-    G2_COUNT(1), local_sort_kernel<kLsSmall, 0><<<nb, kLsSmall, sizeof(LsSmem<kLsSmall>), s>>>(
+    G2_COUNT(1), launch_pdl(local_sort_kernel<kLsSmall, 0>, dim3(nb), dim3(kLsSmall), size_t(sizeof(LsSmem<kLsSmall>)), s, 
         sc.rkeys.p, sc.rvals.p, sc.cursor.p, sc.offset.p, sc.big.p, sc.gate.p, keys_out, vals_out);
     if (G2_LS_CONCURRENT)
         for (int k = 0; k < 2; ++k) {

@@ -5,6 +5,8 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -91,6 +93,27 @@ inline std::atomic<unsigned long long>& launch_counter() {
     return c;
 }
 #define G2_COUNT(k) (::g2::launch_counter() += (k))
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may start while the previous
+// kernel of its stream drains; it must begin with G2_PDL_WAIT() (griddepcontrol.wait: the previous
+// grid complete, its writes visible) before touching memory.  Used only where the previous operation
+// in the stream is a kernel (no event wait, memset or copy in between).  G2_NO_PDL: plain launches.
+#define G2_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+inline bool pdl_enabled() {
+    static const bool on = std::getenv("G2_NO_PDL") == nullptr;
+    return on;
+}
+template <typename... K, typename... A>
+inline void launch_pdl(void (*kernel)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr, cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+    if (e != cudaSuccess) throw std::runtime_error(std::string("launch_pdl: ") + cudaGetErrorString(e));
+}
 
 inline unsigned ceil_div(size_t a, size_t b) { return static_cast<unsigned>((a + b - 1) / b); }
 

@@ -111,6 +111,7 @@ __device__ __forceinline__ void predict_one(double4& p, double& vx, double& vy, 
 __global__ void __launch_bounds__(kBlock) predict_kernel(StepState st, size_t n, const unsigned long long* t_next_p,
                                                           uint64_t now, double tick, uint8_t* __restrict__ active,
                                                           double* __restrict__ bbox, DevFlags* flags) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     const uint64_t t_next = *t_next_p;
     const double dt = dmul(double(t_next - now), tick);
     const double h = dmul(dmul(0.5, dt), dt);
@@ -194,6 +195,7 @@ __global__ void __launch_bounds__(kBlock) correct_kernel(StepState st, const uin
                                                          const float4* __restrict__ acc4,
                                                          const unsigned long long* t_next_p, uint64_t now, double tick,
                                                          SchemeDev sc) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     const uint32_t na = min(*n_sinks, cap);
     const uint64_t t_next = *t_next_p;
     for (uint32_t s = blockIdx.x * kBlock + threadIdx.x; s < na; s += gridDim.x * kBlock) {
@@ -463,7 +465,7 @@ void launch_tnext(const StepState& st, size_t n, unsigned long long* t_next, cud
 unsigned predict_blocks(size_t n) { return grid_for(n / 2 + 1); }
 void launch_predict(const StepState& st, size_t n, const unsigned long long* t_next, uint64_t now, double tick,
                     uint8_t* active_flag, cudaStream_t s, double* bbox_partials, DevFlags* flags) {
-    G2_COUNT(1), predict_kernel<<<predict_blocks(n), kBlock, 0, s>>>(st, n, t_next, now, tick, active_flag,
+    G2_COUNT(1), launch_pdl(predict_kernel, dim3(predict_blocks(n)), dim3(kBlock), size_t(0), s, st, n, t_next, now, tick, active_flag,
                                                                      bbox_partials, flags);
 }
 
@@ -479,7 +481,7 @@ void launch_compact(const uint8_t* flags, size_t n, uint32_t* out, uint32_t* n_o
 void launch_correct(const StepState& st, const uint32_t* sinks, const uint32_t* n_sinks, uint32_t n_cap,
                     const float4* acc4, const unsigned long long* t_next, uint64_t now, double tick, SchemeDev sc,
                     cudaStream_t s) {
-    G2_COUNT(1), correct_kernel<<<grid_for(n_cap), kBlock, 0, s>>>(st, sinks, n_sinks, n_cap, acc4, t_next, now, tick,
+    G2_COUNT(1), launch_pdl(correct_kernel, dim3(grid_for(n_cap)), dim3(kBlock), size_t(0), s, st, sinks, n_sinks, n_cap, acc4, t_next, now, tick,
                                                                    sc);
 }
 

@@ -357,6 +357,7 @@ __global__ void __launch_bounds__(kSplitThreads) split_count_kernel(const uint64
 // one block per depth: exclusive scan over the tiles in place, level size -> totals[d]
 __global__ void __launch_bounds__(1024) split_scan_kernel(uint32_t* __restrict__ tile_counts, uint32_t ntiles,
                                                           uint32_t* __restrict__ totals) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     __shared__ uint32_t wsum[32];
     __shared__ uint32_t carry;
     uint32_t* row = tile_counts + size_t(blockIdx.x) * ntiles;
@@ -400,6 +401,7 @@ __global__ void __launch_bounds__(kSplitThreads) split_write_kernel(SplitArgs a,
                                                                     uint32_t ntiles, const uint32_t* __restrict__ totals,
                                                                     const uint16_t* __restrict__ lohi,
                                                                     const uint32_t* __restrict__ chunk_counts) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     __shared__ uint32_t wcnt[kMaxDepth + 1][kSplitChunks];
     __shared__ uint32_t lstart[kMaxDepth + 2];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -509,6 +511,7 @@ __device__ __forceinline__ void write_topology(uint32_t c, bool valid, uint32_t 
 // per cell: count = end of its digit run (8 keys probed at once, then galloping), and for split
 // cells the number of consecutive next-level cells starting inside it; then the topology outputs
 __global__ void __launch_bounds__(kBlock) split_cells_kernel(SplitArgs a, uint32_t n) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     const uint32_t total = min(a.level_start[kMaxDepth + 1], a.cell_cap);
     const bool topo = a.leaf_of && !(a.topo_gate && *a.topo_gate);
     for (uint32_t b0 = blockIdx.x * kBlock; b0 < total; b0 += gridDim.x * kBlock) {  // warp-uniform trips
@@ -1070,10 +1073,10 @@ bool launch_split(const SplitArgs& a, uint32_t n, cudaStream_t s) {
         uint32_t* chunk_counts = a.tiles + (kMaxDepth + 1) * (size_t(ntiles) + 1) + 32 + (size_t(n) + 1) / 2 + 4;
         G2_COUNT(1), split_count_kernel<<<ntiles, kSplitThreads, 0, s>>>(a.keys, n, a.leaf_cap, a.tiles, ntiles, lohi,
                                                                           chunk_counts);
-        G2_COUNT(1), split_scan_kernel<<<kMaxDepth + 1, 1024, 0, s>>>(a.tiles, ntiles, totals);
-        G2_COUNT(1), split_write_kernel<<<ntiles, kSplitThreads, 0, s>>>(a, n, a.tiles, ntiles, totals, lohi,
+        G2_COUNT(1), launch_pdl(split_scan_kernel, dim3(kMaxDepth + 1), dim3(1024), size_t(0), s, a.tiles, ntiles, totals);
+        G2_COUNT(1), launch_pdl(split_write_kernel, dim3(ntiles), dim3(kSplitThreads), size_t(0), s, a, n, a.tiles, ntiles, totals, lohi,
                                                                           chunk_counts);
-        G2_COUNT(1), split_cells_kernel<<<grid_for(a.cell_cap), kBlock, 0, s>>>(a, n);
+        G2_COUNT(1), launch_pdl(split_cells_kernel, dim3(grid_for(a.cell_cap)), dim3(kBlock), size_t(0), s, a, n);
         G2_CUDA(cudaGetLastError());
         return a.leaf_of != nullptr;
     }

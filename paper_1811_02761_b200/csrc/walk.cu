@@ -402,6 +402,7 @@ __device__ __forceinline__ Screen screen(const TreeView& t, const GroupRec* gp, 
 
 template <bool kPot, bool kEps0, bool kCheck>
 __global__ void __launch_bounds__(kThreads, G2_WALK_MINB) walk_kernel(TreeView t, WalkParams p, WalkBuffers b, DevFlags* flags) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     PairSmem* const pairs = reinterpret_cast<PairSmem*>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1117,6 +1118,7 @@ __device__ __forceinline__ uint32_t slice_owner(const TreeView& t, uint32_t j, u
 // by the owner of the group's slice 0.  The initial-task ordering leaves the sliced groups out.
 __global__ void __launch_bounds__(kMaxHeavy) walk_init_kernel(WalkBuffers b, TreeView t, WalkParams p, int sworld,
                                                               int sself, int ordered) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     __shared__ uint32_t sorted[kMaxHeavy];
     __shared__ uint32_t wsum[kMaxHeavy / 32 + 1];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1243,6 +1245,7 @@ __global__ void __launch_bounds__(256) order_hist_kernel(const GroupRec* __restr
         if (h[i]) atomicAdd(&hist[i], h[i]);
 }
 __global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist, uint32_t* qstate, float heavy) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     __shared__ uint32_t part[1024];
     const uint32_t a = hist[2 * threadIdx.x], c = hist[2 * threadIdx.x + 1];
     part[threadIdx.x] = a + c;
@@ -1278,6 +1281,7 @@ __global__ void __launch_bounds__(1024) order_scan_kernel(uint32_t* hist, uint32
 __global__ void __launch_bounds__(256) order_scatter_kernel(const GroupRec* __restrict__ groups, const uint32_t* qstate,
                                                             const uint8_t* __restrict__ sliced, uint32_t* off,
                                                             uint32_t* order) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     const uint32_t lo = qstate[5], ng = qstate[10];  // the shard's groups (walk_init)
     const uint32_t cut = qstate[12];
     const int lane = threadIdx.x & 31;
@@ -1388,7 +1392,7 @@ void walk_launch_t(const TreeView& t, const WalkParams& p, const WalkBuffers& b,
     static const char* ov = std::getenv("G2_WALK_CTAS_PER_SM");  // development: occupancy experiments
     if (ov) per_sm = std::max(1, std::min(per_sm, std::atoi(ov)));
     const unsigned grid = unsigned(per_sm * kNumSMs);
-    G2_COUNT(1), walk_kernel<kPot, kEps0, kCheck><<<grid, kThreads, kWalkSmem, s>>>(t, p, b, flags);
+    G2_COUNT(1), launch_pdl(walk_kernel<kPot, kEps0, kCheck>, dim3(grid), dim3(kThreads), size_t(kWalkSmem), s, t, p, b, flags);
 }
 
 }  // namespace
@@ -1441,7 +1445,7 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
         const unsigned hb = std::max(1u, std::min<unsigned>(ceil_div(ceil_div(n_sinks_cap, gs), 256), kNumSMs * 4));
         G2_COUNT(1), heavy_select_kernel<<<hb, 256, 0, s>>>(t, b);
     }
-    G2_COUNT(1), walk_init_kernel<<<1, kMaxHeavy, 0, s>>>(b, t, p, b.slice_world, b.slice_rank,
+    G2_COUNT(1), launch_pdl(walk_init_kernel, dim3(1), dim3(kMaxHeavy), size_t(0), s, b, t, p, b.slice_world, b.slice_rank,
                                                           b.order_scratch != nullptr);
     if (b.order_scratch) {
         const unsigned ob = std::max(1u, std::min<unsigned>(ceil_div(ceil_div(n_sinks_cap, gs), 256), kNumSMs * 4));
@@ -1449,8 +1453,8 @@ void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, b
         G2_COUNT(1), order_hist_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.sliced, b.order_scratch);
         static const char* hf = std::getenv("G2_ORDER_HEAVY");  // development: heavy-class fraction sweeps
         const float heavy = hf ? float(std::atof(hf)) : kOrderHeavy;
-        G2_COUNT(1), order_scan_kernel<<<1, 1024, 0, s>>>(b.order_scratch, b.qstate, heavy);
-        G2_COUNT(1), order_scatter_kernel<<<ob, 256, 0, s>>>(b.groups, b.qstate, b.sliced, b.order_scratch,
+        G2_COUNT(1), launch_pdl(order_scan_kernel, dim3(1), dim3(1024), size_t(0), s, b.order_scratch, b.qstate, heavy);
+        G2_COUNT(1), launch_pdl(order_scatter_kernel, dim3(ob), dim3(256), size_t(0), s, b.groups, b.qstate, b.sliced, b.order_scratch,
                                                              const_cast<uint32_t*>(b.order));
         if (heavy < 1.0f) {  // the order scan set the cut; the light class follows the heavy one
             const unsigned tiles = unsigned(std::max<size_t>(1, ceil_div(ceil_div(n_sinks_cap, gs), kOrderTile)));
