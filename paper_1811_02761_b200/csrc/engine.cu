@@ -68,6 +68,7 @@ struct ReorderArgs {
     uint32_t* iout2;      // nullable: a second copy of the new ids (the engine's perm)
 };
 __global__ void __launch_bounds__(kB) reorder_kernel(ReorderArgs r, const uint32_t* __restrict__ src, size_t n) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     for (size_t i = blockIdx.x * size_t(kB) + threadIdx.x; i < n; i += size_t(gridDim.x) * kB) {
         const uint32_t j = src[i];
         r.xout[i] = r.xin[j];
@@ -841,7 +842,7 @@ void Simulation::reorder(const uint32_t* src, uint32_t* perm_out) {
     for (int k = 0; k < 7; ++k) r.in[k] = pairs[k][0]->p, r.out[k] = pairs[k][1]->p;
     r.lin = level_.p, r.lout = level2_.p, r.ain = active_.p, r.aout = active2_.p, r.tin = last_.p, r.tout = last2_.p;
     r.iin = ids_.p, r.iout = ids2_.p, r.iout2 = perm_out;  // ids[src[k]] == the engine's perm[k]
-    G2_COUNT(1), reorder_kernel<<<gridn(n), kB, 0, s>>>(r, src, n);  // one pass over the index for all state
+    G2_COUNT(1), launch_pdl(reorder_kernel, dim3(gridn(n)), dim3(kB), size_t(0), s, r, src, n);  // one pass over the index for all state
     for (auto& pr : pairs) std::swap(pr[0]->p, pr[1]->p);
     eng_.swap_xyzm();
     std::swap(level_.p, level2_.p);

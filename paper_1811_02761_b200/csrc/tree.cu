@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kBlock) bbox_partial_kernel(const double4* __r
 constexpr int kBboxFinalThreads = 1024;
 __global__ void __launch_bounds__(kBboxFinalThreads) bbox_final_kernel(const double* __restrict__ partials, int nb,
                                                                        Cube* cube) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     // one block: min/max are exact in any order
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
@@ -1044,12 +1045,12 @@ inline unsigned grid_for(size_t n) { return std::max(1u, std::min<unsigned>(ceil
 void launch_bbox(const double4* xyzm, size_t n, double* partials, Cube* cube, DevFlags* flags, cudaStream_t s) {
     const unsigned nb = std::max(1u, std::min<unsigned>(ceil_div(n, kBlock * 4), kNumSMs * 4));
     G2_COUNT(1), bbox_partial_kernel<<<nb, kBlock, 0, s>>>(xyzm, n, partials, flags);
-    G2_COUNT(1), bbox_final_kernel<<<1, kBboxFinalThreads, 0, s>>>(partials, int(nb), cube);
+    G2_COUNT(1), launch_pdl(bbox_final_kernel, dim3(1), dim3(kBboxFinalThreads), size_t(0), s, partials, int(nb), cube);
     G2_CUDA(cudaGetLastError());
 }
 
 void launch_bbox_final(const double* partials, unsigned nb, Cube* cube, cudaStream_t s) {
-    G2_COUNT(1), bbox_final_kernel<<<1, kBboxFinalThreads, 0, s>>>(partials, int(nb), cube);
+    G2_COUNT(1), launch_pdl(bbox_final_kernel, dim3(1), dim3(kBboxFinalThreads), size_t(0), s, partials, int(nb), cube);
 }
 
 void launch_keys(const double4* xyzm, const uint32_t* id_of_pos, size_t n, const Cube* cube, uint64_t* key_by_id,

@@ -1349,6 +1349,7 @@ __global__ void __launch_bounds__(kOrderTile) order_light_scatter_kernel(const G
 // only the own shard's slots (the other slots are written by the peers, possibly already)
 __global__ void zero_accum_kernel(float4* accum, const uint32_t* n_sinks, uint32_t cap, uint32_t lo, uint32_t hi,
                                   const uint32_t* shard, uint32_t gs) {
+    G2_PDL_WAIT();  // programmatic dependent launch (launch_pdl)
     if (shard) {
         lo = uint32_t(min(uint64_t(shard[0]) * gs, uint64_t(~0u)));
         hi = uint32_t(min(uint64_t(shard[1]) * gs, uint64_t(~0u)));
@@ -1435,7 +1436,7 @@ void launch_walk_prep(const WalkBuffers& b, uint32_t n_sinks_cap, uint32_t gs, c
                                                               b.self, b.shard);
         G2_CUDA(cudaGetLastError());
     }
-    G2_COUNT(1), zero_accum_kernel<<<zb, 256, 0, s>>>(b.accum, b.n_sinks, n_sinks_cap, zlo, zhi, b.shard, gs);
+    G2_COUNT(1), launch_pdl(zero_accum_kernel, dim3(zb), dim3(256), size_t(0), s, b.accum, b.n_sinks, n_sinks_cap, zlo, zhi, b.shard, gs);
 }
 
 void launch_walk(const TreeView& t, const WalkParams& p, const WalkBuffers& b, bool with_pot, uint32_t n_sinks_cap,
